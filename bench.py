@@ -1,0 +1,362 @@
+#!/usr/bin/env python3
+"""Benchmark of the chained tensor-core fp16 reduction (BASELINE.json metric / configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
+
+One step = one single_pass reduction of n = 2^30 binary16 elements per GPU (uniform[0,1),
+seed 0, m=16, R=1, B=1024: BASELINE configs[1]) with the inputs resident in HBM; at N>1 each
+rank reduces its own contiguous shard (elements [r*n, (r+1)*n) of the same global stream, weak
+scaling) and the N fp32 partials are combined with one NCCL all_reduce.  The input (2 GiB) is
+16x the 126 MB L2, so no flush is needed between steps.
+
+`e2e` repeats the measurement through the reference-facing drop-in call
+tcr_reduce_f32_host (reduce(std::span<const float>) in the reference): fp32 host data in pinned
+memory, host->device copies inside the timed region, 8-byte result read back every step.
+
+`--impl reference` times the reference's own CPU implementation of the path (the reference
+headers compiled as-is into oracle/_ref, parallelised over blocks exactly as
+SURVEY.md Appendix A, all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp16 reduce Gelem/s and % of HBM BW at n=2^30, 1/2/4/8 B200; rel err"
+N_DEFAULT = 1 << 30
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="elements per GPU")
+    ap.add_argument("--R", type=int, default=1)
+    ap.add_argument("--B", type=int, default=1024)
+    ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-comparators", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(n_sample: int, reps: int = 1):
+    """Reference CPU path on all host threads: (Gelem/s, kind, cores, value)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    cores = os.cpu_count() or 1
+    x = O.generate("uniform", 0, n_sample)
+    if O.ref_available():
+        kind = "reference"
+        fn = lambda: O.ref_single_pass_parallel(x, cores, m=16, R=1, B=1024)  # noqa: E731
+    else:
+        kind = "port"
+        fn = lambda: O.single_pass(x, threads=cores, m=16, R=1, B=1024)  # noqa: E731
+    times = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        out = fn()
+        times.append(time.perf_counter() - t)
+    return n_sample / min(times) / 1e9, kind, cores, out.value, times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_sample = 1 << 22
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    cores = os.cpu_count() or 1
+    x = O.generate("uniform", 0, n_sample)
+    kind = "reference" if O.ref_available() else "port"
+
+    def step():
+        if kind == "reference":
+            return O.ref_single_pass_parallel(x, cores, m=16, R=args.R, B=args.B)
+        return O.single_pass(x, threads=cores, m=16, R=args.R, B=args.B)
+
+    for _ in range(args.warmup):
+        step()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t) / args.steps
+    v = n_sample / dt / 1e9
+    line = {"metric": METRIC, "value": v, "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16 in, f32 accumulate (CPU emulation)", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "single_pass m=16 R=%d B=%d uniform[0,1) seed 0" % (args.R, args.B),
+                       "n_per_step": n_sample, "n_target": args.n, "parallelism": "host threads"},
+            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind,
+                             "sample": f"n={n_sample} per step (bounded sample of the n=2^30 workload)"},
+            "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2001_05585_b200 as T
+    from paper_2001_05585_b200 import _capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _capi.load()
+    n = args.n
+    cfg = T.ReductionConfig(m=16, R=args.R, B=args.B, engine=T.Engine(args.engine))
+    c_cfg = cfg.to_c()
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+
+    # input: this rank's shard of the global uniform[0,1) seed-0 stream, generated in place
+    x = T.generate("uniform", 0, n, device=dev, first=rank * n)
+    result = torch.zeros(1, dtype=torch.float32, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    xp, rp, op = C.c_void_p(x.data_ptr()), C.c_void_p(result.data_ptr()), C.c_void_p(ovf.data_ptr())
+
+    kev = []
+
+    def step(timed):
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(c_cfg), rp, op, sp))
+        if timed:
+            e1.record(stream)
+            kev.append((e0, e1))
+        if world > 1:
+            dist.all_reduce(result)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step(False)
+    launches_per_step = lib.tcr_last_launch_count()
+    barrier()
+    with Clocks(local) as clk:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    t = torch.tensor([ms, kms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kms = t.tolist()
+    value = world * n / (ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    achieved = 2.0 * n / (kms * 1e-3) / 1e9  # GB/s, algorithmic bytes = 2 per element
+
+    # accuracy of the last step (result stays on the device until now)
+    got = result.item()
+    exact_local, abs_local = T.exact_sum(x)
+    ex = torch.tensor([exact_local, abs_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ex)
+    exact, absum = ex.tolist()
+    rel_err = abs(got - exact) / abs(exact)
+    ref_val = None
+    gl = os.path.join(ROOT, "tests", "golden", "oracle_large.json")
+    if world == 1 and n == N_DEFAULT and os.path.exists(gl):
+        for rec in json.load(open(gl))["cases"]:
+            if rec["dist"] == "uniform" and rec["seed"] == 0 and rec["n"] == n:
+                ref_val = rec["single_pass"].get(f"m16_R{args.R}_B{args.B}", {}).get("value")
+
+    # comparators (rank 0 view, same input): warp-shuffle CUDA-core kernel, CUB, read probe
+    comparators = None
+    if not args.no_comparators:
+        comparators = {}
+        outc = torch.zeros(2, dtype=torch.float32, device=dev)
+
+        def timeit(fn, reps=10):
+            for _ in range(3):
+                fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            return a.elapsed_time(b) / reps
+
+        cp = C.c_void_p(outc.data_ptr())
+        t_sh = timeit(lambda: _capi.check(lib.tcr_shuffle_f16_async(xp, n, cp, sp)))
+        t_cf = timeit(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 0, cp, sp)))
+        t_ch = timeit(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 1, cp, sp)))
+        t_rd = timeit(lambda: _capi.check(lib.tcr_read_probe_async(xp, 2 * n, sp)))
+        comparators = {
+            "unit": "Gelem/s",
+            "warp_shuffle_fp32": n / t_sh / 1e6,
+            "cub_half_in_float_acc": n / t_cf / 1e6,
+            "cub_half_in_half_acc": n / t_ch / 1e6,
+            "read_probe_GBps": 2 * n / t_rd / 1e6,
+            "speedup_vs_warp_shuffle": t_sh / kms,
+            "speedup_vs_cub_float": t_cf / kms,
+        }
+
+    # end-to-end through the reference-facing drop-in (host fp32 in pinned memory)
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        xh.copy_(T.generate("uniform", 0, n, device=dev, dtype="float32", first=rank * n).cpu())
+        torch.cuda.empty_cache()
+        hp = C.c_void_p(xh.data_ptr())
+        out = _capi.tcr_outcome()
+        e2e_steps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            _capi.check(lib.tcr_reduce_f32_host(hp, n, C.byref(c_cfg), C.byref(out)))
+            if world > 1:
+                r = torch.tensor([out.value], device=dev)
+                dist.all_reduce(r)
+                r.item()
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        s0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        barrier()
+        e_dt = (time.perf_counter() - s0) / e2e_steps
+        et = torch.tensor([e_dt], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_dt = et.item()
+        e2e = {"value": world * n / e_dt / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": 8, "ms_per_step": e_dt * 1e3,
+               "path": "tcr_reduce_f32_host (pinned fp32 host input, pipelined H2D + fused convert/reduce)",
+               "clock": "host wall clock around synchronous calls, max over ranks"}
+        del xh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, kind, cores, val, times = cpu_reference_rate(1 << 26)
+        cpu = {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind,
+               "sample": "uniform[0,1) seed 0, n=2^26 (bounded sample of the 2^30 workload), m=16 R=1 B=1024",
+               "seconds": times[0]}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"single_pass_m16_R{args.R}_B{args.B}_n{n}")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16 in, f32 accumulate (tensor core)", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[1]: single_pass chained-MMA reduction, n=2^30 fp16 per GPU, "
+                                   "m=16 R=%d B=%d, uniform[0,1) seed 0" % (args.R, args.B),
+                       "n_per_gpu": n, "n_total": world * n, "m": 16, "R": args.R, "B": args.B,
+                       "parallelism": f"shard{world}" + ("+nccl_allreduce" if world > 1 else ""),
+                       "l2": "input 2 GiB per GPU > 126 MB L2: no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel_ms": kms, "algorithmic_bytes_per_launch": 2 * n},
+            "hbm_frac_of_8TBs_nominal": achieved / 8000.0,
+            "rel_err_vs_exact": rel_err, "exact_sum": exact, "result": got,
+            "rel_diff_vs_reference_single_pass": (abs(got - ref_val) / abs(exact)) if ref_val else None,
+            "comparators": comparators,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,151 @@
+/*
+ * tcreduce_b200.h -- C ABI of the B200 (sm_100a) chained tensor-core reduction.
+ *
+ * This is the drop-in boundary for the reference's reduction entry points
+ * (/root/reference/proj/include/tcreduce/reduction.hpp).  Plain C: POD structs,
+ * pointers and sizes, no exceptions, no torch types.  Every function returns
+ * TCR_OK (0) or a negative tcr_status; tcr_last_error() gives the message of the
+ * calling thread's last failure.  The C++ header include/tcreduce/reduction.hpp
+ * wraps this ABI back into the reference's exact C++ API (same signatures,
+ * same exception types).
+ *
+ * Library: paper_2001_05585_b200/libtcreduce_b200.so (built by __graft_entry__.build()).
+ */
+#ifndef TCREDUCE_B200_H
+#define TCREDUCE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  INVALID_ARGUMENT <-> std::invalid_argument and OUT_OF_RANGE <->
+ * std::out_of_range in the reference (reduction.hpp:50-56,114,168; fragment.hpp:22-25,65). */
+typedef enum {
+    TCR_OK = 0,
+    TCR_INVALID_ARGUMENT = -1,
+    TCR_OUT_OF_RANGE = -2,
+    TCR_CUDA_ERROR = -3,
+    TCR_NCCL_ERROR = -4,
+    TCR_NOT_SUPPORTED = -5
+} tcr_status;
+
+/* Variant -- reduction.hpp:23 (same numbering). */
+typedef enum {
+    TCR_ORACLE64 = 0,
+    TCR_SHUFFLE32 = 1,
+    TCR_HALF_TREE = 2,
+    TCR_RECURRENCE = 3,
+    TCR_SINGLE_PASS = 4,
+    TCR_SPLIT = 5
+} tcr_variant;
+
+/* AtomicOrder -- reduction.hpp:25. */
+typedef enum { TCR_ASCENDING = 0, TCR_SEEDED_PERMUTATION = 1 } tcr_atomic_order;
+
+/* How block results are combined on the device (no reference counterpart: the
+ * reference serialises its simulated atomics, reduction.hpp:257-268).
+ *   TREE    -- deterministic pairwise tree over block results (default; bit-reproducible,
+ *              independent of launch geometry, more accurate than a serial sum)
+ *   ORDERED -- exactly the reference order: serial fp32 sum, ascending or seeded permutation
+ *   ATOMIC  -- the paper's one atomicAdd per block (order unspecified) */
+typedef enum { TCR_FINALIZE_TREE = 0, TCR_FINALIZE_ORDERED = 1, TCR_FINALIZE_ATOMIC = 2 } tcr_finalize;
+
+/* Kernel family (chosen by measurement; AUTO picks the fastest available for the config). */
+typedef enum { TCR_ENGINE_AUTO = 0, TCR_ENGINE_MMA_SYNC = 1, TCR_ENGINE_TCGEN05 = 2 } tcr_engine;
+
+/* ReductionConfig -- reduction.hpp:39-57 (first seven fields, same meaning and defaults
+ * m=4, R=1, B=128, f=0.5), plus the device-side finalize / engine choice. */
+typedef struct {
+    int32_t variant;      /* tcr_variant */
+    uint32_t m;           /* fragment side, power of two >= 2 */
+    uint32_t R;           /* MMA chain length per warp, >= 1 */
+    uint32_t B;           /* block size in threads, multiple of 32 in [32, 1024] */
+    double f;             /* tensor fraction (split variant), [0, 1] */
+    int32_t atomic_order; /* tcr_atomic_order */
+    uint64_t atomic_seed;
+    int32_t finalize;     /* tcr_finalize */
+    int32_t engine;       /* tcr_engine */
+} tcr_config;
+
+/* ReductionOutcome -- reduction.hpp:59-67.  Counters follow the reference formulas exactly
+ * (they describe the simulated grid, not the B200 launch). */
+typedef struct {
+    double value;
+    int32_t overflow;
+    uint64_t level_count;
+    uint64_t sim_steps;
+    uint64_t mma_count;
+    uint64_t atomic_count;
+    uint64_t shuffle_count;
+} tcr_outcome;
+
+/* Input distributions -- harness.hpp:20 (same numbering). */
+typedef enum { TCR_DIST_NORMAL = 0, TCR_DIST_UNIFORM = 1, TCR_DIST_INTEGERS = 2, TCR_DIST_CONSTANT = 3 } tcr_dist;
+
+/* Defaults of ReductionConfig{} (reduction.hpp:40-46). */
+void tcr_config_init(tcr_config* cfg);
+
+/* ReductionConfig::validate (reduction.hpp:50-56) incl. check_side (fragment.hpp:22-25). */
+int tcr_validate(const tcr_config* cfg);
+
+/* reduce() (reduction.hpp:344-358) over a HOST fp32 array: the drop-in for
+ * `ReductionOutcome reduce(std::span<const float> x, const ReductionConfig& cfg)`.
+ * Host->device copies are pipelined with the fused convert(RNE->binary16)+reduce kernel. */
+int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* cfg, tcr_outcome* out);
+
+/* Same over device-resident data (fp32 converted on load, or binary16 bits).
+ * Synchronous: returns after the result (8 bytes) is back on the host. */
+int tcr_reduce_f32_device(const float* d_x, size_t n, const tcr_config* cfg, tcr_outcome* out,
+                          void* cuda_stream);
+int tcr_reduce_f16_device(const uint16_t* d_x, size_t n, const tcr_config* cfg, tcr_outcome* out,
+                          void* cuda_stream);
+
+/* Asynchronous single_pass over device binary16: enqueues the kernel on `cuda_stream`,
+ * writes the fp32 result to *d_result and ORs the overflow flag into *d_overflow (both device
+ * pointers; *d_overflow is not cleared).  No host synchronisation; CUDA-graph capturable.
+ * This is the per-shard step of the multi-GPU path. */
+int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* cfg, float* d_result,
+                              uint32_t* d_overflow, void* cuda_stream);
+int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* cfg, float* d_result,
+                              uint32_t* d_overflow, void* cuda_stream);
+
+/* Parity hook: per-block fp32 results of single_pass (the reference's block_results,
+ * reduction.hpp:248-255) into d_blocks[tcr_block_count(n, cfg)]. */
+int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* cfg, float* d_blocks,
+                                 void* cuda_stream);
+size_t tcr_block_count(size_t n, const tcr_config* cfg);
+
+/* Counters of the reference formulas for single_pass (reduction.hpp:240-273). */
+int tcr_single_pass_counters(size_t n, const tcr_config* cfg, tcr_outcome* out);
+
+/* Synthetic input on the device: elements [first_index, first_index+n) of
+ * generate(dist, N) (harness.hpp:47-80), bit-identical to the reference generator. */
+int tcr_generate_f16_device(uint16_t* d_x, size_t n, int32_t dist, uint64_t seed, int64_t lo, int64_t hi,
+                            double c, size_t first_index, void* cuda_stream);
+int tcr_generate_f32_device(float* d_x, size_t n, int32_t dist, uint64_t seed, int64_t lo, int64_t hi,
+                            double c, size_t first_index, void* cuda_stream);
+
+/* Exact sum (and sum of |x|) of device binary16 values: the error reference. */
+int tcr_exact_sum_f16_device(const uint16_t* d_x, size_t n, double* sum, double* abs_sum, void* cuda_stream);
+
+/* GPU comparison points: fp32 warp-shuffle kernel and
+ * cub::DeviceReduce::Sum with a float or half accumulator.  Results to *d_result
+ * (float for shuffle / cub-float, binary16 bits in the low half for cub-half). */
+int tcr_shuffle_f16_async(const uint16_t* d_x, size_t n, float* d_result, void* cuda_stream);
+int tcr_cub_sum_f16_async(const uint16_t* d_x, size_t n, int half_accumulator, void* d_result,
+                          void* cuda_stream);
+/* Streaming-read probe over `bytes` of device memory (bandwidth ceiling). */
+int tcr_read_probe_async(const void* d_x, size_t bytes, void* cuda_stream);
+
+/* Number of kernels the last single_pass call on this thread launched (launch accounting). */
+int tcr_last_launch_count(void);
+const char* tcr_last_error(void);
+const char* tcr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCREDUCE_B200_H */

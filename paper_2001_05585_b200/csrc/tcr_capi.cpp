@@ -1,0 +1,472 @@
+// tcr_capi.cpp -- the extern "C" boundary (include/tcreduce_b200.h).
+//
+// Host-side responsibilities only: config validation mirroring the reference
+// (reduction.hpp:50-56, fragment.hpp:22-25), per-(device, stream) workspace,
+// launch geometry, the pipelined host->device drop-in path, and the reference
+// counter formulas.  All arithmetic runs in the sm_100a kernels; there is no
+// CPU fallback: a missing device or kernel is an error, never a host loop.
+#include "tcreduce_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+
+#include "tcr_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define TCR_CUDA(expr)                                                                          \
+    do {                                                                                        \
+        const cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(TCR_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_));   \
+    } while (0)
+
+struct Workspace {
+    float* group_partials = nullptr;
+    size_t gp_cap = 0;
+    float* block_partials = nullptr;
+    size_t bp_cap = 0;
+    uint32_t* order = nullptr;
+    size_t order_cap = 0;
+    // small fixed area: result(float), overflow(u32), ticket(u32), shuffle ticket, exact out[3]
+    unsigned char* fixed = nullptr;
+    void* exact_ws = nullptr;
+    float* shuffle_partials = nullptr;
+    void* cub_temp = nullptr;
+    size_t cub_cap = 0;
+    void* host_pinned = nullptr;  // 64 bytes of result readback
+    // pipelined host path
+    float* ring[2] = {nullptr, nullptr};
+    size_t ring_cap = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+
+    float* result() { return reinterpret_cast<float*>(fixed); }
+    uint32_t* overflow() { return reinterpret_cast<uint32_t*>(fixed + 4); }
+    uint32_t* ticket() { return reinterpret_cast<uint32_t*>(fixed + 8); }
+    uint32_t* sh_ticket() { return reinterpret_cast<uint32_t*>(fixed + 12); }
+    uint32_t* sink() { return reinterpret_cast<uint32_t*>(fixed + 16); }
+    double* exact_out() { return reinterpret_cast<double*>(fixed + 32); }
+};
+
+std::mutex g_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+
+int get_ws(cudaStream_t s, Workspace** out) {
+    int dev = 0;
+    TCR_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& w = g_ws[{dev, s}];
+    if (!w) {
+        w = new Workspace();
+        TCR_CUDA(cudaMalloc(&w->fixed, 256));
+        TCR_CUDA(cudaMemset(w->fixed, 0, 256));
+        TCR_CUDA(cudaMalloc(&w->exact_ws, tcr::exact_ws_bytes()));
+        TCR_CUDA(cudaMalloc(&w->shuffle_partials, sizeof(float) * 8192));
+        TCR_CUDA(cudaMallocHost(&w->host_pinned, 64));
+    }
+    *out = w;
+    return TCR_OK;
+}
+
+template <class T>
+int ensure(T** p, size_t* cap, size_t count, cudaStream_t s) {
+    if (*cap >= count) return TCR_OK;
+    TCR_CUDA(cudaStreamSynchronize(s));
+    if (*p) TCR_CUDA(cudaFree(*p));
+    *p = nullptr;
+    const size_t want = std::max<size_t>(count, 1024);
+    TCR_CUDA(cudaMalloc(reinterpret_cast<void**>(p), want * sizeof(T)));
+    *cap = want;
+    return TCR_OK;
+}
+
+int validate_cfg(const tcr_config* c) {
+    if (!c) return fail(TCR_INVALID_ARGUMENT, "null config");
+    // fragment.hpp:22-25
+    if (c->m < 2 || (c->m & (c->m - 1)) != 0)
+        return fail(TCR_INVALID_ARGUMENT, "fragment side must be a power of two >= 2");
+    // reduction.hpp:52-55
+    if (c->R < 1) return fail(TCR_INVALID_ARGUMENT, "R must be >= 1");
+    if (c->B < 32 || c->B > 1024 || c->B % 32 != 0)
+        return fail(TCR_INVALID_ARGUMENT, "B must be a multiple of 32 in [32, 1024]");
+    if (c->f < 0.0 || c->f > 1.0) return fail(TCR_INVALID_ARGUMENT, "f must be in [0, 1]");
+    if (c->finalize < TCR_FINALIZE_TREE || c->finalize > TCR_FINALIZE_ATOMIC)
+        return fail(TCR_INVALID_ARGUMENT, "unknown finalize mode");
+    if (c->atomic_order != TCR_ASCENDING && c->atomic_order != TCR_SEEDED_PERMUTATION)
+        return fail(TCR_INVALID_ARGUMENT, "unknown atomic order");
+    return TCR_OK;
+}
+
+int check_supported(const tcr_config* c) {
+    if (c->m != 16)
+        return fail(TCR_NOT_SUPPORTED, "single_pass on B200 currently implements m = 16 (the hardware fragment)");
+    if (c->engine == TCR_ENGINE_TCGEN05) return fail(TCR_NOT_SUPPORTED, "tcgen05 engine not built yet");
+    return TCR_OK;
+}
+
+uint64_t next_pow2(uint64_t v) {
+    uint64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+void counters(uint64_t n, const tcr_config* c, tcr_outcome* o) {
+    // reduction.hpp:240-242 and :270-273, :95-96, :177, :182, :267
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    const uint64_t P = next_pow2(g.W);
+    uint64_t lv = 0;
+    for (uint64_t len = P; len > 1; len /= 2) ++lv;
+    o->level_count = 1;
+    o->sim_steps = 2ull * c->R + 2 + lv + g.n_blocks;
+    o->mma_count = g.n_blocks * g.W * (c->R + 1ull);
+    o->atomic_count = g.n_blocks;
+    o->shuffle_count = g.n_blocks * (P - 1);
+}
+
+// Enqueue single_pass over groups [g0, g1) of a (possibly chunked) input.
+int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c, bool f32, float* d_result,
+               uint32_t* d_overflow, float* d_blocks, Workspace* w, cudaStream_t s, uint64_t g0, uint64_t g1,
+               bool finalize_here) {
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    tcr::SpParams p{};
+    p.x = static_cast<const char*>(x) - x_offset * (f32 ? 4 : 2);
+    p.n = n;
+    p.R = c->R;
+    p.W = g.W;
+    p.G = g.G;
+    p.chunk_elems = g.chunk_elems;
+    p.n_blocks = g.n_blocks;
+    p.n_groups = g.n_groups;
+    p.group_begin = g0;
+    p.group_end = g1;
+    int rc = ensure(&w->group_partials, &w->gp_cap, g.n_groups, s);
+    if (rc) return rc;
+    p.group_partials = w->group_partials;
+    p.block_partials = d_blocks;
+    if (c->finalize == TCR_FINALIZE_ORDERED && !d_blocks) {
+        rc = ensure(&w->block_partials, &w->bp_cap, g.n_blocks, s);
+        if (rc) return rc;
+        p.block_partials = w->block_partials;
+        if (c->atomic_order == TCR_SEEDED_PERMUTATION) {
+            rc = ensure(&w->order, &w->order_cap, g.n_blocks, s);
+            if (rc) return rc;
+        }
+    }
+    p.order_scratch = w->order;
+    p.result = d_result;
+    p.overflow = d_overflow;
+    p.ticket = w->ticket();
+    p.finalize = finalize_here ? c->finalize : tcr::kFinNone;
+    if (c->finalize == TCR_FINALIZE_ATOMIC) p.finalize = tcr::kFinAtomic;
+    p.atomic_order = c->atomic_order;
+    p.atomic_seed = c->atomic_seed;
+    if (c->finalize == TCR_FINALIZE_ATOMIC && g0 == 0) {
+        TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
+        ++g_launches;
+    }
+    const uint64_t groups = g1 - g0;
+    const int maxg = tcr::single_pass_m16_max_grid(f32);
+    const int grid = int(std::min<uint64_t>(groups, uint64_t(maxg)));
+    TCR_CUDA(tcr::launch_single_pass_m16(p, f32, grid, s));
+    ++g_launches;
+    return TCR_OK;
+}
+
+int enqueue_finalize(uint64_t n, const tcr_config* c, float* d_result, Workspace* w, cudaStream_t s) {
+    if (c->finalize == TCR_FINALIZE_ATOMIC) return TCR_OK;
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    tcr::SpParams p{};
+    p.n = n;
+    p.R = c->R;
+    p.W = g.W;
+    p.G = g.G;
+    p.n_blocks = g.n_blocks;
+    p.n_groups = g.n_groups;
+    p.group_partials = w->group_partials;
+    p.block_partials = w->block_partials;
+    p.order_scratch = w->order;
+    p.result = d_result;
+    p.finalize = c->finalize;
+    p.atomic_order = c->atomic_order;
+    p.atomic_seed = c->atomic_seed;
+    TCR_CUDA(tcr::launch_finalize(p, s));
+    ++g_launches;
+    return TCR_OK;
+}
+
+int sp_async(const void* d_x, size_t n, const tcr_config* c, bool f32, float* d_result, uint32_t* d_overflow,
+             cudaStream_t s) {
+    g_launches = 0;
+    if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");  // reduction.hpp:282
+    int rc = validate_cfg(c);
+    if (rc) return rc;
+    rc = check_supported(c);
+    if (rc) return rc;
+    if (!d_x || !d_result || !d_overflow) return fail(TCR_INVALID_ARGUMENT, "null device pointer");
+    if (reinterpret_cast<uintptr_t>(d_x) % (f32 ? 32 : 16) != 0)
+        return fail(TCR_INVALID_ARGUMENT, "device input must be 16-byte (binary16) / 32-byte (fp32) aligned");
+    Workspace* w = nullptr;
+    rc = get_ws(s, &w);
+    if (rc) return rc;
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    return enqueue_sp(d_x, 0, n, c, f32, d_result, d_overflow, nullptr, w, s, 0, g.n_groups, true);
+}
+
+int read_result(Workspace* w, cudaStream_t s, float* value, uint32_t* ovf) {
+    TCR_CUDA(cudaMemcpyAsync(w->host_pinned, w->fixed, 8, cudaMemcpyDeviceToHost, s));
+    TCR_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(value, w->host_pinned, 4);
+    std::memcpy(ovf, static_cast<char*>(w->host_pinned) + 4, 4);
+    return TCR_OK;
+}
+
+int reduce_device(const void* d_x, size_t n, const tcr_config* c, tcr_outcome* out, bool f32, cudaStream_t s) {
+    if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
+    std::memset(out, 0, sizeof *out);
+    if (!c) return fail(TCR_INVALID_ARGUMENT, "null config");
+    if (c->variant != TCR_SINGLE_PASS)
+        return fail(TCR_NOT_SUPPORTED, "only the single_pass variant runs on the B200 path so far");
+    Workspace* w = nullptr;
+    int rc = get_ws(s, &w);
+    if (rc) return rc;
+    TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+    rc = sp_async(d_x, n, c, f32, w->result(), w->overflow(), s);
+    if (rc) return rc;
+    ++g_launches;  // memset
+    float v;
+    uint32_t o;
+    rc = read_result(w, s, &v, &o);
+    if (rc) return rc;
+    out->value = v;
+    out->overflow = o ? 1 : 0;
+    counters(n, c, out);
+    return TCR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tcr_config_init(tcr_config* c) {
+    std::memset(c, 0, sizeof *c);
+    c->variant = TCR_SINGLE_PASS;
+    c->m = 4;
+    c->R = 1;
+    c->B = 128;
+    c->f = 0.5;
+    c->atomic_order = TCR_ASCENDING;
+    c->atomic_seed = 0;
+    c->finalize = TCR_FINALIZE_TREE;
+    c->engine = TCR_ENGINE_AUTO;
+}
+
+int tcr_validate(const tcr_config* c) { return validate_cfg(c); }
+
+const char* tcr_last_error(void) { return g_err.c_str(); }
+const char* tcr_version(void) { return "tcreduce-b200 0.1 (sm_100a)"; }
+int tcr_last_launch_count(void) { return g_launches; }
+
+size_t tcr_block_count(size_t n, const tcr_config* c) {
+    if (!c || validate_cfg(c)) return 0;
+    return tcr::make_geometry(n, c->m, c->R, c->B).n_blocks;
+}
+
+int tcr_single_pass_counters(size_t n, const tcr_config* c, tcr_outcome* out) {
+    int rc = validate_cfg(c);
+    if (rc) return rc;
+    std::memset(out, 0, sizeof *out);
+    counters(n, c, out);
+    return TCR_OK;
+}
+
+int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_result,
+                              uint32_t* d_overflow, void* stream) {
+    return sp_async(d_x, n, c, false, d_result, d_overflow, static_cast<cudaStream_t>(stream));
+}
+
+int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* c, float* d_result,
+                              uint32_t* d_overflow, void* stream) {
+    return sp_async(d_x, n, c, true, d_result, d_overflow, static_cast<cudaStream_t>(stream));
+}
+
+int tcr_reduce_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
+    return reduce_device(d_x, n, c, out, false, static_cast<cudaStream_t>(stream));
+}
+
+int tcr_reduce_f32_device(const float* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
+    return reduce_device(d_x, n, c, out, true, static_cast<cudaStream_t>(stream));
+}
+
+int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_blocks,
+                                 void* stream) {
+    g_launches = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+    int rc = validate_cfg(c);
+    if (rc) return rc;
+    rc = check_supported(c);
+    if (rc) return rc;
+    Workspace* w = nullptr;
+    rc = get_ws(s, &w);
+    if (rc) return rc;
+    tcr_config cc = *c;
+    cc.finalize = TCR_FINALIZE_TREE;
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    return enqueue_sp(d_x, 0, n, &cc, false, w->result(), w->overflow(), d_blocks, w, s, 0, g.n_groups, true);
+}
+
+int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outcome* out) {
+    // Drop-in for reduce(std::span<const float>, cfg): pipelined H2D in group-aligned chunks on
+    // a copy stream, fused convert+reduce per chunk on the compute stream, one finaliser.
+    g_launches = 0;
+    if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
+    std::memset(out, 0, sizeof *out);
+    if (!c) return fail(TCR_INVALID_ARGUMENT, "null config");
+    if (c->variant != TCR_SINGLE_PASS)
+        return fail(TCR_NOT_SUPPORTED, "only the single_pass variant runs on the B200 path so far");
+    if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+    if (!x) return fail(TCR_INVALID_ARGUMENT, "null input");
+    int rc = validate_cfg(c);
+    if (rc) return rc;
+    rc = check_supported(c);
+    if (rc) return rc;
+    cudaStream_t s = nullptr;  // legacy default stream of the calling thread's device
+    Workspace* w = nullptr;
+    rc = get_ws(s, &w);
+    if (rc) return rc;
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    // chunk: whole groups, ~32 Mi elements (128 MiB of fp32)
+    const uint64_t groups_per_chunk = std::max<uint64_t>(1, (32ull << 20) / g.group_elems);
+    const uint64_t chunk_elems = groups_per_chunk * g.group_elems;
+    const uint64_t n_chunks = (g.n_groups + groups_per_chunk - 1) / groups_per_chunk;
+    const uint64_t ring_elems = std::min<uint64_t>(chunk_elems, n);
+    if (w->ring_cap < ring_elems) {
+        TCR_CUDA(cudaDeviceSynchronize());
+        for (auto& r : w->ring)
+            if (r) TCR_CUDA(cudaFree(r));
+        for (auto& r : w->ring) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(float)));
+        w->ring_cap = ring_elems;
+    }
+    if (!w->copy_stream) {
+        TCR_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            TCR_CUDA(cudaEventCreateWithFlags(&w->copied[i], cudaEventDisableTiming));
+            TCR_CUDA(cudaEventCreateWithFlags(&w->consumed[i], cudaEventDisableTiming));
+        }
+    }
+    tcr_config cc = *c;
+    TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+    for (uint64_t k = 0; k < n_chunks; ++k) {
+        const int slot = int(k & 1);
+        const uint64_t e0 = k * chunk_elems;
+        const uint64_t e1 = std::min<uint64_t>(n, e0 + chunk_elems);
+        const uint64_t g0 = k * groups_per_chunk;
+        const uint64_t g1 = std::min<uint64_t>(g.n_groups, g0 + groups_per_chunk);
+        if (k >= 2) TCR_CUDA(cudaStreamWaitEvent(w->copy_stream, w->consumed[slot], 0));
+        TCR_CUDA(cudaMemcpyAsync(w->ring[slot], x + e0, (e1 - e0) * sizeof(float), cudaMemcpyHostToDevice,
+                                 w->copy_stream));
+        TCR_CUDA(cudaEventRecord(w->copied[slot], w->copy_stream));
+        TCR_CUDA(cudaStreamWaitEvent(s, w->copied[slot], 0));
+        const bool last = (k + 1 == n_chunks);
+        // single chunk: finalise in the same launch; otherwise one finaliser at the end
+        rc = enqueue_sp(w->ring[slot], e0, n, &cc, true, w->result(), w->overflow(), nullptr, w, s, g0, g1,
+                        last && n_chunks == 1);
+        if (rc) return rc;
+        TCR_CUDA(cudaEventRecord(w->consumed[slot], s));
+    }
+    if (n_chunks > 1) {
+        rc = enqueue_finalize(n, &cc, w->result(), w, s);
+        if (rc) return rc;
+    }
+    float v;
+    uint32_t o;
+    rc = read_result(w, s, &v, &o);
+    if (rc) return rc;
+    out->value = v;
+    out->overflow = o ? 1 : 0;
+    counters(n, c, out);
+    return TCR_OK;
+}
+
+int tcr_generate_f16_device(uint16_t* d_x, size_t n, int32_t dist, uint64_t seed, int64_t lo, int64_t hi,
+                            double cval, size_t first, void* stream) {
+    if (dist < 0 || dist > 3) return fail(TCR_INVALID_ARGUMENT, "unknown distribution");
+    if (dist == TCR_DIST_INTEGERS && hi < lo) return fail(TCR_INVALID_ARGUMENT, "integers: hi < lo");
+    TCR_CUDA(tcr::launch_generate(d_x, true, n, dist, seed, lo, hi, cval, first, static_cast<cudaStream_t>(stream)));
+    return TCR_OK;
+}
+
+int tcr_generate_f32_device(float* d_x, size_t n, int32_t dist, uint64_t seed, int64_t lo, int64_t hi,
+                            double cval, size_t first, void* stream) {
+    if (dist < 0 || dist > 3) return fail(TCR_INVALID_ARGUMENT, "unknown distribution");
+    if (dist == TCR_DIST_INTEGERS && hi < lo) return fail(TCR_INVALID_ARGUMENT, "integers: hi < lo");
+    TCR_CUDA(tcr::launch_generate(d_x, false, n, dist, seed, lo, hi, cval, first, static_cast<cudaStream_t>(stream)));
+    return TCR_OK;
+}
+
+int tcr_exact_sum_f16_device(const uint16_t* d_x, size_t n, double* sum, double* abs_sum, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (reinterpret_cast<uintptr_t>(d_x) % 16) return fail(TCR_INVALID_ARGUMENT, "input must be 16-byte aligned");
+    Workspace* w = nullptr;
+    int rc = get_ws(s, &w);
+    if (rc) return rc;
+    TCR_CUDA(tcr::launch_exact_sum_f16(d_x, n, w->exact_ws, w->exact_out(), s));
+    double h[3];
+    TCR_CUDA(cudaMemcpyAsync(h, w->exact_out(), sizeof h, cudaMemcpyDeviceToHost, s));
+    TCR_CUDA(cudaStreamSynchronize(s));
+    *sum = h[0];
+    *abs_sum = h[1];
+    return TCR_OK;
+}
+
+int tcr_shuffle_f16_async(const uint16_t* d_x, size_t n, float* d_result, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+    if (reinterpret_cast<uintptr_t>(d_x) % 16) return fail(TCR_INVALID_ARGUMENT, "input must be 16-byte aligned");
+    Workspace* w = nullptr;
+    int rc = get_ws(s, &w);
+    if (rc) return rc;
+    const int grid = std::min(tcr::shuffle_max_grid(), 8192);
+    TCR_CUDA(tcr::launch_shuffle_f16(d_x, n, w->shuffle_partials, w->sh_ticket(), d_result, grid, s));
+    g_launches = 1;
+    return TCR_OK;
+}
+
+int tcr_cub_sum_f16_async(const uint16_t* d_x, size_t n, int half_acc, void* d_result, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Workspace* w = nullptr;
+    int rc = get_ws(s, &w);
+    if (rc) return rc;
+    const size_t need = tcr::cub_temp_bytes(n, half_acc != 0);
+    rc = ensure(reinterpret_cast<unsigned char**>(&w->cub_temp), &w->cub_cap, need, s);
+    if (rc) return rc;
+    TCR_CUDA(tcr::cub_sum_f16(d_x, n, d_result, half_acc != 0, w->cub_temp, w->cub_cap, s));
+    return TCR_OK;
+}
+
+int tcr_read_probe_async(const void* d_x, size_t bytes, void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Workspace* w = nullptr;
+    int rc = get_ws(s, &w);
+    if (rc) return rc;
+    TCR_CUDA(tcr::launch_read_probe(d_x, bytes, w->sink(), tcr::sm_count() * 8, s));
+    return TCR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// tcr_kernels.h -- host-visible launch interface of the tcreduce sm_100a kernels.
+// Internal to libtcreduce_b200.so; the public surface is include/tcreduce_b200.h.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tcr {
+
+enum Finalize : int32_t {
+    kFinNone = -1,     // leave group partials for a later finalize launch
+    kFinTree = 0,      // deterministic pairwise tree over block results (default)
+    kFinOrdered = 1,   // reference order: serial fp32 sum, ascending or seeded permutation
+    kFinAtomic = 2,    // paper's atomicAdd per block (non-deterministic order)
+};
+
+// Group-size target: a CTA reduces G logical blocks (G a power of two) of at least this many
+// elements, so the deterministic tree is a fixed function of (n, m, R, B) only.
+constexpr uint64_t kGroupElemsTarget = 1ull << 16;
+constexpr int kSpWarps = 8;            // warps per CTA of the single-pass kernel
+constexpr int kSpThreads = kSpWarps * 32;
+constexpr int kMaxChunksPerGroup = 256;
+
+struct SpGeometry {
+    uint32_t m, R, W;          // fragment side, chain length, warps per logical block (B/32)
+    uint64_t n;                // elements
+    uint64_t chunk_elems;      // R*m*m            (a warp's chunk, reduction.hpp:240)
+    uint64_t block_elems;      // chunk_elems*W    (a logical block's chunk, :241)
+    uint64_t n_blocks;         // max(1, ceil(n / block_elems))  (:242)
+    uint32_t G;                // logical blocks per group (power of two)
+    uint64_t group_elems;      // G*block_elems
+    uint64_t n_groups;         // ceil(n_blocks / G)
+};
+
+SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B);
+
+struct SpParams {
+    const void* x;
+    uint64_t n;
+    uint32_t R, W, G;
+    uint64_t chunk_elems, n_blocks, n_groups;
+    uint64_t group_begin, group_end;   // groups covered by this launch
+    float* group_partials;             // [n_groups]   (tree finaliser input)
+    float* block_partials;             // [n_blocks] or null (ordered finaliser / parity tests)
+    float* result;                     // device scalar
+    uint32_t* overflow;                // device flag (OR)
+    uint32_t* ticket;                  // last-CTA-done counter, returns to 0
+    uint32_t* order_scratch;           // [n_blocks] for the seeded-permutation finaliser
+    int32_t finalize;
+    int32_t atomic_order;
+    uint64_t atomic_seed;
+};
+
+// Single-pass chained-MMA reduction, m = 16, binary16 (or fp32 convert-on-load) input.
+cudaError_t launch_single_pass_m16(const SpParams& p, bool f32_input, int grid, cudaStream_t s);
+cudaError_t launch_finalize(const SpParams& p, cudaStream_t s);
+int single_pass_m16_max_grid(bool f32_input);
+
+// Input generation (harness.hpp:47-80 with SplitMix64 jump-ahead), binary16 or fp32 output.
+cudaError_t launch_generate(void* out, bool f16_out, uint64_t count, int kind, uint64_t seed,
+                            int64_t lo, int64_t hi, double c, uint64_t first, cudaStream_t s);
+
+// Exact fixed-point sum of binary16 values (+ sum |x|, non-finite count).  ws: >= exact_ws_bytes().
+size_t exact_ws_bytes();
+cudaError_t launch_exact_sum_f16(const uint16_t* x, uint64_t n, void* ws, double* d_out3,
+                                 cudaStream_t s);
+
+// CUDA-core fp32 warp-shuffle reduction of binary16 input (the paper's baseline).
+cudaError_t launch_shuffle_f16(const uint16_t* x, uint64_t n, float* partials, uint32_t* ticket,
+                               float* result, int grid, cudaStream_t s);
+int shuffle_max_grid();
+
+// Pure streaming-read probe: the achievable read bandwidth ceiling.
+cudaError_t launch_read_probe(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s);
+
+// CUB DeviceReduce::Sum comparators.
+size_t cub_temp_bytes(uint64_t n, bool half_out);
+cudaError_t cub_sum_f16(const uint16_t* x, uint64_t n, void* out, bool half_out, void* temp,
+                        size_t temp_bytes, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace tcr

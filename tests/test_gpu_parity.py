@@ -1,0 +1,289 @@
+"""GPU parity tests: the sm_100a kernels (through the C ABI) against the oracle.
+
+Tolerances:
+  * integer inputs: bit-exact equality with oracle64 / the reference single_pass;
+  * block results vs the oracle's (the reference's block_results): bit-exact on integer
+    data; on float data only the tensor core's internal fp32 summation order can differ,
+    which the binary16 rounding of C_R almost always absorbs -- |diff| <= 2^-20 relative
+    per block, and the fraction of bit-identical blocks is reported;
+  * uniform: |gpu - exact| / |exact| <= 1e-5 and |gpu - ref_single_pass| / |exact| <= 2e-5;
+  * normal: |gpu - exact| / sum|x| <= 1e-6.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2001_05585_b200 as T  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+DEV = "cuda:0"
+
+
+def cfg16(R=1, B=1024, **kw):
+    return T.ReductionConfig(m=16, R=R, B=B, **kw)
+
+
+def to_dev_f16(h: np.ndarray):
+    return torch.from_numpy(h.view(np.int16).copy()).to(DEV).view(torch.float16)
+
+
+@pytest.fixture(scope="module")
+def ints(oracle):
+    return {s: oracle.generate("integers", s, 1 << 20) for s in (0, 1, 2)}
+
+
+# --------------------------------------------------------------------------- generator / exact sum
+
+@pytest.mark.parametrize("dist,seed,lo,hi", [("uniform", 0, 0, 9), ("normal", 1, 0, 9), ("normal", 17, 0, 9),
+                                             ("integers", 4, -3, 7), ("constant", 0, 0, 9)])
+def test_generator_bit_exact(oracle, dist, seed, lo, hi):
+    n, first = (1 << 20) + 13, 12345
+    g = T.generate(dist, seed, n, lo=lo, hi=hi, c=2.5, first=first)
+    ref = oracle.generate_f16(dist, seed, n, lo=lo, hi=hi, c=2.5, first=first)
+    got = g.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, ref), int((got != ref).sum())
+    g32 = T.generate(dist, seed, 4096, dtype="float32", lo=lo, hi=hi, c=2.5)
+    r32 = oracle.generate(dist, seed, 4096, lo=lo, hi=hi, c=2.5)
+    assert np.array_equal(g32.cpu().numpy().view(np.uint32), r32.view(np.uint32))
+
+
+def test_exact_sum_matches_oracle(oracle):
+    for dist, seed in (("uniform", 0), ("normal", 1)):
+        h = oracle.generate_f16(dist, seed, (1 << 22) + 5)
+        s, a = T.exact_sum(to_dev_f16(h))
+        es, ea = oracle.exact_sum_f16(h)
+        assert s == es and a == ea
+
+
+# --------------------------------------------------------------------------- integers: bit-exact
+
+@pytest.mark.parametrize("fin", [T.Finalize.tree, T.Finalize.ordered, T.Finalize.atomic])
+def test_integer_sweep_bit_exact(ints, oracle, fin):
+    """all 25 (B, R) at m=16 give exactly 4715354 / 4716649 / 4718742."""
+    expect = {0: 4715354.0, 1: 4716649.0, 2: 4718742.0}
+    for seed, x in ints.items():
+        xd = torch.from_numpy(x).to(DEV).half()
+        for B in (32, 128, 256, 512, 1024):
+            for R in (1, 2, 3, 4, 5):
+                out = T.reduce(xd, cfg16(R=R, B=B, finalize=fin))
+                assert out.value == expect[seed], (seed, B, R, out.value)
+                assert not out.overflow
+
+
+def test_integer_block_results_bit_exact(ints, oracle):
+    for R, B in ((1, 1024), (4, 128), (3, 96), (5, 32)):
+        x = ints[1]
+        _, ref_blocks = oracle.single_pass(x, threads=8, want_blocks=True, m=16, R=R, B=B)
+        got = T.block_results(torch.from_numpy(x).to(DEV).half(), cfg16(R=R, B=B)).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), ref_blocks.view(np.uint32))
+
+
+def test_reference_unit_inputs():  # test_reduction.cpp:119-128 at m=16
+    assert T.reduce(torch.ones(2048, device=DEV, dtype=torch.float16), cfg16(R=4, B=128)).value == 2048.0
+    seq = torch.arange(1, 17, device=DEV, dtype=torch.float32).half()
+    o = T.reduce(seq, cfg16(R=1, B=32))
+    assert o.value == 136.0 and o.mma_count == 2 and o.atomic_count == 1
+    assert T.reduce(torch.ones(1 << 26, device=DEV, dtype=torch.float16), cfg16()).value == 67108864.0
+
+
+# --------------------------------------------------------------------------- float data vs the oracle
+
+def _block_parity(oracle, h, R, B):
+    _, ref_blocks = oracle.single_pass(h, threads=8, want_blocks=True, m=16, R=R, B=B)
+    got = T.block_results(to_dev_f16(h), cfg16(R=R, B=B)).cpu().numpy()
+    same = got.view(np.uint32) == ref_blocks.view(np.uint32)
+    rel = np.abs(got.astype(np.float64) - ref_blocks) / np.maximum(np.abs(ref_blocks), 1e-30)
+    return same.mean(), rel.max(), ref_blocks, got
+
+
+@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1)])
+@pytest.mark.parametrize("R,B", [(1, 1024), (4, 128), (2, 32), (5, 96)])
+def test_block_results_vs_oracle(oracle, dist, seed, R, B):
+    h = oracle.generate_f16(dist, seed, (1 << 20) + 777)
+    frac, rel, _, _ = _block_parity(oracle, h, R, B)
+    print(f"\n{dist} R={R} B={B}: bit-identical blocks {frac:.6f}, max rel diff {rel:.3e}")
+    assert rel <= 2.0 ** -20
+    assert frac >= 0.99
+
+
+@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1), ("uniform", 11)])
+def test_ordered_finalize_matches_reference_value(oracle, dist, seed):
+    """finalize=ordered reproduces the reference's serial ascending block accumulation."""
+    n = (1 << 20) + 12345
+    h = oracle.generate_f16(dist, seed, n)
+    xd = to_dev_f16(h)
+    for R, B in ((1, 1024), (4, 128)):
+        ref = oracle.single_pass(h, threads=8, m=16, R=R, B=B)
+        got = T.reduce(xd, cfg16(R=R, B=B, finalize=T.Finalize.ordered))
+        frac, _, rb, gb = _block_parity(oracle, h, R, B)
+        if frac == 1.0:
+            assert got.value == ref.value
+        exact, absum = oracle.exact_sum_f16(h)
+        assert abs(got.value - ref.value) <= 2e-5 * max(abs(exact), 1e-3 * absum)
+        # seeded permutation order (reduction.hpp:259-263)
+        refp = oracle.single_pass(h, threads=8, m=16, R=R, B=B, atomic_order=1, atomic_seed=3)
+        gotp = T.reduce(xd, cfg16(R=R, B=B, finalize=T.Finalize.ordered, atomic_order=T.AtomicOrder.seeded_permutation,
+                                  atomic_seed=3))
+        if frac == 1.0:
+            assert gotp.value == refp.value
+
+
+@pytest.mark.parametrize("fin", [T.Finalize.tree, T.Finalize.atomic])
+def test_tree_and_atomic_within_tolerance(oracle, fin):
+    for dist, seed in (("uniform", 0), ("normal", 1), ("normal", 2)):
+        h = oracle.generate_f16(dist, seed, 1 << 22)
+        exact, absum = oracle.exact_sum_f16(h)
+        ref = oracle.single_pass(h, threads=8, m=16, R=1, B=1024)
+        got = T.reduce(to_dev_f16(h), cfg16(finalize=fin))
+        if dist == "uniform":
+            assert abs(got.value - exact) / abs(exact) <= 1e-5
+            assert abs(got.value - ref.value) / abs(exact) <= 2e-5
+        else:
+            assert abs(got.value - exact) / absum <= 1e-6
+
+
+def test_tree_is_deterministic_and_geometry_independent(oracle):
+    h = oracle.generate_f16("normal", 2, (1 << 22) + 3)
+    xd = to_dev_f16(h)
+    vals = {T.reduce(xd, cfg16(R=2, B=256)).value for _ in range(5)}
+    assert len(vals) == 1
+
+
+# --------------------------------------------------------------------------- edges
+
+@pytest.mark.parametrize("n", [1, 7, 8, 15, 16, 255, 256, 257, 8191, 8192, 8193, 65536 * 3 + 5])
+def test_ragged_sizes(oracle, n):
+    h = oracle.generate_f16("integers", 5, n)
+    x = h.view(np.float16).astype(np.float32)
+    for R, B in ((1, 1024), (3, 64)):
+        got = T.reduce(to_dev_f16(h), cfg16(R=R, B=B, finalize=T.Finalize.ordered))
+        assert got.value == oracle.oracle64(x)
+        assert got.atomic_count == max(1, -(-n // (R * 256 * (B // 32))))
+
+
+def test_zero_padding_neutrality(oracle):  # test_reduction.cpp:178-189
+    h = oracle.generate_f16("normal", 17, 5000)
+    padded = np.concatenate([h, np.zeros(333, np.uint16)])
+    for fin in (T.Finalize.tree, T.Finalize.ordered):
+        a = T.reduce(to_dev_f16(h), cfg16(R=4, B=128, finalize=fin)).value
+        b = T.reduce(to_dev_f16(padded), cfg16(R=4, B=128, finalize=fin)).value
+        assert a == b
+
+
+def test_overflow_detection(oracle):
+    # a column sum past 65504 overflows C_R -> binary16 (reduction.hpp:179-181)
+    x = torch.full((1 << 16,), 8192.0, device=DEV, dtype=torch.float16)
+    o = T.reduce(x, cfg16(R=1, B=128))
+    g = json.load(open(os.path.join(GOLDEN, "reference_small.json")))
+    exp = [c for c in g["cases"] if c["tag"] == "overflow_const_8192"][0]["outcome"]
+    assert o.overflow and exp["overflow"] and math.isinf(o.value) and math.isinf(exp["value"])
+    # 4095 per column at R=1 is fine: 16 * 4095 = 65520 rounds to inf, 16 * 4094 = 65504 does not
+    assert not T.reduce(torch.full((256,), 4094.0, device=DEV, dtype=torch.float16), cfg16(B=32)).overflow
+    assert T.reduce(torch.full((256,), 4095.0, device=DEV, dtype=torch.float16), cfg16(B=32)).overflow
+    nan = torch.zeros(4096, device=DEV, dtype=torch.float16)
+    nan[77] = float("nan")
+    o = T.reduce(nan, cfg16(B=128))
+    assert o.overflow and math.isnan(o.value)
+
+
+def test_fp32_device_and_host_paths(oracle):
+    """Convert-on-load (fragment.hpp:68 from_single in-kernel) equals staging through binary16."""
+    for dist, seed in (("uniform", 0), ("normal", 1)):
+        x = oracle.generate(dist, seed, (1 << 21) + 99)
+        h = np.array(x.astype(np.float16).view(np.uint16))
+        a = T.reduce(to_dev_f16(h), cfg16(R=2, B=512))
+        b = T.reduce(torch.from_numpy(x).to(DEV), cfg16(R=2, B=512))
+        c = T.reduce(x, cfg16(R=2, B=512))  # host fp32 drop-in path
+        assert a.value == b.value == c.value
+        assert a.atomic_count == c.atomic_count
+
+
+def test_host_path_multi_chunk(oracle):
+    x = oracle.generate("uniform", 0, (1 << 26) + 1000)  # > 1 pipelined chunk
+    h = np.array(x.astype(np.float16).view(np.uint16))
+    a = T.reduce(x, cfg16())
+    b = T.reduce(to_dev_f16(h), cfg16())
+    assert a.value == b.value
+    a = T.reduce(x, cfg16(finalize=T.Finalize.ordered))
+    ref = oracle.single_pass(h, threads=8, m=16, R=1, B=1024)
+    assert abs(a.value - ref.value) / abs(ref.value) < 1e-6
+
+
+def test_errors():
+    x = torch.ones(1024, device=DEV, dtype=torch.float16)
+    with pytest.raises(ValueError):
+        T.reduce(x, cfg16(B=48))
+    with pytest.raises(ValueError):
+        T.reduce(x[:0], cfg16())
+    with pytest.raises(ValueError):
+        T.reduce(x, T.ReductionConfig(m=16, R=0))
+
+
+# --------------------------------------------------------------------------- comparators
+
+def test_comparators_within_tolerance(oracle):
+    import ctypes as C
+    from paper_2001_05585_b200 import _capi
+    h = oracle.generate_f16("uniform", 0, (1 << 24) + 9)
+    exact, _ = oracle.exact_sum_f16(h)
+    xd = to_dev_f16(h)
+    out = torch.zeros(2, device=DEV, dtype=torch.float32)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    lib = _capi.load()
+    _capi.check(lib.tcr_shuffle_f16_async(C.c_void_p(xd.data_ptr()), xd.numel(), C.c_void_p(out.data_ptr()), s))
+    _capi.check(lib.tcr_cub_sum_f16_async(C.c_void_p(xd.data_ptr()), xd.numel(), 0,
+                                          C.c_void_p(out[1:].data_ptr()), s))
+    torch.cuda.synchronize()
+    sh, cub = out.cpu().tolist()
+    assert abs(sh - exact) / exact < 1e-5
+    assert abs(cub - exact) / exact < 1e-5
+    half = torch.zeros(1, device=DEV, dtype=torch.float16)
+    _capi.check(lib.tcr_cub_sum_f16_async(C.c_void_p(xd.data_ptr()), xd.numel(), 1, C.c_void_p(half.data_ptr()), s))
+    torch.cuda.synchronize()
+    assert math.isinf(half.item())  # CUB-half overflows on uniform input
+
+
+# --------------------------------------------------------------------------- full size (BASELINE cfg2/cfg4)
+
+def _large():
+    p = os.path.join(GOLDEN, "oracle_large.json")
+    if not os.path.exists(p):
+        pytest.skip("oracle_large.json not generated")
+    return json.load(open(p))
+
+
+@pytest.mark.parametrize("lgn", [26, 28, 30])
+@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1)])
+def test_full_size_against_golden(dist, seed, lgn):
+    recs = [r for r in _large()["cases"] if r["dist"] == dist and r["seed"] == seed and r["n"] == 1 << lgn]
+    if not recs:
+        pytest.skip("no golden")
+    rec = recs[0]
+    x = T.generate(dist, seed, rec["n"])
+    s, a = T.exact_sum(x)
+    assert s == rec["exact_f16_sum"] and a == rec["abs_f16_sum"]  # generator is bit-exact at full size
+    for key, ref in rec["single_pass"].items():
+        R, B = int(key.split("_")[1][1:]), int(key.split("_")[2][1:])
+        for fin in (T.Finalize.tree, T.Finalize.ordered):
+            got = T.reduce(x, cfg16(R=R, B=B, finalize=fin))
+            assert got.overflow == ref["overflow"]
+            assert got.atomic_count == ref["atomic_count"] and got.mma_count == ref["mma_count"]
+            err_exact = abs(got.value - s)
+            err_ref = abs(got.value - ref["value"])
+            print(f"\n{dist} 2^{lgn} {key} {fin.name}: gpu {got.value!r} ref {ref['value']!r} exact {s!r} "
+                  f"rel_err_exact {err_exact / abs(s):.3e} rel_vs_ref {err_ref / abs(s):.3e}")
+            if dist == "uniform":
+                assert err_exact / abs(s) <= 1e-5 and err_ref / abs(s) <= 2e-5
+            else:
+                assert err_exact / a <= 1e-6 and err_ref / a <= 1e-6
+    del x
+    torch.cuda.empty_cache()
