@@ -1,0 +1,19 @@
+#!/bin/bash
+# One gpurun call: tests, smoke, bench, launch list and one ncu --set full capture.
+# Usage (from this container): gpurun --timeout 1500 -- 'bash tools/gpu_round.sh TAG'
+TAG=${1:-r1}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+nproc > $OUT/nproc.txt; lscpu | grep -i "model name" >> $OUT/nproc.txt
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -rA -s > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
+timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
+if [ "${NCU:-1}" = "1" ]; then
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+     python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_launch_bench.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sp16_kernel -s 2 -c 1 \
+     -o $OUT/sp16 python bench.py --steps 2 --warmup 2 --no-e2e --no-cpu --no-comparators > $OUT/ncu_full.log 2>&1
+fi
+echo done > $OUT/DONE
