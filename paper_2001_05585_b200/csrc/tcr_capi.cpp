@@ -22,6 +22,8 @@
 namespace {
 
 thread_local std::string g_err;
+// Set from measurement: which engine AUTO uses when both apply.
+constexpr bool kAutoPrefersTc05 = false;
 thread_local int g_launches = 0;
 
 int fail(int code, const std::string& msg) {
@@ -116,8 +118,20 @@ int validate_cfg(const tcr_config* c) {
 int check_supported(const tcr_config* c) {
     if (c->m != 16)
         return fail(TCR_NOT_SUPPORTED, "single_pass on B200 currently implements m = 16 (the hardware fragment)");
-    if (c->engine == TCR_ENGINE_TCGEN05) return fail(TCR_NOT_SUPPORTED, "tcgen05 engine not built yet");
+    if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_TCGEN05)
+        return fail(TCR_INVALID_ARGUMENT, "unknown engine");
     return TCR_OK;
+}
+
+// Engine choice: explicit, or AUTO = the measured winner when the geometry allows it.
+bool use_tc05(const tcr_config* c, const tcr::SpGeometry& g, bool f32) {
+    if (f32) return false;
+    uint32_t Q, ns;
+    if (!tcr::tc05_plan(g, &Q, &ns)) return false;
+    if (g.n / g.group_elems == 0) return false;
+    if (c->engine == TCR_ENGINE_TCGEN05) return true;
+    if (c->engine == TCR_ENGINE_MMA_SYNC) return false;
+    return kAutoPrefersTc05;
 }
 
 uint64_t next_pow2(uint64_t v) {
@@ -180,7 +194,22 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;
     }
-    const uint64_t groups = g1 - g0;
+    if (g0 == 0 && g1 == g.n_groups && use_tc05(c, g, f32)) {
+        // full groups on the tcgen05/TMA engine, the ragged tail (< 1 group) on the mma.sync engine;
+        // the last launch finalises
+        const uint64_t n_tiles = n / g.group_elems;
+        tcr::SpParams pt = p;
+        pt.group_begin = 0;
+        pt.group_end = n_tiles;
+        if (n_tiles < g.n_groups) pt.finalize = tcr::kFinNone;
+        if (c->finalize == TCR_FINALIZE_ATOMIC) pt.finalize = tcr::kFinAtomic;
+        const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(tcr::sm_count())));
+        TCR_CUDA(tcr::launch_tc05(pt, g, n_tiles, grid, s));
+        ++g_launches;
+        if (n_tiles == g.n_groups) return TCR_OK;
+        p.group_begin = n_tiles;
+    }
+    const uint64_t groups = p.group_end - p.group_begin;
     const int maxg = tcr::single_pass_m16_max_grid(f32);
     const int grid = int(std::min<uint64_t>(groups, uint64_t(maxg)));
     TCR_CUDA(tcr::launch_single_pass_m16(p, f32, grid, s));

@@ -55,6 +55,12 @@ struct SpParams {
 // Single-pass chained-MMA reduction, m = 16, binary16 (or fp32 convert-on-load) input.
 cudaError_t launch_single_pass_m16(const SpParams& p, bool f32_input, int grid, cudaStream_t s);
 cudaError_t launch_finalize(const SpParams& p, cudaStream_t s);
+
+// tcgen05 + TMA engine over the first n_tiles FULL groups (binary16 input).  tc05_plan says
+// whether the geometry is supported (m = 16, R <= 12, G*W a multiple of 8) and picks the slot
+// size (Q MMA-groups of 8 chunks) and ring depth.
+bool tc05_plan(const SpGeometry& g, uint32_t* Q, uint32_t* ring_slots);
+cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
 int single_pass_m16_max_grid(bool f32_input);
 
 // Input generation (harness.hpp:47-80 with SplitMix64 jump-ahead), binary16 or fp32 output.

@@ -33,11 +33,11 @@ struct Frag {
     uint32_t r0, r1, r2, r3;
 };
 
-template <bool F32IN>
+template <bool F32IN, bool CHECKED>
 __device__ __forceinline__ Frag load_line(const void* x, uint64_t e, uint64_t n) {
     // e = element index of this lane's 8-element line
     Frag f;
-    if (e + 8 <= n) {
+    if (!CHECKED || e + 8 <= n) {
         if constexpr (F32IN) {
             const float* p = static_cast<const float*>(x) + e;
             const float4 lo = ldg_stream_f4(p);
@@ -153,6 +153,77 @@ __device__ void finalize_cta(const SpParams& p, float* s_scratch) {
     }
 }
 
+template <bool F32IN, bool CHECKED>
+__device__ __forceinline__ void sp16_group(const SpParams& p, uint64_t gi, float* s_chunk, bool& ovf) {
+    const unsigned warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const unsigned c = lane & 3;
+    // load mapping: lane L = 8a + 4b + d reads line (k = 2a + b + 8(d>>1), half h = d&1)
+    const unsigned la = lane >> 3, lb = (lane >> 2) & 1, ld = lane & 3;
+    const uint32_t line_off = 16u * (2u * la + lb + 8u * (ld >> 1)) + 8u * (ld & 1u);
+    const uint32_t R = p.R, W = p.W, G = p.G;
+    const uint32_t Cg = G * W;                      // chunks per group
+    const uint64_t ce = p.chunk_elems;              // R*256
+    const uint64_t jump = 256ull + uint64_t(kSpWarps - 1) * ce;  // next fragment at chunk wrap
+    const uint64_t chunk0 = gi * uint64_t(Cg);
+    const uint32_t nch = Cg > warp ? (Cg - warp + kSpWarps - 1) / kSpWarps : 0;
+    const uint32_t F = nch * R;
+    uint64_t l_elem = (chunk0 + warp) * ce + line_off;
+    uint32_t l_r = 0;
+    Frag buf[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (uint32_t(u) < F) {
+            buf[u] = load_line<F32IN, CHECKED>(p.x, l_elem, p.n);
+            if (++l_r == R) { l_r = 0; l_elem += jump; } else { l_elem += 256; }
+        } else {
+            buf[u] = Frag{0, 0, 0, 0};
+        }
+    }
+    float acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t c_r = 0, c_ch = warp;
+    for (uint32_t f0 = 0; f0 < F; f0 += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const Frag v = buf[u];
+            if (f0 + U + u < F) {
+                buf[u] = load_line<F32IN, CHECKED>(p.x, l_elem, p.n);
+                if (++l_r == R) { l_r = 0; l_elem += jump; } else { l_elem += 256; }
+            }
+            if (f0 + u < F) {
+                const uint32_t t0 = movmatrix_trans(v.r0), t1 = movmatrix_trans(v.r1);
+                const uint32_t t2 = movmatrix_trans(v.r2), t3 = movmatrix_trans(v.r3);
+                const uint32_t q0 = __shfl_xor_sync(kFull, t0, 16), q1 = __shfl_xor_sync(kFull, t1, 16);
+                const uint32_t q2 = __shfl_xor_sync(kFull, t2, 16), q3 = __shfl_xor_sync(kFull, t3, 16);
+                if (c_r == 0) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) { acc1[i] = 0.f; acc2[i] = 0.f; }
+                }
+                mma_16816(acc1, t0, t1, q0, q1, kOnesF16x2, kOnesF16x2);
+                mma_16816(acc2, t2, t3, q2, q3, kOnesF16x2, kOnesF16x2);
+                if (++c_r == R) {
+                    const uint32_t h0 = f32_to_h(acc1[0]), h1 = f32_to_h(acc1[2]);
+                    const uint32_t h2 = f32_to_h(acc2[0]), h3 = f32_to_h(acc2[2]);
+                    const uint32_t sel = c == 0 ? h0 : c == 1 ? h1 : c == 2 ? h2 : h3;
+                    const uint32_t v0 = __shfl_sync(kFull, sel, c);
+                    const uint32_t v1 = __shfl_sync(kFull, sel, 4 + c);
+                    const uint32_t v2 = __shfl_sync(kFull, sel, 8 + c);
+                    const uint32_t v3 = __shfl_sync(kFull, sel, 12 + c);
+                    const uint32_t a01 = v0 | (v1 << 16), a23 = v2 | (v3 << 16);
+                    float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                    mma_16816(fin, a01, a01, a23, a23, kOnesF16x2, kOnesF16x2);
+                    // any non-finite binary16 partial makes the finishing sum non-finite (and no
+                    // sum of 16 finite binary16 values overflows fp32): one check per chunk
+                    ovf |= !isfinite(fin[0]);
+                    if (lane == 0) s_chunk[c_ch] = fin[0];
+                    c_r = 0;
+                    c_ch += kSpWarps;
+                }
+            }
+        }
+    }
+}
+
 template <bool F32IN>
 __global__ void __launch_bounds__(kSpThreads, 4) sp16_kernel(const SpParams p) {
     __shared__ float s_chunk[kMaxChunksPerGroup];
@@ -162,82 +233,14 @@ __global__ void __launch_bounds__(kSpThreads, 4) sp16_kernel(const SpParams p) {
 
     const unsigned warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
-    const unsigned c = lane & 3;
-    // load mapping: lane L = 8a + 4b + d reads line (k = 2a + b + 8(d>>1), half h = d&1)
-    const unsigned la = lane >> 3, lb = (lane >> 2) & 1, ld = lane & 3;
-    const uint32_t line_off = 16u * (2u * la + lb + 8u * (ld >> 1)) + 8u * (ld & 1u);
-
-    const uint32_t R = p.R, W = p.W, G = p.G;
-    const uint32_t Cg = G * W;                      // chunks per group
-    const uint64_t ce = p.chunk_elems;              // R*256
-    const uint64_t jump = 256ull + uint64_t(kSpWarps - 1) * ce;  // next fragment at chunk wrap
+    const uint32_t W = p.W, G = p.G;
+    const uint64_t ce = p.chunk_elems;
     bool ovf = false;
 
+    const uint64_t full_groups = p.n / (uint64_t(G) * W * ce);  // groups with no element past n
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
-        const uint64_t chunk0 = gi * uint64_t(Cg);
-        const uint32_t nch = Cg > warp ? (Cg - warp + kSpWarps - 1) / kSpWarps : 0;
-        const uint64_t F = uint64_t(nch) * R;
-
-        // load cursor
-        uint64_t l_elem = (chunk0 + warp) * ce + line_off;
-        uint32_t l_r = 0;
-        Frag buf[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (uint64_t(u) < F) {
-                buf[u] = load_line<F32IN>(p.x, l_elem, p.n);
-                if (++l_r == R) { l_r = 0; l_elem += jump; } else { l_elem += 256; }
-            } else {
-                buf[u] = Frag{0, 0, 0, 0};
-            }
-        }
-
-        float acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t c_r = 0, c_ch = warp;  // compute cursor: fragment r of chunk c_ch (group-local)
-        for (uint64_t f0 = 0; f0 < F; f0 += U) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const Frag v = buf[u];
-                const uint64_t fn = f0 + U + u;
-                if (fn < F) {
-                    buf[u] = load_line<F32IN>(p.x, l_elem, p.n);
-                    if (++l_r == R) { l_r = 0; l_elem += jump; } else { l_elem += 256; }
-                }
-                if (f0 + u < F) {
-                    // ---- one fragment: 4 MOVM + 4 SHFL + 2 HMMA.16816
-                    const uint32_t t0 = movmatrix_trans(v.r0), t1 = movmatrix_trans(v.r1);
-                    const uint32_t t2 = movmatrix_trans(v.r2), t3 = movmatrix_trans(v.r3);
-                    const uint32_t q0 = __shfl_xor_sync(kFull, t0, 16), q1 = __shfl_xor_sync(kFull, t1, 16);
-                    const uint32_t q2 = __shfl_xor_sync(kFull, t2, 16), q3 = __shfl_xor_sync(kFull, t3, 16);
-                    if (c_r == 0) {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) { acc1[i] = 0.f; acc2[i] = 0.f; }
-                    }
-                    // rows g: column J(g)+0 / J(g)+4, rows g+8: J(g)+2 / J(g)+6
-                    mma_16816(acc1, t0, t1, q0, q1, kOnesF16x2, kOnesF16x2);
-                    mma_16816(acc2, t2, t3, q2, q3, kOnesF16x2, kOnesF16x2);
-                    if (++c_r == R) {
-                        // ---- C_R -> binary16 (reduction.hpp:179-181), then finishing MMA (:182)
-                        const uint16_t h0 = f32_to_h(acc1[0]), h1 = f32_to_h(acc1[2]);
-                        const uint16_t h2 = f32_to_h(acc2[0]), h3 = f32_to_h(acc2[2]);
-                        ovf |= h_overflowed(h0) | h_overflowed(h1) | h_overflowed(h2) | h_overflowed(h3);
-                        // lane (g', c') contributes h_{J(g') + 2c'}; lane (g, c) gathers
-                        // h_{2c}, h_{2c+1}, h_{2c+8}, h_{2c+9} from lanes c, 4+c, 8+c, 12+c.
-                        const uint32_t sel = c == 0 ? h0 : c == 1 ? h1 : c == 2 ? h2 : h3;
-                        const uint32_t v0 = __shfl_sync(kFull, sel, c);
-                        const uint32_t v1 = __shfl_sync(kFull, sel, 4 + c);
-                        const uint32_t v2 = __shfl_sync(kFull, sel, 8 + c);
-                        const uint32_t v3 = __shfl_sync(kFull, sel, 12 + c);
-                        const uint32_t a01 = v0 | (v1 << 16), a23 = v2 | (v3 << 16);
-                        float fin[4] = {0.f, 0.f, 0.f, 0.f};
-                        mma_16816(fin, a01, a01, a23, a23, kOnesF16x2, kOnesF16x2);
-                        if (lane == 0) s_chunk[c_ch] = fin[0];
-                        c_r = 0;
-                        c_ch += kSpWarps;
-                    }
-                }
-            }
-        }
+        if (gi < full_groups) sp16_group<F32IN, false>(p, gi, s_chunk, ovf);
+        else sp16_group<F32IN, true>(p, gi, s_chunk, ovf);
         __syncthreads();
 
         // ---- block stage: reference pairwise tree over the W warp results (:253, :90-101)

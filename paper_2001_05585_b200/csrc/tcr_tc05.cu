@@ -1,0 +1,457 @@
+// tcr_tc05.cu -- single-pass chained reduction on the 5th-gen tensor cores (tcgen05 + TMA + TMEM).
+//
+// Same element partition, block stage and group stage as tcr_single_pass.cu (reference
+// reduction.hpp:164-184, :238-275); different machinery:
+//
+//   warp 0  TMA producer  -- cp.async.bulk.tensor.3d (SWIZZLE_32B) streams whole slots of the
+//                            input (Q MMA-groups of 8 warp-chunks) into a smem ring; mbarrier tx.
+//   warp 1  MMA issuer    -- one thread issues tcgen05.mma.kind::f16, M=128 N=16 K=16:
+//                            A = 8 chunks' fragment r viewed MN-major (row m = 16*chunk + j,
+//                            K = fragment row k), B = ones.  The 32-byte swizzle the TMA applies
+//                            is exactly the UMMA SWIZZLE_32B MN-major atom, so TMEM lane
+//                            16*chunk + j accumulates column j of the chunk: the reference's
+//                            C_r = ones x M_r + C_{r-1}, chained R times in TMEM.
+//   warps 2-5 epilogue    -- tcgen05.ld (32x32b) of the accumulators, C_R -> binary16 (RNE) with
+//                            the overflow note, the finishing MMA (HMMA.16816: sum of the 16
+//                            binary16 partials, two chunks per warp), block pairwise tree, group
+//                            tree -> group partial.  Last CTA finalises.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "tcr_device.cuh"
+#include "tcr_kernels.h"
+
+namespace tcr {
+
+namespace {
+
+constexpr int kTcThreads = 192;     // 6 warps
+constexpr int kEpiWarp0 = 2;
+constexpr int kAccBufs = 4;         // TMEM accumulator ring depth
+constexpr uint32_t kRingBytes = 192 * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// UMMA shared-memory matrix descriptor (sm_100: version 1 at bits 46-47).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(layout & 7) << 61;
+    return d;
+}
+
+constexpr uint32_t kLayoutNone = 0, kLayoutSw32 = 6;
+
+// kind::f16 instruction descriptor: D f32, A/B f16, A MN-major, B K-major, N=16, M=128.
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (0u << 16) | ((16u >> 3) << 17) |
+                            ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+    return v;
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ float warp_tree_xor(float v) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float o = __shfl_xor_sync(kFull, v, off);
+        v = (lane_id() & off) ? (o + v) : (v + o);
+    }
+    return v;
+}
+
+// Canonical adjacent tree over vals[0,count) (zero padded to a power of two) by the first
+// `nthr` threads (power of two, multiple of 32); every thread of the CTA must call it.
+__device__ float cta_tree(const float* vals, uint64_t count, float* s_scratch, unsigned nthr) {
+    uint64_t P = 1;
+    while (P < count) P <<= 1;
+    uint64_t seg = P / nthr;
+    if (seg == 0) seg = 1;
+    float acc = 0.0f;
+    const uint64_t lo = uint64_t(threadIdx.x) * seg;
+    if (threadIdx.x < nthr && lo < P) {
+        float stk[40];
+        int top = 0;
+        for (uint64_t i = 0; i < seg; ++i) {
+            const uint64_t idx = lo + i;
+            float v = idx < count ? __ldcg(vals + idx) : 0.0f;
+            for (uint64_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
+            stk[top++] = v;
+        }
+        acc = stk[0];
+    }
+    if (threadIdx.x < nthr) {
+        acc = warp_tree_xor(acc);
+        if (lane_id() == 0) s_scratch[threadIdx.x >> 5] = acc;
+    }
+    __syncthreads();
+    float r = 0.0f;
+    if (threadIdx.x < 32) {
+        r = lane_id() < (nthr >> 5) ? s_scratch[lane_id()] : 0.0f;
+        r = warp_tree_xor(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+struct SmemLayout {
+    uint32_t ring_off, ones_off, bar_off, misc_off, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(uint32_t slot_bytes, uint32_t ns) {
+    SmemLayout L;
+    L.ring_off = 0;
+    L.ones_off = slot_bytes * ns;
+    L.bar_off = L.ones_off + 1024;
+    L.misc_off = L.bar_off + 8 * (2 * ns + 2 * kAccBufs) + 16;
+    L.total = L.misc_off + 4 * (2 * kMaxChunksPerGroup + kMaxChunksPerGroup + 64) + 1024;  // +1024 align slack
+    return L;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const uint32_t Q, const uint32_t ns,
+            const uint64_t n_tiles) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t R = p.R, W = p.W, G = p.G;
+    const uint32_t slot_bytes = 4096u * Q * R;
+    const SmemLayout L = smem_layout(slot_bytes, ns);
+    unsigned char* ring = smem + L.ring_off;
+    uint16_t* ones = reinterpret_cast<uint16_t*>(smem + L.ones_off);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* empty = full + ns;
+    uint64_t* tfull = empty + ns;
+    uint64_t* tempty = tfull + kAccBufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+    float* s_chunk = reinterpret_cast<float*>(smem + L.misc_off);          // [2][256]
+    float* s_block = s_chunk + 2 * kMaxChunksPerGroup;                     // [256]
+    float* s_scratch = s_block + kMaxChunksPerGroup;                        // [32]
+    int* s_last = reinterpret_cast<int*>(s_scratch + 32);
+
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const uint32_t Cg = G * W;                        // chunks per tile (group)
+    const uint32_t slots_per_tile = Cg / (8u * Q);
+    const uint32_t acc_cols = 16u * Q;                // TMEM columns per accumulator buffer
+
+    // ---- setup
+    for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) ones[i] = 0x3C00u;
+    if (warp == 0 && lane == 0) {
+        for (uint32_t i = 0; i < ns; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kAccBufs; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
+    uint32_t ncols = 32;
+    while (ncols < acc_cols * kAccBufs) ncols <<= 1;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(ncols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ones[] visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    bool ovf = false;
+
+    if (warp == 0) {
+        // ================= TMA producer
+        if (lane == 0) {
+            const uint64_t policy = evict_first_policy();
+            uint32_t t = 0;
+            const uint64_t slabs_per_slot = 16ull * Q * R;   // 8-row slabs (128 elements)
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const uint64_t slab0 = tile * (uint64_t(Cg) * R * 2);  // chunk = R*256 el = 2R slabs
+                for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
+                    const uint32_t rs = t % ns, ph = (t / ns) & 1;
+                    mbar_wait(&empty[rs], ph ^ 1);
+                    mbar_expect_tx(&full[rs], slot_bytes);
+                    tma_load_3d(ring + size_t(rs) * slot_bytes, &tmap, &full[rs], 0, 0,
+                                int(slab0 + uint64_t(s) * slabs_per_slot), policy);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (single thread)
+        if (lane == 0) {
+            const uint64_t bdesc = umma_desc(smem_u32(ones), 128, 256, kLayoutNone);
+            uint32_t t = 0;
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
+                    const uint32_t rs = t % ns, ph = (t / ns) & 1;
+                    const uint32_t ab = t % kAccBufs, aph = (t / kAccBufs) & 1;
+                    mbar_wait(&full[rs], ph);
+                    mbar_wait(&tempty[ab], aph ^ 1);
+                    tc_fence_after();
+                    const uint32_t sbase = smem_u32(ring + size_t(rs) * slot_bytes);
+                    for (uint32_t q = 0; q < Q; ++q) {
+                        const uint32_t d = tmem_base + ab * acc_cols + 16u * q;
+                        for (uint32_t r = 0; r < R; ++r) {
+                            // 8 chunks of this MMA-group, fragment r: MN atoms (chunks) R*512 B apart,
+                            // K groups of 8 rows 256 B apart
+                            const uint32_t a = sbase + (8u * q * R + r) * 512u;
+                            umma_f16(d, umma_desc(a, R * 512u, 256u, kLayoutSw32), bdesc, r > 0 ? 1u : 0u);
+                        }
+                    }
+                    umma_commit(&empty[rs]);   // smem slot reusable once these MMAs retire
+                    umma_commit(&tfull[ab]);   // accumulators ready for the epilogue
+                }
+            }
+        }
+    } else {
+        // ================= epilogue warps 2..5: TMEM quarter qw = warp % 4
+        const uint32_t qw = warp & 3u;
+        const uint32_t c = lane & 3u;
+        const uint32_t ew = warp - kEpiWarp0;        // 0..3
+        uint32_t t = 0, tb = 0;
+        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, tb ^= 1) {
+            float* chunks = s_chunk + tb * kMaxChunksPerGroup;
+            for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
+                const uint32_t ab = t % kAccBufs, aph = (t / kAccBufs) & 1;
+                mbar_wait(&tfull[ab], aph);
+                tc_fence_after();
+                uint32_t v[4];
+                const uint32_t taddr = tmem_base + ((32u * qw) << 16) + ab * acc_cols;
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q)
+                    if (q < Q) v[q] = tmem_ld1(taddr + 16u * q);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[ab]);
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) {
+                    if (q >= Q) break;
+                    // lane l holds C_R[j = l & 15] of chunk 2*qw + (l >> 4) of MMA-group q
+                    const uint16_t h = f32_to_h(__uint_as_float(v[q]));
+                    ovf |= h_overflowed(h);
+                    const uint32_t nb = __shfl_down_sync(kFull, uint32_t(h), 1);
+                    const uint32_t hp = uint32_t(h) | (nb << 16);        // even lanes: (h_2i, h_2i+1)
+                    const uint32_t a0 = __shfl_sync(kFull, hp, 2 * c);
+                    const uint32_t a2 = __shfl_sync(kFull, hp, 2 * c + 8);
+                    const uint32_t a1 = __shfl_sync(kFull, hp, 16 + 2 * c);
+                    const uint32_t a3 = __shfl_sync(kFull, hp, 16 + 2 * c + 8);
+                    float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                    // finishing MMA (reduction.hpp:182): rows 0-7 chunk A, rows 8-15 chunk B
+                    mma_16816(fin, a0, a1, a2, a3, kOnesF16x2, kOnesF16x2);
+                    if (lane == 0) {
+                        const uint32_t ch = s * 8u * Q + 8u * q + 2u * qw;
+                        chunks[ch] = fin[0];
+                        chunks[ch + 1] = fin[2];
+                    }
+                }
+            }
+            named_bar(1, 128);
+            // block stage: pairwise tree over W chunk results (reduction.hpp:253, :90-101)
+            uint32_t P = 1;
+            while (P < W) P <<= 1;
+            for (uint32_t b = ew; b < G; b += 4) {
+                float x = lane < W ? chunks[b * W + lane] : 0.0f;
+                for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
+                if (lane == 0) {
+                    s_block[b] = x;
+                    const uint64_t gb = tile * G + b;
+                    if (p.block_partials) p.block_partials[gb] = x;
+                    if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
+                }
+            }
+            named_bar(1, 128);
+            if (ew == 0 && p.group_partials) {
+                const uint32_t seg = G >= 32 ? G / 32 : 1;
+                float x = 0.0f;
+                if (lane * seg < G) {
+                    float loc[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? s_block[lane * seg + i] : 0.0f;
+#pragma unroll
+                    for (int w2 = 1; w2 < 8; w2 <<= 1)
+#pragma unroll
+                        for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
+                    x = loc[0];
+                }
+                x = warp_tree_xor(x);
+                if (lane == 0) p.group_partials[tile] = x;
+            }
+            named_bar(1, 128);
+        }
+        if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+    }
+
+    // ---- teardown
+    tc_fence_before();
+    __threadfence();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+
+    if (p.finalize == kFinTree || p.finalize == kFinOrdered) {
+        if (threadIdx.x == 0) {
+            const unsigned tk = atomicAdd(p.ticket, 1u);
+            *s_last = (tk == gridDim.x - 1);
+        }
+        __syncthreads();
+        if (*s_last) {
+            __threadfence();
+            if (p.finalize == kFinTree) {
+                const float r = cta_tree(p.group_partials, p.n_groups, s_scratch, 128);
+                if (threadIdx.x == 0) *p.result = r;
+            } else if (threadIdx.x == 0) {
+                float acc = 0.0f;
+                if (p.atomic_order == 1) {
+                    uint32_t* order = p.order_scratch;
+                    for (uint64_t i = 0; i < p.n_blocks; ++i) order[i] = uint32_t(i);
+                    uint64_t st = p.atomic_seed;
+                    for (uint64_t i = p.n_blocks; i > 1; --i) {
+                        st += 0x9E3779B97F4A7C15ull;
+                        uint64_t z = st;
+                        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+                        z ^= z >> 31;
+                        const uint64_t r = z % i;
+                        const uint32_t tt = order[i - 1];
+                        order[i - 1] = order[r];
+                        order[r] = tt;
+                    }
+                    for (uint64_t i = 0; i < p.n_blocks; ++i) acc += __ldcg(p.block_partials + order[i]);
+                } else {
+                    for (uint64_t b = 0; b < p.n_blocks; ++b) acc += __ldcg(p.block_partials + b);
+                }
+                *p.result = acc;
+            }
+            if (threadIdx.x == 0) *p.ticket = 0u;
+        }
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+bool tc05_plan(const SpGeometry& g, uint32_t* Q_out, uint32_t* ns_out) {
+    if (g.m != 16 || g.R > 12) return false;
+    const uint64_t cg = uint64_t(g.G) * g.W;
+    if (cg % 8 != 0 || cg > uint64_t(kMaxChunksPerGroup)) return false;
+    uint32_t Q = 4;
+    while (Q > 1 && (cg % (8ull * Q) != 0 || Q * g.R > 8)) Q >>= 1;
+    const uint32_t slot = 4096u * Q * g.R;
+    uint32_t ns = kRingBytes / slot;
+    if (ns > 16) ns = 16;
+    if (ns < 2) return false;
+    *Q_out = Q;
+    *ns_out = ns;
+    return true;
+}
+
+cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s) {
+    uint32_t Q, ns;
+    if (!tc05_plan(g, &Q, &ns)) return cudaErrorInvalidValue;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {16, 8, cuuint64_t(n_tiles * g.group_elems / 128)};
+    const cuuint64_t strides[2] = {32, 256};
+    const cuuint32_t box[3] = {16, 8, cuuint32_t(16u * Q * g.R)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(p.x), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    const SmemLayout L = smem_layout(4096u * Q * g.R, ns);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    tc05_kernel<<<grid, kTcThreads, L.total, s>>>(map, p, Q, ns, n_tiles);
+    return cudaGetLastError();
+}
+
+}  // namespace tcr
