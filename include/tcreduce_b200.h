@@ -118,6 +118,11 @@ int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config
                                  void* cuda_stream);
 size_t tcr_block_count(size_t n, const tcr_config* cfg);
 
+/* Shard alignment for multi-GPU single_pass: elements per kernel group (G logical blocks).
+ * Shards cut on multiples of this keep every rank's block/group partition a sub-partition of
+ * the single-GPU one.  0 on an invalid config. */
+size_t tcr_group_elems(const tcr_config* cfg);
+
 /* Counters of the reference formulas for single_pass (reduction.hpp:240-273). */
 int tcr_single_pass_counters(size_t n, const tcr_config* cfg, tcr_outcome* out);
 

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tcr_block_results_f16_device": (C.c_int, [_P, _SZ, _CFG, _P, _P]),
     "tcr_block_count": (_SZ, [_SZ, _CFG]),
     "tcr_single_pass_counters": (C.c_int, [_SZ, _CFG, _OUT]),
+    "tcr_group_elems": (_SZ, [_CFG]),
     "tcr_generate_f16_device": (C.c_int, [_P, _SZ, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_double,
                                           _SZ, _P]),
     "tcr_generate_f32_device": (C.c_int, [_P, _SZ, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_double,

@@ -316,6 +316,11 @@ size_t tcr_block_count(size_t n, const tcr_config* c) {
     return tcr::make_geometry(n, c->m, c->R, c->B).n_blocks;
 }
 
+size_t tcr_group_elems(const tcr_config* c) {
+    if (!c || validate_cfg(c)) return 0;
+    return tcr::make_geometry(1, c->m, c->R, c->B).group_elems;
+}
+
 int tcr_single_pass_counters(size_t n, const tcr_config* c, tcr_outcome* out) {
     int rc = validate_cfg(c);
     if (rc) return rc;
