@@ -210,7 +210,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         p.group_begin = n_tiles;
     }
     const uint64_t groups = p.group_end - p.group_begin;
-    const int maxg = tcr::single_pass_m16_max_grid(f32);
+    const int maxg = tcr::single_pass_m16_max_grid(f32, c->R);
     const int grid = int(std::min<uint64_t>(groups, uint64_t(maxg)));
     TCR_CUDA(tcr::launch_single_pass_m16(p, f32, grid, s));
     ++g_launches;

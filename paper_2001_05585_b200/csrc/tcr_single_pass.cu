@@ -154,7 +154,7 @@ __device__ void finalize_cta(const SpParams& p, float* s_scratch) {
 }
 
 template <bool F32IN, bool CHECKED>
-__device__ __forceinline__ void sp16_group(const SpParams& p, uint64_t gi, float* s_chunk, bool& ovf) {
+__device__ __noinline__ void sp16_group(const SpParams& p, uint64_t gi, float* s_chunk, bool& ovf) {
     const unsigned warp = threadIdx.x >> 5;
     const unsigned lane = lane_id();
     const unsigned c = lane & 3;
@@ -224,8 +224,86 @@ __device__ __forceinline__ void sp16_group(const SpParams& p, uint64_t gi, float
     }
 }
 
-template <bool F32IN>
-__global__ void __launch_bounds__(kSpThreads, 4) sp16_kernel(const SpParams p) {
+
+// Fast path for full groups with a compile-time chain length RT (1..5): a batch of UC chunks
+// (UC*RT fragments) is loaded while the previous batch is reduced; every address offset inside
+// a batch is a compile-time constant; two chunks share one finishing HMMA when UC >= 2.
+template <bool F32IN, int RT>
+__device__ __forceinline__ void sp16_group_fast(const SpParams& p, uint64_t gi, float* s_chunk, bool& ovf) {
+    constexpr int UC = RT == 1 ? 4 : RT == 2 ? 2 : 1;   // chunks per batch
+    constexpr int BF = UC * RT;                          // fragments per batch
+    constexpr uint64_t CE = uint64_t(RT) * 256;          // chunk elements
+    constexpr uint64_t WSTRIDE = uint64_t(kSpWarps) * CE;  // next chunk of the same warp
+    const unsigned warp = threadIdx.x >> 5;
+    const unsigned lane = lane_id();
+    const unsigned c = lane & 3;
+    const unsigned la = lane >> 3, lb = (lane >> 2) & 1, ld = lane & 3;
+    const uint32_t line_off = 16u * (2u * la + lb + 8u * (ld >> 1)) + 8u * (ld & 1u);
+    const uint32_t Cg = p.G * p.W;
+    const uint32_t nch = Cg > warp ? (Cg - warp + kSpWarps - 1) / kSpWarps : 0;
+    const uint64_t base = (gi * uint64_t(Cg) + warp) * CE + line_off;
+
+    auto load_batch = [&](uint32_t i0, Frag (&f)[BF]) {
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                if (i0 + u < nch) f[u * RT + r] = load_line<F32IN, false>(p.x, base + (i0 + u) * WSTRIDE + r * 256, p.n);
+                else f[u * RT + r] = Frag{0, 0, 0, 0};
+            }
+        }
+    };
+
+    Frag cur[BF], nxt[BF];
+    load_batch(0, cur);
+    for (uint32_t i0 = 0; i0 < nch; i0 += UC) {
+        if (i0 + UC < nch) load_batch(i0 + UC, nxt);
+        uint32_t sel[UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+            float acc1[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                const Frag v = cur[u * RT + r];
+                const uint32_t t0 = movmatrix_trans(v.r0), t1 = movmatrix_trans(v.r1);
+                const uint32_t t2 = movmatrix_trans(v.r2), t3 = movmatrix_trans(v.r3);
+                const uint32_t q0 = __shfl_xor_sync(kFull, t0, 16), q1 = __shfl_xor_sync(kFull, t1, 16);
+                const uint32_t q2 = __shfl_xor_sync(kFull, t2, 16), q3 = __shfl_xor_sync(kFull, t3, 16);
+                mma_16816(acc1, t0, t1, q0, q1, kOnesF16x2, kOnesF16x2);
+                mma_16816(acc2, t2, t3, q2, q3, kOnesF16x2, kOnesF16x2);
+            }
+            const uint32_t h0 = f32_to_h(acc1[0]), h1 = f32_to_h(acc1[2]);
+            const uint32_t h2 = f32_to_h(acc2[0]), h3 = f32_to_h(acc2[2]);
+            sel[u] = c == 0 ? h0 : c == 1 ? h1 : c == 2 ? h2 : h3;
+        }
+#pragma unroll
+        for (int u = 0; u < UC; u += (UC >= 2 ? 2 : 1)) {
+            const int v_ = UC >= 2 ? u + 1 : u;
+            const uint32_t aA = __shfl_sync(kFull, sel[u], c) | (__shfl_sync(kFull, sel[u], 4 + c) << 16);
+            const uint32_t cA = __shfl_sync(kFull, sel[u], 8 + c) | (__shfl_sync(kFull, sel[u], 12 + c) << 16);
+            uint32_t aB = aA, cB = cA;
+            if (UC >= 2) {
+                aB = __shfl_sync(kFull, sel[v_], c) | (__shfl_sync(kFull, sel[v_], 4 + c) << 16);
+                cB = __shfl_sync(kFull, sel[v_], 8 + c) | (__shfl_sync(kFull, sel[v_], 12 + c) << 16);
+            }
+            float fin[4] = {0.f, 0.f, 0.f, 0.f};
+            // finishing MMA (reduction.hpp:182): rows 0-7 chunk u, rows 8-15 chunk u+1
+            mma_16816(fin, aA, aB, cA, cB, kOnesF16x2, kOnesF16x2);
+            ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
+            if (lane == 0) {
+                if (i0 + u < nch) s_chunk[warp + (i0 + u) * kSpWarps] = fin[0];
+                if (UC >= 2 && i0 + v_ < nch) s_chunk[warp + (i0 + v_) * kSpWarps] = fin[2];
+            }
+        }
+        if (i0 + UC < nch) {
+#pragma unroll
+            for (int i = 0; i < BF; ++i) cur[i] = nxt[i];
+        }
+    }
+}
+
+template <bool F32IN, int RT>
+__global__ void __launch_bounds__(kSpThreads, 3) sp16_kernel(const SpParams p) {
     __shared__ float s_chunk[kMaxChunksPerGroup];
     __shared__ float s_block[kMaxChunksPerGroup];
     __shared__ float s_scratch[32];
@@ -239,8 +317,12 @@ __global__ void __launch_bounds__(kSpThreads, 4) sp16_kernel(const SpParams p) {
 
     const uint64_t full_groups = p.n / (uint64_t(G) * W * ce);  // groups with no element past n
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
-        if (gi < full_groups) sp16_group<F32IN, false>(p, gi, s_chunk, ovf);
-        else sp16_group<F32IN, true>(p, gi, s_chunk, ovf);
+        if (gi < full_groups) {
+            if constexpr (RT > 0) sp16_group_fast<F32IN, RT>(p, gi, s_chunk, ovf);
+            else sp16_group<F32IN, false>(p, gi, s_chunk, ovf);
+        } else {
+            sp16_group<F32IN, true>(p, gi, s_chunk, ovf);
+        }
         __syncthreads();
 
         // ---- block stage: reference pairwise tree over the W warp results (:253, :90-101)
@@ -306,9 +388,24 @@ __global__ void __launch_bounds__(kSpThreads) finalize_kernel(const SpParams p) 
 
 }  // namespace
 
+template <bool F32IN>
+using SpKernel = void (*)(SpParams);
+
+template <bool F32IN>
+static SpKernel<F32IN> pick_kernel(uint32_t R) {
+    switch (R) {
+    case 1: return sp16_kernel<F32IN, 1>;
+    case 2: return sp16_kernel<F32IN, 2>;
+    case 3: return sp16_kernel<F32IN, 3>;
+    case 4: return sp16_kernel<F32IN, 4>;
+    case 5: return sp16_kernel<F32IN, 5>;
+    default: return sp16_kernel<F32IN, 0>;
+    }
+}
+
 cudaError_t launch_single_pass_m16(const SpParams& p, bool f32_input, int grid, cudaStream_t s) {
-    if (f32_input) sp16_kernel<true><<<grid, kSpThreads, 0, s>>>(p);
-    else sp16_kernel<false><<<grid, kSpThreads, 0, s>>>(p);
+    if (f32_input) pick_kernel<true>(p.R)<<<grid, kSpThreads, 0, s>>>(p);
+    else pick_kernel<false>(p.R)<<<grid, kSpThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -317,12 +414,12 @@ cudaError_t launch_finalize(const SpParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-int single_pass_m16_max_grid(bool f32_input) {
+int single_pass_m16_max_grid(bool f32_input, uint32_t R) {
     int per_sm = 0;
     if (f32_input)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sp16_kernel<true>, kSpThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pick_kernel<true>(R), kSpThreads, 0);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sp16_kernel<false>, kSpThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pick_kernel<false>(R), kSpThreads, 0);
     if (per_sm < 1) per_sm = 1;
     return per_sm * sm_count();
 }

@@ -25,9 +25,8 @@ namespace tcr {
 
 namespace {
 
-constexpr int kTcThreads = 192;     // 6 warps
 constexpr int kEpiWarp0 = 2;
-constexpr int kAccBufs = 4;         // TMEM accumulator ring depth
+constexpr int kAccBufs = 8;         // TMEM accumulator ring depth
 constexpr uint32_t kRingBytes = 192 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -170,6 +169,10 @@ __device__ float cta_tree(const float* vals, uint64_t count, float* s_scratch, u
     return r;
 }
 
+constexpr int kEpiGroups = 3;                         // epilogue warpgroups, round-robin over slots
+constexpr int kTcThreads = 64 + 128 * kEpiGroups;       // TMA warp + MMA warp + epilogue
+constexpr int kTileBufs = 8;                            // per-tile chunk/block tables in flight
+
 struct SmemLayout {
     uint32_t ring_off, ones_off, bar_off, misc_off, total;
 };
@@ -180,13 +183,14 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t slot_bytes, uint32_t 
     L.ones_off = slot_bytes * ns;
     L.bar_off = L.ones_off + 1024;
     L.misc_off = L.bar_off + 8 * (2 * ns + 2 * kAccBufs) + 16;
-    L.total = L.misc_off + 4 * (2 * kMaxChunksPerGroup + kMaxChunksPerGroup + 64) + 1024;  // +1024 align slack
+    // s_chunk[kTileBufs][256] + s_block[kTileBufs][256] + s_scratch[32] + s_done[kTileBufs] + s_own[4] + s_last
+    L.total = L.misc_off + 4 * (2 * kTileBufs * kMaxChunksPerGroup + 32 + kTileBufs + 8) + 1024;  // +1024 align slack
     return L;
 }
 
+template <int Q>
 __global__ void __launch_bounds__(kTcThreads, 1)
-tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const uint32_t Q, const uint32_t ns,
-            const uint64_t n_tiles) {
+tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const uint32_t ns, const uint64_t n_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t R = p.R, W = p.W, G = p.G;
@@ -199,18 +203,21 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
     uint64_t* tfull = empty + ns;
     uint64_t* tempty = tfull + kAccBufs;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
-    float* s_chunk = reinterpret_cast<float*>(smem + L.misc_off);          // [2][256]
-    float* s_block = s_chunk + 2 * kMaxChunksPerGroup;                     // [256]
-    float* s_scratch = s_block + kMaxChunksPerGroup;                        // [32]
-    int* s_last = reinterpret_cast<int*>(s_scratch + 32);
+    float* s_chunk = reinterpret_cast<float*>(smem + L.misc_off);             // [kTileBufs][256]
+    float* s_block = s_chunk + kTileBufs * kMaxChunksPerGroup;                 // [kTileBufs][256]
+    float* s_scratch = s_block + kTileBufs * kMaxChunksPerGroup;               // [32]
+    uint32_t* s_done = reinterpret_cast<uint32_t*>(s_scratch + 32);            // [kTileBufs]
+    uint32_t* s_own = s_done + kTileBufs;                                      // [4]
+    int* s_last = reinterpret_cast<int*>(s_own + 4);
 
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const uint32_t Cg = G * W;                        // chunks per tile (group)
     const uint32_t slots_per_tile = Cg / (8u * Q);
-    const uint32_t acc_cols = 16u * Q;                // TMEM columns per accumulator buffer
+    constexpr uint32_t acc_cols = 16u * Q;            // TMEM columns per accumulator buffer
 
     // ---- setup
     for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) ones[i] = 0x3C00u;
+    if (threadIdx.x < kTileBufs) s_done[threadIdx.x] = 0;
     if (warp == 0 && lane == 0) {
         for (uint32_t i = 0; i < ns; ++i) {
             mbar_init(&full[i], 1);
@@ -223,8 +230,8 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
-    uint32_t ncols = 32;
-    while (ncols < acc_cols * kAccBufs) ncols <<= 1;
+    constexpr uint32_t ncols = acc_cols * kAccBufs <= 32 ? 32 : acc_cols * kAccBufs <= 64 ? 64
+                             : acc_cols * kAccBufs <= 128 ? 128 : acc_cols * kAccBufs <= 256 ? 256 : 512;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(ncols));
@@ -267,7 +274,8 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                     mbar_wait(&tempty[ab], aph ^ 1);
                     tc_fence_after();
                     const uint32_t sbase = smem_u32(ring + size_t(rs) * slot_bytes);
-                    for (uint32_t q = 0; q < Q; ++q) {
+#pragma unroll
+                    for (uint32_t q = 0; q < uint32_t(Q); ++q) {
                         const uint32_t d = tmem_base + ab * acc_cols + 16u * q;
                         for (uint32_t r = 0; r < R; ++r) {
                             // 8 chunks of this MMA-group, fragment r: MN atoms (chunks) R*512 B apart,
@@ -282,34 +290,36 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
             }
         }
     } else {
-        // ================= epilogue warps 2..5: TMEM quarter qw = warp % 4
-        const uint32_t qw = warp & 3u;
+        // ================= epilogue: warpgroup eg takes slots t = eg (mod kEpiGroups)
+        const uint32_t ew = warp - kEpiWarp0;         // 0 .. 4*kEpiGroups-1
+        const uint32_t eg = ew >> 2, w4 = ew & 3u;    // warpgroup, warp within it
+        const uint32_t qw = warp & 3u;                // TMEM lane quarter this warp may access
         const uint32_t c = lane & 3u;
-        const uint32_t ew = warp - kEpiWarp0;        // 0..3
-        uint32_t t = 0, tb = 0;
-        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, tb ^= 1) {
-            float* chunks = s_chunk + tb * kMaxChunksPerGroup;
+        const int bar_id = 1 + int(eg);
+        uint32_t t = 0, k = 0;
+        uint32_t P = 1;
+        while (P < W) P <<= 1;
+        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+            const uint32_t buf = k % kTileBufs;
+            float* chunks = s_chunk + buf * kMaxChunksPerGroup;
             for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
+                if (t % kEpiGroups != eg) continue;
                 const uint32_t ab = t % kAccBufs, aph = (t / kAccBufs) & 1;
                 mbar_wait(&tfull[ab], aph);
                 tc_fence_after();
-                uint32_t v[4];
+                uint32_t v[Q];
                 const uint32_t taddr = tmem_base + ((32u * qw) << 16) + ab * acc_cols;
 #pragma unroll
-                for (uint32_t q = 0; q < 4; ++q)
-                    if (q < Q) v[q] = tmem_ld1(taddr + 16u * q);
+                for (int q = 0; q < Q; ++q) v[q] = tmem_ld1(taddr + 16u * q);
                 tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[ab]);
 #pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    if (q >= Q) break;
+                for (int q = 0; q < Q; ++q) {
                     // lane l holds C_R[j = l & 15] of chunk 2*qw + (l >> 4) of MMA-group q
-                    const uint16_t h = f32_to_h(__uint_as_float(v[q]));
-                    ovf |= h_overflowed(h);
-                    const uint32_t nb = __shfl_down_sync(kFull, uint32_t(h), 1);
-                    const uint32_t hp = uint32_t(h) | (nb << 16);        // even lanes: (h_2i, h_2i+1)
+                    const uint32_t h = f32_to_h(__uint_as_float(v[q]));
+                    const uint32_t hp = h | (__shfl_down_sync(kFull, h, 1) << 16);  // even lanes: (h_2i, h_2i+1)
                     const uint32_t a0 = __shfl_sync(kFull, hp, 2 * c);
                     const uint32_t a2 = __shfl_sync(kFull, hp, 2 * c + 8);
                     const uint32_t a1 = __shfl_sync(kFull, hp, 16 + 2 * c);
@@ -317,45 +327,59 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                     float fin[4] = {0.f, 0.f, 0.f, 0.f};
                     // finishing MMA (reduction.hpp:182): rows 0-7 chunk A, rows 8-15 chunk B
                     mma_16816(fin, a0, a1, a2, a3, kOnesF16x2, kOnesF16x2);
+                    // a non-finite binary16 partial makes its finishing sum non-finite
+                    ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
                     if (lane == 0) {
                         const uint32_t ch = s * 8u * Q + 8u * q + 2u * qw;
                         chunks[ch] = fin[0];
                         chunks[ch + 1] = fin[2];
                     }
                 }
-            }
-            named_bar(1, 128);
-            // block stage: pairwise tree over W chunk results (reduction.hpp:253, :90-101)
-            uint32_t P = 1;
-            while (P < W) P <<= 1;
-            for (uint32_t b = ew; b < G; b += 4) {
-                float x = lane < W ? chunks[b * W + lane] : 0.0f;
-                for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
-                if (lane == 0) {
-                    s_block[b] = x;
-                    const uint64_t gb = tile * G + b;
-                    if (p.block_partials) p.block_partials[gb] = x;
-                    if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
+                // slot bookkeeping: the warpgroup that completes a tile runs its trees
+                named_bar(bar_id, 128);
+                if (w4 == 0 && lane == 0) {
+                    __threadfence_block();
+                    const uint32_t old = atomicAdd(&s_done[buf], 1u);
+                    s_own[eg] = (old + 1 == slots_per_tile);
+                    __threadfence_block();
+                }
+                named_bar(bar_id, 128);
+                if (s_own[eg]) {
+                    float* blocks = s_block + buf * kMaxChunksPerGroup;
+                    // block stage: pairwise tree over W chunk results (reduction.hpp:253, :90-101)
+                    for (uint32_t b = w4; b < G; b += 4) {
+                        float x = lane < W ? chunks[b * W + lane] : 0.0f;
+                        for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
+                        if (lane == 0) {
+                            blocks[b] = x;
+                            const uint64_t gb = tile * G + b;
+                            if (p.block_partials) p.block_partials[gb] = x;
+                            if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
+                        }
+                    }
+                    named_bar(bar_id, 128);
+                    if (w4 == 0) {
+                        if (p.group_partials) {
+                            const uint32_t seg = G >= 32 ? G / 32 : 1;
+                            float x = 0.0f;
+                            if (lane * seg < G) {
+                                float loc[8];
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? blocks[lane * seg + i] : 0.0f;
+#pragma unroll
+                                for (int w2 = 1; w2 < 8; w2 <<= 1)
+#pragma unroll
+                                    for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
+                                x = loc[0];
+                            }
+                            x = warp_tree_xor(x);
+                            if (lane == 0) p.group_partials[tile] = x;
+                        }
+                        if (lane == 0) s_done[buf] = 0;
+                    }
+                    named_bar(bar_id, 128);
                 }
             }
-            named_bar(1, 128);
-            if (ew == 0 && p.group_partials) {
-                const uint32_t seg = G >= 32 ? G / 32 : 1;
-                float x = 0.0f;
-                if (lane * seg < G) {
-                    float loc[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? s_block[lane * seg + i] : 0.0f;
-#pragma unroll
-                    for (int w2 = 1; w2 < 8; w2 <<= 1)
-#pragma unroll
-                        for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
-                    x = loc[0];
-                }
-                x = warp_tree_xor(x);
-                if (lane == 0) p.group_partials[tile] = x;
-            }
-            named_bar(1, 128);
         }
         if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     }
@@ -376,7 +400,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
         if (*s_last) {
             __threadfence();
             if (p.finalize == kFinTree) {
-                const float r = cta_tree(p.group_partials, p.n_groups, s_scratch, 128);
+                const float r = cta_tree(p.group_partials, p.n_groups, s_scratch, 256);
                 if (threadIdx.x == 0) *p.result = r;
             } else if (threadIdx.x == 0) {
                 float acc = 0.0f;
@@ -433,6 +457,7 @@ bool tc05_plan(const SpGeometry& g, uint32_t* Q_out, uint32_t* ns_out) {
     const uint32_t slot = 4096u * Q * g.R;
     uint32_t ns = kRingBytes / slot;
     if (ns > 16) ns = 16;
+    if (smem_layout(slot, ns).total > 227u * 1024u) return false;
     if (ns < 2) return false;
     *Q_out = Q;
     *ns_out = ns;
@@ -456,11 +481,15 @@ cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles
     const SmemLayout L = smem_layout(4096u * Q * g.R, ns);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
+        for (auto fn : {tc05_kernel<1>, tc05_kernel<2>, tc05_kernel<4>}) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            if (e != cudaSuccess) return e;
+        }
         attr_set = true;
     }
-    tc05_kernel<<<grid, kTcThreads, L.total, s>>>(map, p, Q, ns, n_tiles);
+    if (Q == 4) tc05_kernel<4><<<grid, kTcThreads, L.total, s>>>(map, p, ns, n_tiles);
+    else if (Q == 2) tc05_kernel<2><<<grid, kTcThreads, L.total, s>>>(map, p, ns, n_tiles);
+    else tc05_kernel<1><<<grid, kTcThreads, L.total, s>>>(map, p, ns, n_tiles);
     return cudaGetLastError();
 }
 
