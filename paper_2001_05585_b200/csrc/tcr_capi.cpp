@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -190,6 +191,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     if (c->finalize == TCR_FINALIZE_ATOMIC) p.finalize = tcr::kFinAtomic;
     p.atomic_order = c->atomic_order;
     p.atomic_seed = c->atomic_seed;
+    if (const char* dm = std::getenv("TCR_DEBUG_MODE")) p.debug_mode = std::atoi(dm);
     if (c->finalize == TCR_FINALIZE_ATOMIC && g0 == 0) {
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;

@@ -50,6 +50,9 @@ struct SpParams {
     int32_t finalize;
     int32_t atomic_order;
     uint64_t atomic_seed;
+    // Profiling hook (env TCR_DEBUG_MODE, never set in production): tcgen05 engine only --
+    // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map.
+    int32_t debug_mode;
 };
 
 // Single-pass chained-MMA reduction, m = 16, binary16 (or fp32 convert-on-load) input.

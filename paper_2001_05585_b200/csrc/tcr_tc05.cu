@@ -75,6 +75,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -256,8 +264,13 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                     const uint32_t rs = t % ns, ph = (t / ns) & 1;
                     mbar_wait(&empty[rs], ph ^ 1);
                     mbar_expect_tx(&full[rs], slot_bytes);
-                    tma_load_3d(ring + size_t(rs) * slot_bytes, &tmap, &full[rs], 0, 0,
-                                int(slab0 + uint64_t(s) * slabs_per_slot), policy);
+                    if (p.debug_mode == 2)
+                        bulk_load_1d(ring + size_t(rs) * slot_bytes,
+                                     static_cast<const char*>(p.x) + (slab0 + uint64_t(s) * slabs_per_slot) * 256,
+                                     slot_bytes, &full[rs], policy);
+                    else
+                        tma_load_3d(ring + size_t(rs) * slot_bytes, &tmap, &full[rs], 0, 0,
+                                    int(slab0 + uint64_t(s) * slabs_per_slot), policy);
                 }
             }
         }
@@ -271,6 +284,10 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                     const uint32_t rs = t % ns, ph = (t / ns) & 1;
                     const uint32_t ab = t % kAccBufs, aph = (t / kAccBufs) & 1;
                     mbar_wait(&full[rs], ph);
+                    if (p.debug_mode == 1) {
+                        mbar_arrive(&empty[rs]);
+                        continue;
+                    }
                     mbar_wait(&tempty[ab], aph ^ 1);
                     tc_fence_after();
                     const uint32_t sbase = smem_u32(ring + size_t(rs) * slot_bytes);
@@ -291,15 +308,17 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
         }
     } else {
         // ================= epilogue: warpgroup eg takes slots t = eg (mod kEpiGroups)
+        uint64_t n_tiles_epi = n_tiles;
         const uint32_t ew = warp - kEpiWarp0;         // 0 .. 4*kEpiGroups-1
         const uint32_t eg = ew >> 2, w4 = ew & 3u;    // warpgroup, warp within it
         const uint32_t qw = warp & 3u;                // TMEM lane quarter this warp may access
         const uint32_t c = lane & 3u;
         const int bar_id = 1 + int(eg);
         uint32_t t = 0, k = 0;
+        if (p.debug_mode == 1) n_tiles_epi = 0;
         uint32_t P = 1;
         while (P < W) P <<= 1;
-        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        for (uint64_t tile = blockIdx.x; tile < n_tiles_epi; tile += gridDim.x, ++k) {
             const uint32_t buf = k % kTileBufs;
             float* chunks = s_chunk + buf * kMaxChunksPerGroup;
             for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {

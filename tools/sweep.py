@@ -1,0 +1,145 @@
+#!/usr/bin/env python3
+"""BASELINE configs[2] (B x R sweep at n=2^28 vs warp-shuffle and CUB) and configs[3]
+(precision study, n = 2^26 .. 2^30, uniform and normal) on one B200.
+
+    python tools/sweep.py [--sweep] [--precision] [--out gpurun_out/sweep.json]
+
+Every point: CUDA-event time of the single_pass kernel (median of reps, inputs > L2),
+Gelem/s, GB/s and fraction of the measured HBM copy bandwidth; precision points add the
+relative error against the exact sum of the binary16 inputs (device fixed-point sum) and
+against the reference single_pass value (tests/golden/oracle_large.json, produced by the
+pinned oracle from the reference algorithm).  Also writes the reference's 14-column CSV
+schema (csv.hpp:14-15) with a wall-clock column appended.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--precision", action="store_true")
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
+    args = ap.parse_args()
+    if not (args.sweep or args.precision):
+        args.sweep = args.precision = True
+
+    import torch
+
+    import paper_2001_05585_b200 as T
+    from paper_2001_05585_b200 import _capi
+
+    lib = _capi.load()
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    res = torch.zeros(2, dtype=torch.float32, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    rp, op = C.c_void_p(res.data_ptr()), C.c_void_p(ovf.data_ptr())
+
+    def time_fn(fn, reps):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts), min(ts)
+
+    out = {"peak_hbm_gbs": peak, "device": torch.cuda.get_device_name(0)}
+    csv_rows = []
+
+    if args.sweep:
+        n = 1 << 28
+        x = T.generate("uniform", 0, n, device=dev)
+        xp = C.c_void_p(x.data_ptr())
+        pts = []
+        for engine in (T.Engine.tcgen05, T.Engine.mma_sync):
+            for B in (32, 128, 256, 512, 1024):
+                for R in (1, 2, 3, 4, 5):
+                    cfg = T.ReductionConfig(m=16, R=R, B=B, engine=engine)
+                    c = cfg.to_c()
+                    med, best = time_fn(lambda: _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(c), rp, op, sp)),
+                                        args.reps)
+                    torch.cuda.synchronize()
+                    val = res[0].item()
+                    pts.append({"engine": engine.name, "B": B, "R": R, "ms": med, "ms_best": best,
+                                "gelem_s": n / med / 1e6, "gb_s": 2 * n / med / 1e6,
+                                "frac_hbm": 2 * n / med / 1e6 / peak, "value": val,
+                                "launches": lib.tcr_last_launch_count()})
+                    csv_rows.append(("uniform", 0, n, "single_pass", 16, R, B, val, med, engine.name))
+                    print(json.dumps(pts[-1]), flush=True)
+        comps = {}
+        comps["warp_shuffle_fp32"] = time_fn(lambda: _capi.check(lib.tcr_shuffle_f16_async(xp, n, rp, sp)), args.reps)[0]
+        comps["cub_half_in_float_acc"] = time_fn(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 0, rp, sp)),
+                                                 args.reps)[0]
+        comps["cub_half_in_half_acc"] = time_fn(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 1, rp, sp)),
+                                                args.reps)[0]
+        comps["read_probe"] = time_fn(lambda: _capi.check(lib.tcr_read_probe_async(xp, 2 * n, sp)), args.reps)[0]
+        out["sweep"] = {"n": n, "dist": "uniform s0", "points": pts,
+                        "comparators_ms": comps,
+                        "comparators_gelem_s": {k: n / v / 1e6 for k, v in comps.items()}}
+        best = min(pts, key=lambda p: p["ms"])
+        out["sweep"]["best"] = best
+        out["sweep"]["speedup_best_vs_warp_shuffle"] = comps["warp_shuffle_fp32"] / best["ms"]
+        del x
+        torch.cuda.empty_cache()
+
+    if args.precision:
+        gl = os.path.join(ROOT, "tests", "golden", "oracle_large.json")
+        golden = {(r["dist"], r["seed"], r["n"]): r for r in json.load(open(gl))["cases"]} if os.path.exists(gl) else {}
+        prec = []
+        for dist, seed in (("uniform", 0), ("normal", 1), ("normal", 2), ("normal", 3)):
+            for lgn in (26, 27, 28, 29, 30):
+                n = 1 << lgn
+                x = T.generate(dist, seed, n, device=dev)
+                exact, absum = T.exact_sum(x)
+                for (R, B) in ((1, 1024), (4, 128), (1, 128), (5, 32)):
+                    for fin in (T.Finalize.tree, T.Finalize.ordered):
+                        o = T.reduce(x, T.ReductionConfig(m=16, R=R, B=B, finalize=fin))
+                        g = golden.get((dist, seed, n), {}).get("single_pass", {}).get(f"m16_R{R}_B{B}")
+                        rec = {"dist": dist, "seed": seed, "n": n, "R": R, "B": B, "finalize": fin.name,
+                               "value": o.value, "overflow": o.overflow, "exact": exact, "abs_sum": absum,
+                               "rel_err_exact": abs(o.value - exact) / abs(exact),
+                               "err_over_abs_sum": abs(o.value - exact) / absum,
+                               "reference_value": g["value"] if g else None,
+                               "rel_diff_reference": (abs(o.value - g["value"]) / abs(exact)) if g else None,
+                               "reference_rel_err_exact": (abs(g["value"] - exact) / abs(exact)) if g else None}
+                        prec.append(rec)
+                        print(json.dumps(rec), flush=True)
+                del x
+                torch.cuda.empty_cache()
+        out["precision"] = prec
+
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(out, f, indent=1)
+    if csv_rows:
+        # csv.hpp:14-15 schema + wall-clock columns
+        with open(os.path.splitext(args.out)[0] + ".csv", "w") as f:
+            f.write("dist,seed,n,variant,m,R,B,f,value,error_pct,overflow,sim_steps,mma_count,atomic_count,"
+                    "ms,engine\n")
+            for (dist, seed, n, var, m, R, B, val, ms, eng) in csv_rows:
+                c = T.counters(n, T.ReductionConfig(m=m, R=R, B=B))
+                f.write(f"{dist},{seed},{n},{var},{m},{R},{B},0.5,{val:.9g},,0,{c.sim_steps},{c.mma_count},"
+                        f"{c.atomic_count},{ms:.6f},{eng}\n")
+
+
+if __name__ == "__main__":
+    main()
