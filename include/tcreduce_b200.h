@@ -53,8 +53,17 @@ typedef enum { TCR_ASCENDING = 0, TCR_SEEDED_PERMUTATION = 1 } tcr_atomic_order;
  *   ATOMIC  -- the paper's one atomicAdd per block (order unspecified) */
 typedef enum { TCR_FINALIZE_TREE = 0, TCR_FINALIZE_ORDERED = 1, TCR_FINALIZE_ATOMIC = 2 } tcr_finalize;
 
-/* Kernel family (chosen by measurement; AUTO picks the fastest available for the config). */
-typedef enum { TCR_ENGINE_AUTO = 0, TCR_ENGINE_MMA_SYNC = 1, TCR_ENGINE_TCGEN05 = 2 } tcr_engine;
+/* Kernel family (chosen by measurement; AUTO picks the fastest available for the config).
+ *   MMA_SYNC      -- 1-D TMA bulk copies into a smem ring, ldmatrix.trans + HMMA.16816 chain
+ *   TCGEN05       -- tensor-map TMA (SWIZZLE_32B) ring, single-thread tcgen05.mma into TMEM
+ *   MMA_SYNC_REGS -- streaming 128-bit loads straight into registers, MOVM + HMMA (also the
+ *                    fp32 convert-on-load path and the ragged tail of every engine) */
+typedef enum {
+    TCR_ENGINE_AUTO = 0,
+    TCR_ENGINE_MMA_SYNC = 1,
+    TCR_ENGINE_TCGEN05 = 2,
+    TCR_ENGINE_MMA_SYNC_REGS = 3
+} tcr_engine;
 
 /* ReductionConfig -- reduction.hpp:39-57 (first seven fields, same meaning and defaults
  * m=4, R=1, B=128, f=0.5), plus the device-side finalize / engine choice. */
@@ -147,6 +156,8 @@ int tcr_read_probe_async(const void* d_x, size_t bytes, void* cuda_stream);
 
 /* Number of kernels the last single_pass call on this thread launched (launch accounting). */
 int tcr_last_launch_count(void);
+/* Engine (tcr_engine) that reduced the full groups in the last single_pass call on this thread. */
+int tcr_last_engine(void);
 const char* tcr_last_error(void);
 const char* tcr_version(void);
 

@@ -26,6 +26,7 @@ thread_local std::string g_err;
 // Set from measurement: which engine AUTO uses when both apply.
 constexpr bool kAutoPrefersTc05 = false;
 thread_local int g_launches = 0;
+thread_local int g_engine = 0;  // engine that ran the full groups of the last call
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -119,20 +120,28 @@ int validate_cfg(const tcr_config* c) {
 int check_supported(const tcr_config* c) {
     if (c->m != 16)
         return fail(TCR_NOT_SUPPORTED, "single_pass on B200 currently implements m = 16 (the hardware fragment)");
-    if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_TCGEN05)
+    if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_MMA_SYNC_REGS)
         return fail(TCR_INVALID_ARGUMENT, "unknown engine");
     return TCR_OK;
 }
 
-// Engine choice: explicit, or AUTO = the measured winner when the geometry allows it.
-bool use_tc05(const tcr_config* c, const tcr::SpGeometry& g, bool f32) {
-    if (f32) return false;
-    uint32_t Q, ns;
-    if (!tcr::tc05_plan(g, &Q, &ns)) return false;
-    if (g.n / g.group_elems == 0) return false;
-    if (c->engine == TCR_ENGINE_TCGEN05) return true;
-    if (c->engine == TCR_ENGINE_MMA_SYNC) return false;
-    return kAutoPrefersTc05;
+// Engine choice for the full groups: explicit, or AUTO = the measured winner when the geometry
+// allows it.  The register engine always takes the ragged tail and the fp32 input path.
+int pick_engine(const tcr_config* c, const tcr::SpGeometry& g, bool f32) {
+    if (f32 || g.n / g.group_elems == 0) return TCR_ENGINE_MMA_SYNC_REGS;
+    uint32_t a, b;
+    const bool tc_ok = tcr::tc05_plan(g, &a, &b);
+    const bool bk_ok = tcr::bulk_plan(g, &a, &b);
+    switch (c->engine) {
+    case TCR_ENGINE_TCGEN05: return tc_ok ? TCR_ENGINE_TCGEN05 : TCR_ENGINE_MMA_SYNC_REGS;
+    case TCR_ENGINE_MMA_SYNC: return bk_ok ? TCR_ENGINE_MMA_SYNC : TCR_ENGINE_MMA_SYNC_REGS;
+    case TCR_ENGINE_MMA_SYNC_REGS: return TCR_ENGINE_MMA_SYNC_REGS;
+    default:
+        if (kAutoPrefersTc05 && tc_ok) return TCR_ENGINE_TCGEN05;
+        if (bk_ok) return TCR_ENGINE_MMA_SYNC;
+        if (tc_ok) return TCR_ENGINE_TCGEN05;
+        return TCR_ENGINE_MMA_SYNC_REGS;
+    }
 }
 
 uint64_t next_pow2(uint64_t v) {
@@ -196,9 +205,11 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;
     }
-    if (g0 == 0 && g1 == g.n_groups && use_tc05(c, g, f32)) {
-        // full groups on the tcgen05/TMA engine, the ragged tail (< 1 group) on the mma.sync engine;
-        // the last launch finalises
+    const int engine = (g0 == 0 && g1 == g.n_groups) ? pick_engine(c, g, f32) : TCR_ENGINE_MMA_SYNC_REGS;
+    g_engine = engine;
+    if (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC) {
+        // full groups on a TMA-fed persistent engine (one CTA per SM), the ragged tail (< 1 group)
+        // on the register engine; the last launch finalises
         const uint64_t n_tiles = n / g.group_elems;
         tcr::SpParams pt = p;
         pt.group_begin = 0;
@@ -206,7 +217,8 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         if (n_tiles < g.n_groups) pt.finalize = tcr::kFinNone;
         if (c->finalize == TCR_FINALIZE_ATOMIC) pt.finalize = tcr::kFinAtomic;
         const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(tcr::sm_count())));
-        TCR_CUDA(tcr::launch_tc05(pt, g, n_tiles, grid, s));
+        if (engine == TCR_ENGINE_TCGEN05) TCR_CUDA(tcr::launch_tc05(pt, g, n_tiles, grid, s));
+        else TCR_CUDA(tcr::launch_bulk(pt, g, n_tiles, grid, s));
         ++g_launches;
         if (n_tiles == g.n_groups) return TCR_OK;
         p.group_begin = n_tiles;
@@ -312,6 +324,7 @@ int tcr_validate(const tcr_config* c) { return validate_cfg(c); }
 const char* tcr_last_error(void) { return g_err.c_str(); }
 const char* tcr_version(void) { return "tcreduce-b200 0.1 (sm_100a)"; }
 int tcr_last_launch_count(void) { return g_launches; }
+int tcr_last_engine(void) { return g_engine; }
 
 size_t tcr_block_count(size_t n, const tcr_config* c) {
     if (!c || validate_cfg(c)) return 0;

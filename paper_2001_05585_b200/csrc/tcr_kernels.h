@@ -64,6 +64,11 @@ cudaError_t launch_finalize(const SpParams& p, cudaStream_t s);
 // size (Q MMA-groups of 8 chunks) and ring depth.
 bool tc05_plan(const SpGeometry& g, uint32_t* Q, uint32_t* ring_slots);
 cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
+
+// TMA-staged mma.sync engine (1-D bulk copies into a smem ring, ldmatrix.trans + HMMA) over the
+// first n_tiles FULL groups.  bulk_plan picks the slot (SC chunks) and ring depth.
+bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
+cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
 int single_pass_m16_max_grid(bool f32_input, uint32_t R);
 
 // Input generation (harness.hpp:47-80 with SplitMix64 jump-ahead), binary16 or fp32 output.

@@ -1,0 +1,207 @@
+// tcr_pipeline.cuh -- shared sm_100a pipeline pieces: mbarriers, TMA / bulk copies, named
+// barriers, the canonical pairwise trees and the last-CTA finaliser.
+#pragma once
+
+#include <cuda.h>
+#include <cstdint>
+
+#include "tcr_device.cuh"
+#include "tcr_kernels.h"
+
+namespace tcr {
+namespace pipe {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// Watchdog: a pipeline bug must surface as a kernel error, never as a hung GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++spins == (1u << 28)) __trap();
+    }
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ float warp_tree_xor(float v) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float o = __shfl_xor_sync(kFull, v, off);
+        v = (lane_id() & off) ? (o + v) : (v + o);
+    }
+    return v;
+}
+
+// Canonical adjacent tree over vals[0,count) (zero padded to a power of two) by the first
+// `nthr` threads (power of two, multiple of 32); every thread of the CTA must call it.
+__device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, float* s_scratch, unsigned nthr) {
+    uint64_t P = 1;
+    while (P < count) P <<= 1;
+    uint64_t seg = P / nthr;
+    if (seg == 0) seg = 1;
+    float acc = 0.0f;
+    const uint64_t lo = uint64_t(threadIdx.x) * seg;
+    if (threadIdx.x < nthr && lo < P) {
+        float stk[40];
+        int top = 0;
+        for (uint64_t i = 0; i < seg; ++i) {
+            const uint64_t idx = lo + i;
+            float v = idx < count ? __ldcg(vals + idx) : 0.0f;
+            for (uint64_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
+            stk[top++] = v;
+        }
+        acc = stk[0];
+    }
+    if (threadIdx.x < nthr) {
+        acc = warp_tree_xor(acc);
+        if (lane_id() == 0) s_scratch[threadIdx.x >> 5] = acc;
+    }
+    __syncthreads();
+    float r = 0.0f;
+    if (threadIdx.x < 32) {
+        r = lane_id() < (nthr >> 5) ? s_scratch[lane_id()] : 0.0f;
+        r = warp_tree_xor(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+
+// Last-CTA-done finaliser shared by the persistent engines: every thread of the CTA calls it
+// after publishing its partials (__threadfence + __syncthreads done by the caller).
+__device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_scratch, int* s_last, unsigned nthr) {
+    if (!(p.finalize == kFinTree || p.finalize == kFinOrdered)) return;
+    if (threadIdx.x == 0) {
+        const unsigned tk = atomicAdd(p.ticket, 1u);
+        *s_last = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    if (p.finalize == kFinTree) {
+        const float r = cta_tree(p.group_partials, p.n_groups, s_scratch, nthr);
+        if (threadIdx.x == 0) *p.result = r;
+    } else if (threadIdx.x == 0) {
+        // reduction.hpp:257-268: serial binary32 accumulation, ascending or seeded permutation
+        float acc = 0.0f;
+        if (p.atomic_order == 1) {
+            uint32_t* order = p.order_scratch;
+            for (uint64_t i = 0; i < p.n_blocks; ++i) order[i] = uint32_t(i);
+            uint64_t st = p.atomic_seed;
+            for (uint64_t i = p.n_blocks; i > 1; --i) {
+                st += 0x9E3779B97F4A7C15ull;
+                uint64_t z = st;
+                z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+                z ^= z >> 31;
+                const uint64_t r = z % i;
+                const uint32_t tt = order[i - 1];
+                order[i - 1] = order[r];
+                order[r] = tt;
+            }
+            for (uint64_t i = 0; i < p.n_blocks; ++i) acc += __ldcg(p.block_partials + order[i]);
+        } else {
+            for (uint64_t b = 0; b < p.n_blocks; ++b) acc += __ldcg(p.block_partials + b);
+        }
+        *p.result = acc;
+    }
+    if (threadIdx.x == 0) *p.ticket = 0u;
+}
+
+// Block stage (reference pairwise tree over W chunk results, reduction.hpp:253, :90-101) and
+// group stage (adjacent tree over G block results) for one tile, by `nwarps` warps starting at
+// warp index w0 of the caller's warp set (w = caller's index in that set).
+__device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t tile, const float* chunks,
+                                                  float* blocks, uint32_t w, uint32_t nwarps) {
+    const uint32_t W = p.W, G = p.G;
+    const unsigned lane = lane_id();
+    uint32_t P = 1;
+    while (P < W) P <<= 1;
+    for (uint32_t b = w; b < G; b += nwarps) {
+        float x = lane < W ? chunks[b * W + lane] : 0.0f;
+        for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
+        if (lane == 0) {
+            blocks[b] = x;
+            const uint64_t gb = tile * G + b;
+            if (gb < p.n_blocks) {
+                if (p.block_partials) p.block_partials[gb] = x;
+                if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void tile_tree_group(const SpParams& p, uint64_t tile, const float* blocks) {
+    const uint32_t G = p.G;
+    const unsigned lane = lane_id();
+    if (!p.group_partials) return;
+    const uint32_t seg = G >= 32 ? G / 32 : 1;
+    float x = 0.0f;
+    if (lane * seg < G) {
+        float loc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? blocks[lane * seg + i] : 0.0f;
+#pragma unroll
+        for (int w2 = 1; w2 < 8; w2 <<= 1)
+#pragma unroll
+            for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
+        x = loc[0];
+    }
+    x = warp_tree_xor(x);
+    if (lane == 0) p.group_partials[tile] = x;
+}
+
+}  // namespace pipe
+}  // namespace tcr

@@ -20,74 +20,17 @@
 
 #include "tcr_device.cuh"
 #include "tcr_kernels.h"
+#include "tcr_pipeline.cuh"
 
 namespace tcr {
 
 namespace {
 
+using namespace pipe;
+
 constexpr int kEpiWarp0 = 2;
 constexpr int kAccBufs = 8;         // TMEM accumulator ring depth
 constexpr uint32_t kRingBytes = 192 * 1024;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-// Watchdog: a pipeline bug must surface as a kernel error, never as a hung GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if (++spins == (1u << 28)) __trap();
-    }
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
-                                            uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
 
 // UMMA shared-memory matrix descriptor (sm_100: version 1 at bits 46-47).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -129,53 +72,6 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
 }
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ void named_bar(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-__device__ __forceinline__ float warp_tree_xor(float v) {
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const float o = __shfl_xor_sync(kFull, v, off);
-        v = (lane_id() & off) ? (o + v) : (v + o);
-    }
-    return v;
-}
-
-// Canonical adjacent tree over vals[0,count) (zero padded to a power of two) by the first
-// `nthr` threads (power of two, multiple of 32); every thread of the CTA must call it.
-__device__ float cta_tree(const float* vals, uint64_t count, float* s_scratch, unsigned nthr) {
-    uint64_t P = 1;
-    while (P < count) P <<= 1;
-    uint64_t seg = P / nthr;
-    if (seg == 0) seg = 1;
-    float acc = 0.0f;
-    const uint64_t lo = uint64_t(threadIdx.x) * seg;
-    if (threadIdx.x < nthr && lo < P) {
-        float stk[40];
-        int top = 0;
-        for (uint64_t i = 0; i < seg; ++i) {
-            const uint64_t idx = lo + i;
-            float v = idx < count ? __ldcg(vals + idx) : 0.0f;
-            for (uint64_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
-            stk[top++] = v;
-        }
-        acc = stk[0];
-    }
-    if (threadIdx.x < nthr) {
-        acc = warp_tree_xor(acc);
-        if (lane_id() == 0) s_scratch[threadIdx.x >> 5] = acc;
-    }
-    __syncthreads();
-    float r = 0.0f;
-    if (threadIdx.x < 32) {
-        r = lane_id() < (nthr >> 5) ? s_scratch[lane_id()] : 0.0f;
-        r = warp_tree_xor(r);
-    }
-    __syncthreads();
-    return r;
-}
 
 constexpr int kEpiGroups = 3;                         // epilogue warpgroups, round-robin over slots
 constexpr int kTcThreads = 64 + 128 * kEpiGroups;       // TMA warp + MMA warp + epilogue
@@ -365,35 +261,10 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                 named_bar(bar_id, 128);
                 if (s_own[eg]) {
                     float* blocks = s_block + buf * kMaxChunksPerGroup;
-                    // block stage: pairwise tree over W chunk results (reduction.hpp:253, :90-101)
-                    for (uint32_t b = w4; b < G; b += 4) {
-                        float x = lane < W ? chunks[b * W + lane] : 0.0f;
-                        for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
-                        if (lane == 0) {
-                            blocks[b] = x;
-                            const uint64_t gb = tile * G + b;
-                            if (p.block_partials) p.block_partials[gb] = x;
-                            if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
-                        }
-                    }
+                    tile_trees_blocks(p, tile, chunks, blocks, w4, 4);
                     named_bar(bar_id, 128);
                     if (w4 == 0) {
-                        if (p.group_partials) {
-                            const uint32_t seg = G >= 32 ? G / 32 : 1;
-                            float x = 0.0f;
-                            if (lane * seg < G) {
-                                float loc[8];
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? blocks[lane * seg + i] : 0.0f;
-#pragma unroll
-                                for (int w2 = 1; w2 < 8; w2 <<= 1)
-#pragma unroll
-                                    for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
-                                x = loc[0];
-                            }
-                            x = warp_tree_xor(x);
-                            if (lane == 0) p.group_partials[tile] = x;
-                        }
+                        tile_tree_group(p, tile, blocks);
                         if (lane == 0) s_done[buf] = 0;
                     }
                     named_bar(bar_id, 128);
@@ -410,43 +281,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
     tc_fence_after();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
 
-    if (p.finalize == kFinTree || p.finalize == kFinOrdered) {
-        if (threadIdx.x == 0) {
-            const unsigned tk = atomicAdd(p.ticket, 1u);
-            *s_last = (tk == gridDim.x - 1);
-        }
-        __syncthreads();
-        if (*s_last) {
-            __threadfence();
-            if (p.finalize == kFinTree) {
-                const float r = cta_tree(p.group_partials, p.n_groups, s_scratch, 256);
-                if (threadIdx.x == 0) *p.result = r;
-            } else if (threadIdx.x == 0) {
-                float acc = 0.0f;
-                if (p.atomic_order == 1) {
-                    uint32_t* order = p.order_scratch;
-                    for (uint64_t i = 0; i < p.n_blocks; ++i) order[i] = uint32_t(i);
-                    uint64_t st = p.atomic_seed;
-                    for (uint64_t i = p.n_blocks; i > 1; --i) {
-                        st += 0x9E3779B97F4A7C15ull;
-                        uint64_t z = st;
-                        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-                        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-                        z ^= z >> 31;
-                        const uint64_t r = z % i;
-                        const uint32_t tt = order[i - 1];
-                        order[i - 1] = order[r];
-                        order[r] = tt;
-                    }
-                    for (uint64_t i = 0; i < p.n_blocks; ++i) acc += __ldcg(p.block_partials + order[i]);
-                } else {
-                    for (uint64_t b = 0; b < p.n_blocks; ++b) acc += __ldcg(p.block_partials + b);
-                }
-                *p.result = acc;
-            }
-            if (threadIdx.x == 0) *p.ticket = 0u;
-        }
-    }
+    finalize_last_cta(p, s_scratch, s_last, 256);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -40,10 +40,11 @@ class Finalize(enum.IntEnum):         # device-side combine of block results (tc
     atomic = 2
 
 
-class Engine(enum.IntEnum):
+class Engine(enum.IntEnum):          # tcreduce_b200.h tcr_engine
     auto = 0
-    mma_sync = 1
-    tcgen05 = 2
+    mma_sync = 1          # TMA bulk ring + ldmatrix.trans + HMMA
+    tcgen05 = 2           # tensor-map TMA (SW32) + tcgen05.mma into TMEM
+    mma_sync_regs = 3     # 128-bit loads into registers + MOVM + HMMA (tails, fp32 input)
 
 
 class DistKind(enum.IntEnum):         # harness.hpp:20
@@ -198,3 +199,7 @@ def counters(n: int, cfg: ReductionConfig) -> ReductionOutcome:
 
 def last_launch_count() -> int:
     return _capi.load().tcr_last_launch_count()
+
+
+def last_engine() -> Engine:
+    return Engine(_capi.load().tcr_last_engine())
