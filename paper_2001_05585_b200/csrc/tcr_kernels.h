@@ -51,7 +51,8 @@ struct SpParams {
     int32_t atomic_order;
     uint64_t atomic_seed;
     // Profiling hook (env TCR_DEBUG_MODE, never set in production): tcgen05 engine only --
-    // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map.
+    // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
+    // 3 = TMA + MMA without the epilogue (accumulators overwritten unread).
     int32_t debug_mode;
 };
 
