@@ -28,7 +28,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 DEV = "cuda:0"
 
 
-ENGINES = [T.Engine.mma_sync, T.Engine.tcgen05]
+ENGINES = [T.Engine.mma_sync, T.Engine.tcgen05, T.Engine.mma_sync_regs]
 
 
 def cfg16(R=1, B=1024, **kw):
@@ -131,14 +131,15 @@ def test_block_results_vs_oracle(oracle, dist, seed, R, B, engine):
 
 @pytest.mark.parametrize("R,B", [(1, 1024), (4, 128), (3, 96), (5, 32), (2, 256)])
 def test_engines_agree(oracle, R, B):
-    """tcgen05/TMEM chain and mma.sync chain give the same block results."""
+    """The three engines (register mma.sync, TMA-staged mma.sync, tcgen05/TMEM) agree."""
     h = oracle.generate_f16("uniform", 7, (1 << 22) + 4321)
     xd = to_dev_f16(h)
-    a = T.block_results(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync)).cpu().numpy()
-    b = T.block_results(xd, cfg16(R=R, B=B, engine=T.Engine.tcgen05)).cpu().numpy()
-    same = (a.view(np.uint32) == b.view(np.uint32)).mean()
-    print(f"\nengines R={R} B={B}: identical blocks {same:.6f}")
-    assert same >= 0.99 and np.abs(a - b).max() <= 2.0 ** -20 * np.abs(a).max()
+    a = T.block_results(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync_regs)).cpu().numpy()
+    for eng in (T.Engine.mma_sync, T.Engine.tcgen05):
+        b = T.block_results(xd, cfg16(R=R, B=B, engine=eng)).cpu().numpy()
+        same = (a.view(np.uint32) == b.view(np.uint32)).mean()
+        print(f"\nengines regs vs {eng.name} R={R} B={B}: identical blocks {same:.6f}")
+        assert same >= 0.99 and np.abs(a - b).max() <= 2.0 ** -20 * np.abs(a).max()
 
 
 @pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1), ("uniform", 11)])
