@@ -25,7 +25,7 @@ namespace {
 
 using namespace pipe;
 
-constexpr int kBkConsumers = 8;                       // consumer warps
+constexpr int kBkConsumers = 16;                      // consumer warps
 constexpr int kBkThreads = 32 * (1 + kBkConsumers);
 constexpr uint32_t kBkRingBytes = 192 * 1024;
 constexpr int kBkTileBufs = 2;
@@ -165,7 +165,7 @@ sp_bulk_kernel(const SpParams p, const uint32_t SC, const uint32_t ns, const uin
                 const uint32_t rs = t % ns, ph = (t / ns) & 1;
                 mbar_wait(&full[rs], ph);
                 const uint32_t sa = smem_u32(ring + size_t(rs) * slot_bytes);
-                bk_warp_chunks<RT>(sa, lane_off, R, scw, cw, chunks, s * SC, ovf);
+                if (p.debug_mode != 1) bk_warp_chunks<RT>(sa, lane_off, R, scw, cw, chunks, s * SC, ovf);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[rs]);
             }
@@ -179,7 +179,7 @@ sp_bulk_kernel(const SpParams p, const uint32_t SC, const uint32_t ns, const uin
     }
     __threadfence();
     __syncthreads();
-    finalize_last_cta(p, s_scratch, s_last, 256);
+    finalize_last_cta(p, s_scratch, s_last, 512);
 }
 
 }  // namespace
@@ -190,7 +190,7 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC_out, uint32_t* ns_out) {
     // slot = SC chunks (a multiple of the consumer count), ~32 KB, dividing the tile
     uint32_t SC = 0;
     for (uint32_t cand = 256; cand >= uint32_t(kBkConsumers); cand -= kBkConsumers) {
-        if (cand % kBkConsumers == 0 && cg % cand == 0 && uint64_t(cand) * g.R * 512u <= 32768u) {
+        if (cand % kBkConsumers == 0 && cg % cand == 0 && uint64_t(cand) * g.R * 512u <= 49152u) {
             SC = cand;
             break;
         }
