@@ -57,12 +57,14 @@ typedef enum { TCR_FINALIZE_TREE = 0, TCR_FINALIZE_ORDERED = 1, TCR_FINALIZE_ATO
  *   MMA_SYNC      -- 1-D TMA bulk copies into a smem ring, ldmatrix.trans + HMMA.16816 chain
  *   TCGEN05       -- tensor-map TMA (SWIZZLE_32B) ring, single-thread tcgen05.mma into TMEM
  *   MMA_SYNC_REGS -- streaming 128-bit loads straight into registers, MOVM + HMMA (also the
- *                    fp32 convert-on-load path and the ragged tail of every engine) */
+ *                    fp32 convert-on-load path and the ragged tail of the TMA engines)
+ *   MMA_SYNC_ASYNC -- per-warp cp.async (LDGSTS) ring, ldmatrix.trans + HMMA */
 typedef enum {
     TCR_ENGINE_AUTO = 0,
     TCR_ENGINE_MMA_SYNC = 1,
     TCR_ENGINE_TCGEN05 = 2,
-    TCR_ENGINE_MMA_SYNC_REGS = 3
+    TCR_ENGINE_MMA_SYNC_REGS = 3,
+    TCR_ENGINE_MMA_SYNC_ASYNC = 4
 } tcr_engine;
 
 /* ReductionConfig -- reduction.hpp:39-57 (first seven fields, same meaning and defaults

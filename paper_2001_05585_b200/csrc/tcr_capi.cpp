@@ -120,7 +120,7 @@ int validate_cfg(const tcr_config* c) {
 int check_supported(const tcr_config* c) {
     if (c->m != 16)
         return fail(TCR_NOT_SUPPORTED, "single_pass on B200 currently implements m = 16 (the hardware fragment)");
-    if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_MMA_SYNC_REGS)
+    if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_MMA_SYNC_ASYNC)
         return fail(TCR_INVALID_ARGUMENT, "unknown engine");
     return TCR_OK;
 }
@@ -128,7 +128,9 @@ int check_supported(const tcr_config* c) {
 // Engine choice for the full groups: explicit, or AUTO = the measured winner when the geometry
 // allows it.  The register engine always takes the ragged tail and the fp32 input path.
 int pick_engine(const tcr_config* c, const tcr::SpGeometry& g, bool f32) {
-    if (f32 || g.n / g.group_elems == 0) return TCR_ENGINE_MMA_SYNC_REGS;
+    if (f32) return TCR_ENGINE_MMA_SYNC_REGS;
+    if (c->engine == TCR_ENGINE_MMA_SYNC_ASYNC) return TCR_ENGINE_MMA_SYNC_ASYNC;
+    if (g.n / g.group_elems == 0) return TCR_ENGINE_MMA_SYNC_REGS;
     uint32_t a, b;
     const bool tc_ok = tcr::tc05_plan(g, &a, &b);
     const bool bk_ok = tcr::bulk_plan(g, &a, &b);
@@ -205,8 +207,15 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;
     }
-    const int engine = (g0 == 0 && g1 == g.n_groups) ? pick_engine(c, g, f32) : TCR_ENGINE_MMA_SYNC_REGS;
+    int engine = (g0 == 0 && g1 == g.n_groups) ? pick_engine(c, g, f32) : TCR_ENGINE_MMA_SYNC_REGS;
+    if (!f32 && c->engine == TCR_ENGINE_MMA_SYNC_ASYNC) engine = TCR_ENGINE_MMA_SYNC_ASYNC;
     g_engine = engine;
+    if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
+        const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, uint64_t(tcr::async_max_grid(c->R))));
+        TCR_CUDA(tcr::launch_async(p, grid, s));
+        ++g_launches;
+        return TCR_OK;
+    }
     if (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC) {
         // full groups on a TMA-fed persistent engine (one CTA per SM), the ragged tail (< 1 group)
         // on the register engine; the last launch finalises

@@ -69,6 +69,11 @@ cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles
 // TMA-staged mma.sync engine (1-D bulk copies into a smem ring, ldmatrix.trans + HMMA) over the
 // first n_tiles FULL groups.  bulk_plan picks the slot (SC chunks) and ring depth.
 bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
+
+// Per-warp cp.async pipeline engine (LDGSTS ring per warp, ldmatrix.trans + HMMA); handles any
+// group range including the ragged tail (zero-fill copies).  binary16 input.
+int async_max_grid(uint32_t R);
+cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
 cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
 int single_pass_m16_max_grid(bool f32_input, uint32_t R);
 

@@ -1,0 +1,191 @@
+// tcr_sp_async.cu -- single-pass chained reduction, m = 16: per-warp cp.async pipeline engine.
+//
+// Same element partition, block stage and group stage as the other engines (reference
+// reduction.hpp:164-184, :238-275).  Every warp owns a private ring of D fragment stages
+// (512 B each) in shared memory and streams its own warp-chunks through it:
+//
+//   cp.async.cg 16 B per lane (LDGSTS, L1 bypass) -> stage (f + D-1) % D, one commit group per
+//   fragment; cp.async.wait_group(D-1) retires fragment f; ONE ldmatrix.x4.trans hands every
+//   lane the A fragment whose row j is column j of the 16x16 fragment (all 16 k), ONE
+//   HMMA.16816 against ones accumulates C_r = ones x M_r + C_{r-1} (reduction.hpp:177).
+//   C_R -> binary16 and the finishing HMMA run once per two chunks.
+//
+// No CTA-wide synchronisation inside the stream: D-1 fragments per warp are always in flight
+// without holding registers, and the zero-fill form of cp.async gives the reference's zero
+// padding (reduction.hpp:244-245) for the ragged tail for free.  The destination of each
+// 16-byte line is XOR-swizzled on row bit 2 so the transposing ldmatrix is bank-conflict free.
+#include <cuda_runtime.h>
+
+#include "tcr_device.cuh"
+#include "tcr_kernels.h"
+#include "tcr_pipeline.cuh"
+
+namespace tcr {
+
+namespace {
+
+using namespace pipe;
+
+constexpr int kAsWarps = 8;
+constexpr int kAsThreads = 32 * kAsWarps;
+constexpr int kAsDepth = 8;                          // fragment stages per warp
+constexpr int kAsStageBytes = 512;
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& d0, uint32_t& d1, uint32_t& d2, uint32_t& d3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(d3)
+                 : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+// byte offset of line (k, half) of a fragment stage, swizzled: half ^= bit 2 of k
+__device__ __forceinline__ uint32_t swz(uint32_t k, uint32_t half) { return 32u * k + 16u * (half ^ ((k >> 2) & 1u)); }
+
+template <int RT>
+__device__ __forceinline__ void as_group(const SpParams& p, uint64_t gi, uint32_t ring_saddr, float* s_chunk,
+                                         bool& ovf) {
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned c = lane & 3u;
+    const uint32_t R = RT > 0 ? uint32_t(RT) : p.R;
+    const uint32_t Cg = p.G * p.W;
+    const uint32_t nch = Cg > warp ? (Cg - warp + kAsWarps - 1) / kAsWarps : 0;
+    const uint32_t F = nch * R;
+    const uint64_t ce = uint64_t(R) * 256u;
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint64_t n = p.n;
+    // copy side: lane copies bytes [16*lane, 16*lane+16) of the fragment = line (k = lane/2, half = lane&1)
+    const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
+    // ldmatrix side: matrix mi = lane>>3 supplies line (k = (lane&7) + 8*(mi>>1), half = mi&1)
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_off = swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+
+    // element index of fragment f's first element for this warp
+    auto frag_elem = [&](uint32_t f) -> uint64_t {
+        const uint32_t ci = f / R, r = f - ci * R;
+        return (gi * uint64_t(Cg) + warp + uint64_t(ci) * kAsWarps) * ce + uint64_t(r) * 256u;
+    };
+    auto issue = [&](uint32_t f) {
+        if (f < F) {
+            const uint64_t e = frag_elem(f) + 8u * lane;
+            const uint32_t bytes = e + 8 <= n ? 16u : (e < n ? uint32_t(n - e) * 2u : 0u);
+            cp_async16(ring_saddr + (f % kAsDepth) * kAsStageBytes + cp_dst, x + (e < n ? e : 0), bytes);
+        }
+        cp_async_commit();
+    };
+
+#pragma unroll
+    for (int f = 0; f < kAsDepth - 1; ++f) issue(uint32_t(f));
+
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t r = 0, ci = 0, pend = 0;
+    uint32_t a01p = 0, a23p = 0;   // packed binary16 partials of the pending (even) chunk
+    for (uint32_t f = 0; f < F; ++f) {
+        issue(f + kAsDepth - 1);
+        cp_async_wait<kAsDepth - 1>();
+        __syncwarp();
+        uint32_t d0, d1, d2, d3;
+        ldsm_x4_trans(ring_saddr + (f % kAsDepth) * kAsStageBytes + ld_off, d0, d1, d2, d3);
+        __syncwarp();  // every lane has its registers before the stage is refilled
+        mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
+        if (++r == R) {
+            // thread (g, c): acc[0] = C_R[j = g], acc[2] = C_R[j = g + 8] -> binary16 (:179-181)
+            const uint32_t pk = uint32_t(f32_to_h(acc[0])) | (uint32_t(f32_to_h(acc[2])) << 16);
+            const uint32_t vA = __shfl_sync(kFull, pk, 8 * c);        // (h_2c,   h_2c+8)
+            const uint32_t vB = __shfl_sync(kFull, pk, 8 * c + 4);    // (h_2c+1, h_2c+9)
+            const uint32_t a01 = prmt(vA, vB, 0x5410), a23 = prmt(vA, vB, 0x7632);
+            if (pend) {
+                float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                // finishing MMA (reduction.hpp:182): rows 0-7 chunk ci-1, rows 8-15 chunk ci
+                mma_16816(fin, a01p, a01, a23p, a23, kOnesF16x2, kOnesF16x2);
+                ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
+                if (lane == 0) {
+                    s_chunk[warp + (ci - 1) * kAsWarps] = fin[0];
+                    s_chunk[warp + ci * kAsWarps] = fin[2];
+                }
+                pend = 0;
+            } else {
+                a01p = a01;
+                a23p = a23;
+                pend = 1;
+            }
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            r = 0;
+            ++ci;
+        }
+    }
+    if (pend) {
+        float fin[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_16816(fin, a01p, a01p, a23p, a23p, kOnesF16x2, kOnesF16x2);
+        ovf |= !isfinite(fin[0]);
+        if (lane == 0) s_chunk[warp + (ci - 1) * kAsWarps] = fin[0];
+    }
+    cp_async_wait<0>();
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kAsThreads, 4) sp_async_kernel(const SpParams p) {
+    __shared__ __align__(128) unsigned char s_ring[kAsWarps * kAsDepth * kAsStageBytes];
+    __shared__ float s_chunk[kMaxChunksPerGroup];
+    __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ float s_scratch[32];
+    __shared__ int s_last;
+    const unsigned warp = threadIdx.x >> 5;
+    const uint32_t ring = smem_u32(s_ring) + warp * kAsDepth * kAsStageBytes;
+    bool ovf = false;
+    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+        as_group<RT>(p, gi, ring, s_chunk, ovf);
+        __syncthreads();
+        tile_trees_blocks(p, gi, s_chunk, s_block, warp, kAsWarps);
+        __syncthreads();
+        if (warp == 0) tile_tree_group(p, gi, s_block);
+        __syncthreads();
+    }
+    if (__any_sync(kFull, ovf) && lane_id() == 0) atomicOr(p.overflow, 1u);
+    __threadfence();
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kAsThreads);
+}
+
+using AsKernel = void (*)(SpParams);
+
+AsKernel pick(uint32_t R) {
+    switch (R) {
+    case 1: return sp_async_kernel<1>;
+    case 2: return sp_async_kernel<2>;
+    case 3: return sp_async_kernel<3>;
+    case 4: return sp_async_kernel<4>;
+    case 5: return sp_async_kernel<5>;
+    default: return sp_async_kernel<0>;
+    }
+}
+
+}  // namespace
+
+int async_max_grid(uint32_t R) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pick(R), kAsThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    return per_sm * sm_count();
+}
+
+cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s) {
+    pick(p.R)<<<grid, kAsThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace tcr

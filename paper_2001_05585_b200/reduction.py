@@ -45,6 +45,7 @@ class Engine(enum.IntEnum):          # tcreduce_b200.h tcr_engine
     mma_sync = 1          # TMA bulk ring + ldmatrix.trans + HMMA
     tcgen05 = 2           # tensor-map TMA (SW32) + tcgen05.mma into TMEM
     mma_sync_regs = 3     # 128-bit loads into registers + MOVM + HMMA (tails, fp32 input)
+    mma_sync_async = 4    # per-warp cp.async ring + ldmatrix.trans + HMMA
 
 
 class DistKind(enum.IntEnum):         # harness.hpp:20

@@ -28,7 +28,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 DEV = "cuda:0"
 
 
-ENGINES = [T.Engine.mma_sync, T.Engine.tcgen05, T.Engine.mma_sync_regs]
+ENGINES = [T.Engine.mma_sync, T.Engine.tcgen05, T.Engine.mma_sync_regs, T.Engine.mma_sync_async]
 
 
 def cfg16(R=1, B=1024, **kw):
@@ -135,7 +135,7 @@ def test_engines_agree(oracle, R, B):
     h = oracle.generate_f16("uniform", 7, (1 << 22) + 4321)
     xd = to_dev_f16(h)
     a = T.block_results(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync_regs)).cpu().numpy()
-    for eng in (T.Engine.mma_sync, T.Engine.tcgen05):
+    for eng in (T.Engine.mma_sync, T.Engine.tcgen05, T.Engine.mma_sync_async):
         b = T.block_results(xd, cfg16(R=R, B=B, engine=eng)).cpu().numpy()
         same = (a.view(np.uint32) == b.view(np.uint32)).mean()
         print(f"\nengines regs vs {eng.name} R={R} B={B}: identical blocks {same:.6f}")
