@@ -137,6 +137,74 @@ __device__ __forceinline__ void as_group(const SpParams& p, uint64_t gi, uint32_
     cp_async_wait<0>();
 }
 
+
+// Static fast path: full group, RT in {1, 2, 4} (RT | kAsDepth), and every warp's fragment count a
+// multiple of kAsDepth.  Stage indices, chunk boundaries and finishing pairs are compile-time.
+template <int RT>
+__device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, uint32_t ring_saddr, float* s_chunk,
+                                                bool& ovf) {
+    static_assert(kAsDepth % (2 * RT) == 0, "static path needs 2*RT | depth");
+    constexpr uint32_t CPI = kAsDepth / RT;                 // chunks per outer iteration
+    constexpr uint64_t CE = uint64_t(RT) * 256u;            // chunk elements
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned c = lane & 3u;
+    const uint32_t Cg = p.G * p.W;
+    const uint32_t nch = Cg / kAsWarps;
+    const uint32_t iters = nch / CPI;
+    const uint16_t* gp = static_cast<const uint16_t*>(p.x) + (gi * uint64_t(Cg) + warp) * CE + 8u * lane;
+    const uint32_t cp_dst = ring_saddr + swz(lane >> 1, lane & 1u);
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_base = ring_saddr + swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+    // global element offset of warp-local fragment g (chunk g/RT, fragment g%RT)
+#define TCR_FRAG_OFF(g) (uint64_t((g) / RT) * kAsWarps * CE + uint64_t((g) % RT) * 256u)
+#pragma unroll
+    for (int u = 0; u < kAsDepth - 1; ++u) {
+        cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
+        cp_async_commit();
+    }
+    float* out = s_chunk + warp;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint16_t* gq = gp + uint64_t(it) * CPI * kAsWarps * CE;
+        uint32_t a01p = 0, a23p = 0;
+        float acc[4];
+#pragma unroll
+        for (int u = 0; u < kAsDepth; ++u) {
+            // refill the stage consumed one step ago with fragment it*D + u + D-1
+            if (it + 1 < iters || u == 0)
+                cp_async16(cp_dst + ((u + kAsDepth - 1) % kAsDepth) * kAsStageBytes, gq + TCR_FRAG_OFF(u + kAsDepth - 1),
+                           16u);
+            cp_async_commit();
+            cp_async_wait<kAsDepth - 1>();
+            __syncwarp();
+            uint32_t d0, d1, d2, d3;
+            ldsm_x4_trans(ld_base + u * kAsStageBytes, d0, d1, d2, d3);
+            if (u % RT == 0) acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
+            if (u % RT == RT - 1) {
+                const uint32_t pk = uint32_t(f32_to_h(acc[0])) | (uint32_t(f32_to_h(acc[2])) << 16);
+                const uint32_t vA = __shfl_sync(kFull, pk, 8 * c);
+                const uint32_t vB = __shfl_sync(kFull, pk, 8 * c + 4);
+                const uint32_t a01 = prmt(vA, vB, 0x5410), a23 = prmt(vA, vB, 0x7632);
+                if ((u / RT) % 2 == 0) {
+                    a01p = a01;
+                    a23p = a23;
+                } else {
+                    float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                    mma_16816(fin, a01p, a01, a23p, a23, kOnesF16x2, kOnesF16x2);
+                    ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
+                    if (lane == 0) {
+                        const uint32_t ci = it * CPI + u / RT;     // odd chunk of the pair
+                        out[(ci - 1) * kAsWarps] = fin[0];
+                        out[ci * kAsWarps] = fin[2];
+                    }
+                }
+            }
+        }
+    }
+#undef TCR_FRAG_OFF
+    cp_async_wait<0>();
+}
+
 template <int RT>
 __global__ void __launch_bounds__(kAsThreads, 4) sp_async_kernel(const SpParams p) {
     __shared__ __align__(128) unsigned char s_ring[kAsWarps * kAsDepth * kAsStageBytes];
@@ -147,8 +215,18 @@ __global__ void __launch_bounds__(kAsThreads, 4) sp_async_kernel(const SpParams 
     const unsigned warp = threadIdx.x >> 5;
     const uint32_t ring = smem_u32(s_ring) + warp * kAsDepth * kAsStageBytes;
     bool ovf = false;
+    const uint64_t full_groups = p.n / (uint64_t(p.G) * p.W * p.chunk_elems);
+    const uint32_t Cg = p.G * p.W;
+    bool static_ok = false;
+    if constexpr (RT == 1 || RT == 2 || RT == 4)
+        static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % kAsDepth == 0;
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
-        as_group<RT>(p, gi, ring, s_chunk, ovf);
+        if constexpr (RT == 1 || RT == 2 || RT == 4) {
+            if (static_ok && gi < full_groups) as_group_static<RT>(p, gi, ring, s_chunk, ovf);
+            else as_group<RT>(p, gi, ring, s_chunk, ovf);
+        } else {
+            as_group<RT>(p, gi, ring, s_chunk, ovf);
+        }
         __syncthreads();
         tile_trees_blocks(p, gi, s_chunk, s_block, warp, kAsWarps);
         __syncthreads();
