@@ -52,7 +52,8 @@ struct SpParams {
     uint64_t atomic_seed;
     // Profiling hook (env TCR_DEBUG_MODE, never set in production): tcgen05 engine only --
     // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
-    // 3 = TMA + MMA without the epilogue (accumulators overwritten unread).
+    // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
+    // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
     int32_t debug_mode;
 };
 

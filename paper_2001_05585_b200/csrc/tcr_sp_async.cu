@@ -28,7 +28,6 @@ using namespace pipe;
 
 constexpr int kAsWarps = 8;
 constexpr int kAsThreads = 32 * kAsWarps;
-constexpr int kAsDepth = 8;                          // fragment stages per warp
 constexpr int kAsStageBytes = 512;
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
@@ -56,7 +55,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 // byte offset of line (k, half) of a fragment stage, swizzled: half ^= bit 2 of k
 __device__ __forceinline__ uint32_t swz(uint32_t k, uint32_t half) { return 32u * k + 16u * (half ^ ((k >> 2) & 1u)); }
 
-template <int RT>
+template <int RT, int D>
 __device__ __forceinline__ void as_group(const SpParams& p, uint64_t gi, uint32_t ring_saddr, float* s_chunk,
                                          bool& ovf) {
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
@@ -83,23 +82,23 @@ __device__ __forceinline__ void as_group(const SpParams& p, uint64_t gi, uint32_
         if (f < F) {
             const uint64_t e = frag_elem(f) + 8u * lane;
             const uint32_t bytes = e + 8 <= n ? 16u : (e < n ? uint32_t(n - e) * 2u : 0u);
-            cp_async16(ring_saddr + (f % kAsDepth) * kAsStageBytes + cp_dst, x + (e < n ? e : 0), bytes);
+            cp_async16(ring_saddr + (f % D) * kAsStageBytes + cp_dst, x + (e < n ? e : 0), bytes);
         }
         cp_async_commit();
     };
 
 #pragma unroll
-    for (int f = 0; f < kAsDepth - 1; ++f) issue(uint32_t(f));
+    for (int f = 0; f < D - 1; ++f) issue(uint32_t(f));
 
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     uint32_t r = 0, ci = 0, pend = 0;
     uint32_t a01p = 0, a23p = 0;   // packed binary16 partials of the pending (even) chunk
     for (uint32_t f = 0; f < F; ++f) {
-        issue(f + kAsDepth - 1);
-        cp_async_wait<kAsDepth - 1>();
+        issue(f + D - 1);
+        cp_async_wait<D - 1>();
         __syncwarp();
         uint32_t d0, d1, d2, d3;
-        ldsm_x4_trans(ring_saddr + (f % kAsDepth) * kAsStageBytes + ld_off, d0, d1, d2, d3);
+        ldsm_x4_trans(ring_saddr + (f % D) * kAsStageBytes + ld_off, d0, d1, d2, d3);
         __syncwarp();  // every lane has its registers before the stage is refilled
         mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
         if (++r == R) {
@@ -138,13 +137,13 @@ __device__ __forceinline__ void as_group(const SpParams& p, uint64_t gi, uint32_
 }
 
 
-// Static fast path: full group, RT in {1, 2, 4} (RT | kAsDepth), and every warp's fragment count a
-// multiple of kAsDepth.  Stage indices, chunk boundaries and finishing pairs are compile-time.
-template <int RT>
+// Static fast path: full group, RT in {1, 2, 4} (RT | D), and every warp's fragment count a
+// multiple of D.  Stage indices, chunk boundaries and finishing pairs are compile-time.
+template <int RT, int D>
 __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, uint32_t ring_saddr, float* s_chunk,
                                                 bool& ovf) {
-    static_assert(kAsDepth % (2 * RT) == 0, "static path needs 2*RT | depth");
-    constexpr uint32_t CPI = kAsDepth / RT;                 // chunks per outer iteration
+    static_assert(D % (2 * RT) == 0, "static path needs 2*RT | depth");
+    constexpr uint32_t CPI = D / RT;                 // chunks per outer iteration
     constexpr uint64_t CE = uint64_t(RT) * 256u;            // chunk elements
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned c = lane & 3u;
@@ -158,7 +157,7 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
     // global element offset of warp-local fragment g (chunk g/RT, fragment g%RT)
 #define TCR_FRAG_OFF(g) (uint64_t((g) / RT) * kAsWarps * CE + uint64_t((g) % RT) * 256u)
 #pragma unroll
-    for (int u = 0; u < kAsDepth - 1; ++u) {
+    for (int u = 0; u < D - 1; ++u) {
         cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
         cp_async_commit();
     }
@@ -168,13 +167,13 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
         uint32_t a01p = 0, a23p = 0;
         float acc[4];
 #pragma unroll
-        for (int u = 0; u < kAsDepth; ++u) {
+        for (int u = 0; u < D; ++u) {
             // refill the stage consumed one step ago with fragment it*D + u + D-1
             if (it + 1 < iters || u == 0)
-                cp_async16(cp_dst + ((u + kAsDepth - 1) % kAsDepth) * kAsStageBytes, gq + TCR_FRAG_OFF(u + kAsDepth - 1),
+                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + TCR_FRAG_OFF(u + D - 1),
                            16u);
             cp_async_commit();
-            cp_async_wait<kAsDepth - 1>();
+            cp_async_wait<D - 1>();
             __syncwarp();
             uint32_t d0, d1, d2, d3;
             ldsm_x4_trans(ld_base + u * kAsStageBytes, d0, d1, d2, d3);
@@ -205,27 +204,40 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
     cp_async_wait<0>();
 }
 
+// Ring depth per chain length: 2*R | D keeps every stage index and chunk pair compile-time.
+template <int RT> struct AsDepth { static constexpr int value = 8; };
+template <> struct AsDepth<1> { static constexpr int value = 16; };
+template <> struct AsDepth<2> { static constexpr int value = 16; };
+template <> struct AsDepth<3> { static constexpr int value = 12; };
+template <> struct AsDepth<4> { static constexpr int value = 16; };
+template <> struct AsDepth<5> { static constexpr int value = 10; };
+
 template <int RT>
-__global__ void __launch_bounds__(kAsThreads, 4) sp_async_kernel(const SpParams p) {
-    __shared__ __align__(128) unsigned char s_ring[kAsWarps * kAsDepth * kAsStageBytes];
+constexpr uint32_t as_smem_bytes() {
+    return uint32_t(kAsWarps) * AsDepth<RT>::value * kAsStageBytes;
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
+    constexpr int D = AsDepth<RT>::value;
+    extern __shared__ __align__(128) unsigned char s_ring[];
     __shared__ float s_chunk[kMaxChunksPerGroup];
     __shared__ float s_block[kMaxChunksPerGroup];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
     const unsigned warp = threadIdx.x >> 5;
-    const uint32_t ring = smem_u32(s_ring) + warp * kAsDepth * kAsStageBytes;
+    const uint32_t ring = smem_u32(s_ring) + warp * D * kAsStageBytes;
     bool ovf = false;
     const uint64_t full_groups = p.n / (uint64_t(p.G) * p.W * p.chunk_elems);
     const uint32_t Cg = p.G * p.W;
     bool static_ok = false;
-    if constexpr (RT == 1 || RT == 2 || RT == 4)
-        static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % kAsDepth == 0;
+    if constexpr (RT > 0) static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % D == 0;
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
-        if constexpr (RT == 1 || RT == 2 || RT == 4) {
-            if (static_ok && gi < full_groups) as_group_static<RT>(p, gi, ring, s_chunk, ovf);
-            else as_group<RT>(p, gi, ring, s_chunk, ovf);
+        if constexpr (RT > 0) {
+            if (static_ok && gi < full_groups) as_group_static<RT, D>(p, gi, ring, s_chunk, ovf);
+            else as_group<RT, D>(p, gi, ring, s_chunk, ovf);
         } else {
-            as_group<RT>(p, gi, ring, s_chunk, ovf);
+            as_group<RT, D>(p, gi, ring, s_chunk, ovf);
         }
         __syncthreads();
         tile_trees_blocks(p, gi, s_chunk, s_block, warp, kAsWarps);
@@ -241,28 +253,50 @@ __global__ void __launch_bounds__(kAsThreads, 4) sp_async_kernel(const SpParams 
 
 using AsKernel = void (*)(SpParams);
 
-AsKernel pick(uint32_t R) {
+struct AsPick {
+    AsKernel fn;
+    uint32_t smem;
+};
+
+AsPick pick(uint32_t R) {
     switch (R) {
-    case 1: return sp_async_kernel<1>;
-    case 2: return sp_async_kernel<2>;
-    case 3: return sp_async_kernel<3>;
-    case 4: return sp_async_kernel<4>;
-    case 5: return sp_async_kernel<5>;
-    default: return sp_async_kernel<0>;
+    case 1: return {sp_async_kernel<1>, as_smem_bytes<1>()};
+    case 2: return {sp_async_kernel<2>, as_smem_bytes<2>()};
+    case 3: return {sp_async_kernel<3>, as_smem_bytes<3>()};
+    case 4: return {sp_async_kernel<4>, as_smem_bytes<4>()};
+    case 5: return {sp_async_kernel<5>, as_smem_bytes<5>()};
+    default: return {sp_async_kernel<0>, as_smem_bytes<0>()};
     }
+}
+
+bool as_attr_once() {
+    static bool done = false;
+    if (!done) {
+        for (uint32_t R = 0; R <= 5; ++R) {
+            const AsPick k = pick(R);
+            if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(k.smem)) != cudaSuccess)
+                return false;
+        }
+        done = true;
+    }
+    return true;
 }
 
 }  // namespace
 
 int async_max_grid(uint32_t R) {
+    as_attr_once();
+    const AsPick k = pick(R);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pick(R), kAsThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kAsThreads, k.smem);
     if (per_sm < 1) per_sm = 1;
     return per_sm * sm_count();
 }
 
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s) {
-    pick(p.R)<<<grid, kAsThreads, 0, s>>>(p);
+    if (!as_attr_once()) return cudaErrorInvalidValue;
+    const AsPick k = pick(p.R);
+    k.fn<<<grid, kAsThreads, k.smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -49,13 +49,18 @@ constexpr uint32_t kLayoutNone = 0, kLayoutSw32 = 6;
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (0u << 16) | ((16u >> 3) << 17) |
                             ((128u >> 4) << 24);
 
-__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate,
+                                         uint32_t idesc = kIdesc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+
+// Profiling-only instruction descriptors (debug modes 4/5): A K-major; N = 64.
+constexpr uint32_t kIdescKmajor = (1u << 4) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescN64 = (1u << 4) | (1u << 15) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -184,7 +189,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                         mbar_arrive(&empty[rs]);
                         continue;
                     }
-                    if (p.debug_mode != 3) mbar_wait(&tempty[ab], aph ^ 1);
+                    if (p.debug_mode < 3) mbar_wait(&tempty[ab], aph ^ 1);
                     tc_fence_after();
                     const uint32_t sbase = smem_u32(ring + size_t(rs) * slot_bytes);
 #pragma unroll
@@ -194,7 +199,14 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                             // 8 chunks of this MMA-group, fragment r: MN atoms (chunks) R*512 B apart,
                             // K groups of 8 rows 256 B apart
                             const uint32_t a = sbase + (8u * q * R + r) * 512u;
-                            umma_f16(d, umma_desc(a, R * 512u, 256u, kLayoutSw32), bdesc, r > 0 ? 1u : 0u);
+                            if (p.debug_mode == 4)        // timing only: A read K-major (wrong partition)
+                                umma_f16(tmem_base, umma_desc(a, 256u, R * 512u, kLayoutSw32), bdesc, r > 0 ? 1u : 0u,
+                                         kIdescKmajor);
+                            else if (p.debug_mode == 5)   // timing only: N = 64 into one accumulator
+                                umma_f16(tmem_base, umma_desc(a, R * 512u, 256u, kLayoutSw32), bdesc, r > 0 ? 1u : 0u,
+                                         kIdescN64);
+                            else
+                                umma_f16(d, umma_desc(a, R * 512u, 256u, kLayoutSw32), bdesc, r > 0 ? 1u : 0u);
                         }
                     }
                     umma_commit(&empty[rs]);   // smem slot reusable once these MMAs retire
@@ -211,7 +223,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
         const uint32_t c = lane & 3u;
         const int bar_id = 1 + int(eg);
         uint32_t t = 0, k = 0;
-        if (p.debug_mode == 1 || p.debug_mode == 3) n_tiles_epi = 0;
+        if (p.debug_mode == 1 || p.debug_mode >= 3) n_tiles_epi = 0;
         uint32_t P = 1;
         while (P < W) P <<= 1;
         for (uint64_t tile = blockIdx.x; tile < n_tiles_epi; tile += gridDim.x, ++k) {
