@@ -23,8 +23,6 @@
 namespace {
 
 thread_local std::string g_err;
-// Set from measurement: which engine AUTO uses when both apply.
-constexpr bool kAutoPrefersTc05 = false;
 thread_local int g_launches = 0;
 thread_local int g_engine = 0;  // engine that ran the full groups of the last call
 
@@ -129,20 +127,18 @@ int check_supported(const tcr_config* c) {
 // allows it.  The register engine always takes the ragged tail and the fp32 input path.
 int pick_engine(const tcr_config* c, const tcr::SpGeometry& g, bool f32) {
     if (f32) return TCR_ENGINE_MMA_SYNC_REGS;
-    if (c->engine == TCR_ENGINE_MMA_SYNC_ASYNC) return TCR_ENGINE_MMA_SYNC_ASYNC;
-    if (g.n / g.group_elems == 0) return TCR_ENGINE_MMA_SYNC_REGS;
     uint32_t a, b;
-    const bool tc_ok = tcr::tc05_plan(g, &a, &b);
-    const bool bk_ok = tcr::bulk_plan(g, &a, &b);
+    const bool full = g.n / g.group_elems > 0;
     switch (c->engine) {
-    case TCR_ENGINE_TCGEN05: return tc_ok ? TCR_ENGINE_TCGEN05 : TCR_ENGINE_MMA_SYNC_REGS;
-    case TCR_ENGINE_MMA_SYNC: return bk_ok ? TCR_ENGINE_MMA_SYNC : TCR_ENGINE_MMA_SYNC_REGS;
+    case TCR_ENGINE_TCGEN05: return full && tcr::tc05_plan(g, &a, &b) ? TCR_ENGINE_TCGEN05 : TCR_ENGINE_MMA_SYNC_REGS;
+    case TCR_ENGINE_MMA_SYNC: return full && tcr::bulk_plan(g, &a, &b) ? TCR_ENGINE_MMA_SYNC : TCR_ENGINE_MMA_SYNC_REGS;
     case TCR_ENGINE_MMA_SYNC_REGS: return TCR_ENGINE_MMA_SYNC_REGS;
+    case TCR_ENGINE_MMA_SYNC_ASYNC: return TCR_ENGINE_MMA_SYNC_ASYNC;
     default:
-        if (kAutoPrefersTc05 && tc_ok) return TCR_ENGINE_TCGEN05;
-        if (bk_ok) return TCR_ENGINE_MMA_SYNC;
-        if (tc_ok) return TCR_ENGINE_TCGEN05;
-        return TCR_ENGINE_MMA_SYNC_REGS;
+        // AUTO: the measured winner on B200 for binary16 input (DESIGN.md §3 table):
+        // per-warp cp.async pipeline 6.1 TB/s > TMA-bulk mma.sync 4.5 > register mma.sync 3.6 >
+        // tcgen05 2.8 (n = 2^30, R = 1, B = 1024)
+        return TCR_ENGINE_MMA_SYNC_ASYNC;
     }
 }
 
@@ -207,8 +203,10 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;
     }
-    int engine = (g0 == 0 && g1 == g.n_groups) ? pick_engine(c, g, f32) : TCR_ENGINE_MMA_SYNC_REGS;
-    if (!f32 && c->engine == TCR_ENGINE_MMA_SYNC_ASYNC) engine = TCR_ENGINE_MMA_SYNC_ASYNC;
+    int engine = pick_engine(c, g, f32);
+    // a partial group range (pipelined host path) can only run on engines that take any range
+    if ((g0 != 0 || g1 != g.n_groups) && (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC))
+        engine = TCR_ENGINE_MMA_SYNC_REGS;
     g_engine = engine;
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
         const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, uint64_t(tcr::async_max_grid(c->R))));
