@@ -30,9 +30,17 @@ constexpr int kAsWarps = 8;
 constexpr int kAsThreads = 32 * kAsWarps;
 constexpr int kAsStageBytes = 512;
 
+// L2 prefetch granularity of the 16-byte copies (PF: 0 none, 128, 256 bytes)
+template <int PF = 256>
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
-                 : "memory");
+    if constexpr (PF == 256)
+        asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
+                     : "memory");
+    else if constexpr (PF == 128)
+        asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
+                     : "memory");
+    else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -139,9 +147,12 @@ __device__ __forceinline__ void as_group(const SpParams& p, uint64_t gi, uint32_
 
 // Static fast path: full group, RT in {1, 2, 4} (RT | D), and every warp's fragment count a
 // multiple of D.  Stage indices, chunk boundaries and finishing pairs are compile-time.
+// The stream never drains between two static groups of the same CTA: the last D-1 refills of a
+// group fetch the first D-1 fragments of the next one (same stages, same commit-group count),
+// so memory stays busy through the block/group trees and the CTA barrier.
 template <int RT, int D>
 __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, uint32_t ring_saddr, float* s_chunk,
-                                                bool& ovf) {
+                                                bool& ovf, bool prologue, bool prefetch_next, uint64_t gnext) {
     static_assert(D % (2 * RT) == 0, "static path needs 2*RT | depth");
     constexpr uint32_t CPI = D / RT;                 // chunks per outer iteration
     constexpr uint64_t CE = uint64_t(RT) * 256u;            // chunk elements
@@ -156,11 +167,14 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
     const uint32_t ld_base = ring_saddr + swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
     // global element offset of warp-local fragment g (chunk g/RT, fragment g%RT)
 #define TCR_FRAG_OFF(g) (uint64_t((g) / RT) * kAsWarps * CE + uint64_t((g) % RT) * 256u)
+    if (prologue) {
 #pragma unroll
-    for (int u = 0; u < D - 1; ++u) {
-        cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
-        cp_async_commit();
+        for (int u = 0; u < D - 1; ++u) {
+            cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
+            cp_async_commit();
+        }
     }
+    const uint16_t* gn = static_cast<const uint16_t*>(p.x) + (gnext * uint64_t(Cg) + warp) * CE + 8u * lane;
     float* out = s_chunk + warp;
     for (uint32_t it = 0; it < iters; ++it) {
         const uint16_t* gq = gp + uint64_t(it) * CPI * kAsWarps * CE;
@@ -172,6 +186,8 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
             if (it + 1 < iters || u == 0)
                 cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + TCR_FRAG_OFF(u + D - 1),
                            16u);
+            else if (prefetch_next)   // stage u-1 <- fragment u-1 of the next group
+                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gn + TCR_FRAG_OFF(u - 1), 16u);
             cp_async_commit();
             cp_async_wait<D - 1>();
             __syncwarp();
@@ -201,7 +217,7 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
         }
     }
 #undef TCR_FRAG_OFF
-    cp_async_wait<0>();
+    if (!prefetch_next) cp_async_wait<0>();
 }
 
 // Ring depth per chain length: 2*R | D keeps every stage index and chunk pair compile-time.
@@ -232,10 +248,18 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     const uint32_t Cg = p.G * p.W;
     bool static_ok = false;
     if constexpr (RT > 0) static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % D == 0;
+    bool prefetched = false;   // this group's first D-1 fragments are already in flight
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
         if constexpr (RT > 0) {
-            if (static_ok && gi < full_groups) as_group_static<RT, D>(p, gi, ring, s_chunk, ovf);
-            else as_group<RT, D>(p, gi, ring, s_chunk, ovf);
+            if (static_ok && gi < full_groups) {
+                const uint64_t gn = gi + gridDim.x;
+                const bool next_static = gn < p.group_end && gn < full_groups;
+                as_group_static<RT, D>(p, gi, ring, s_chunk, ovf, !prefetched, next_static, gn);
+                prefetched = next_static;
+            } else {
+                as_group<RT, D>(p, gi, ring, s_chunk, ovf);
+                prefetched = false;
+            }
         } else {
             as_group<RT, D>(p, gi, ring, s_chunk, ovf);
         }
