@@ -54,6 +54,7 @@ struct SpParams {
     // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
     // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
+    // cp.async engine: 8 = no prefetch across group boundaries (results unchanged).
     int32_t debug_mode;
 };
 

@@ -1,0 +1,82 @@
+#!/usr/bin/env python3
+"""Interleaved A/B timing of single_pass variants in ONE process on one GPU (profiling tool).
+
+    python tools/ab.py [--n 1073741824] [--rounds 7] [--reps 10] SPEC [SPEC ...]
+
+SPEC = label:engine:R:B[:ENV=VAL,...]  e.g.  async:4:1:1024  tc05:2:1:1024:TCR_DEBUG_MODE=3
+Rounds alternate between the specs so clock / thermal drift hits all of them alike; the
+median over rounds of the per-round mean kernel time is reported (CUDA events on the
+launch stream, inputs 2 GiB > L2).
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1 << 30)
+    ap.add_argument("--rounds", type=int, default=7)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("specs", nargs="+")
+    a = ap.parse_args()
+    import torch
+    import paper_2001_05585_b200 as T
+    from paper_2001_05585_b200 import _capi
+    lib = _capi.load()
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(st.cuda_stream)
+    x = T.generate("uniform", 0, a.n, device=dev)
+    res = torch.zeros(1, dtype=torch.float32, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    xp, rp, op = C.c_void_p(x.data_ptr()), C.c_void_p(res.data_ptr()), C.c_void_p(ovf.data_ptr())
+    specs = []
+    for s in a.specs:
+        parts = s.split(":")
+        env = dict(kv.split("=") for kv in parts[4].split(",")) if len(parts) > 4 and parts[4] else {}
+        cfg = T.ReductionConfig(m=16, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])))
+        specs.append((parts[0], cfg.to_c(), env))
+    times = {s[0]: [] for s in specs}
+    vals = {}
+    for rnd in range(a.rounds):
+        for label, c, env in specs:
+            old = {k: os.environ.get(k) for k in env}
+            os.environ.update(env)
+            try:
+                for _ in range(3):
+                    _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(a.reps):
+                    _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))
+                e1.record(st)
+                e1.synchronize()
+                times[label].append(e0.elapsed_time(e1) / a.reps)
+                vals[label] = res.item()
+            finally:
+                for k, v in old.items():
+                    if v is None:
+                        os.environ.pop(k, None)
+                    else:
+                        os.environ[k] = v
+    out = {}
+    for label, _, _ in specs:
+        ms = statistics.median(times[label])
+        out[label] = {"ms_median": ms, "ms_min": min(times[label]), "gelem_s": a.n / ms / 1e6,
+                      "tb_s": 2 * a.n / ms / 1e9, "value": vals[label]}
+        print(f"{label:24s} {ms * 1e3:8.1f} us  {a.n / ms / 1e6:8.1f} Gelem/s  {2 * a.n / ms / 1e9:6.3f} TB/s  "
+              f"(min {min(times[label]) * 1e3:.1f} us)  value {vals[label]!r}", flush=True)
+    if a.out:
+        json.dump(out, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
