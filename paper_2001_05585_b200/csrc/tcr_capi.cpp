@@ -52,8 +52,11 @@ struct Workspace {
     void* cub_temp = nullptr;
     size_t cub_cap = 0;
     void* host_pinned = nullptr;  // 64 bytes of result readback
+    uint16_t* conv = nullptr;  // fp32 -> binary16 staging for m != 16
+    size_t conv_cap = 0;
     // pipelined host path
     float* ring[2] = {nullptr, nullptr};
+    uint16_t* ring16[2] = {nullptr, nullptr};
     size_t ring_cap = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
@@ -116,8 +119,14 @@ int validate_cfg(const tcr_config* c) {
 }
 
 int check_supported(const tcr_config* c) {
-    if (c->m != 16)
-        return fail(TCR_NOT_SUPPORTED, "single_pass on B200 currently implements m = 16 (the hardware fragment)");
+    if (c->m != 16) {
+        const tcr::SpGeometry g = tcr::make_geometry(1u << 20, c->m, c->R, c->B);
+        if (!tcr::genm_supported(g))
+            return fail(TCR_NOT_SUPPORTED, "fragment side m=" + std::to_string(c->m) + " with R=" + std::to_string(c->R) +
+                                               " is not implemented on the B200 path (supported: m=16 any R; m in "
+                                               "{4,32,64,128} any R; m=8 with R in {1,2} or 4|R; m=2 with R in "
+                                               "{1,2} or 4|R)");
+    }
     if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_MMA_SYNC_ASYNC)
         return fail(TCR_INVALID_ARGUMENT, "unknown engine");
     return TCR_OK;
@@ -203,6 +212,14 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;
     }
+    if (c->m != 16) {
+        // m != 16: the selector-matrix engine (binary16 input; fp32 callers convert first)
+        if (f32) return fail(TCR_NOT_SUPPORTED, "internal: m != 16 needs binary16 input");
+        g_engine = TCR_ENGINE_MMA_SYNC_ASYNC;
+        TCR_CUDA(tcr::launch_genm(p, g, s));
+        ++g_launches;
+        return TCR_OK;
+    }
     int engine = pick_engine(c, g, f32);
     // a partial group range (pipelined host path) can only run on engines that take any range
     if ((g0 != 0 || g1 != g.n_groups) && (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC))
@@ -275,6 +292,14 @@ int sp_async(const void* d_x, size_t n, const tcr_config* c, bool f32, float* d_
     rc = get_ws(s, &w);
     if (rc) return rc;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    if (f32 && c->m != 16) {
+        // from_single (fragment.hpp:68) applied up front, then the binary16 engine
+        rc = ensure(&w->conv, &w->conv_cap, n, s);
+        if (rc) return rc;
+        TCR_CUDA(tcr::launch_convert_f32_f16(static_cast<const float*>(d_x), w->conv, n, s));
+        ++g_launches;
+        return enqueue_sp(w->conv, 0, n, c, false, d_result, d_overflow, nullptr, w, s, 0, g.n_groups, true);
+    }
     return enqueue_sp(d_x, 0, n, c, f32, d_result, d_overflow, nullptr, w, s, 0, g.n_groups, true);
 }
 
@@ -417,6 +442,9 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
         for (auto& r : w->ring)
             if (r) TCR_CUDA(cudaFree(r));
         for (auto& r : w->ring) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(float)));
+        for (auto& r : w->ring16)
+            if (r) TCR_CUDA(cudaFree(r));
+        for (auto& r : w->ring16) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(uint16_t)));
         w->ring_cap = ring_elems;
     }
     if (!w->copy_stream) {
@@ -441,8 +469,15 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
         TCR_CUDA(cudaStreamWaitEvent(s, w->copied[slot], 0));
         const bool last = (k + 1 == n_chunks);
         // single chunk: finalise in the same launch; otherwise one finaliser at the end
-        rc = enqueue_sp(w->ring[slot], e0, n, &cc, true, w->result(), w->overflow(), nullptr, w, s, g0, g1,
-                        last && n_chunks == 1);
+        if (cc.m == 16) {
+            rc = enqueue_sp(w->ring[slot], e0, n, &cc, true, w->result(), w->overflow(), nullptr, w, s, g0, g1,
+                            last && n_chunks == 1);
+        } else {
+            TCR_CUDA(tcr::launch_convert_f32_f16(w->ring[slot], w->ring16[slot], e1 - e0, s));
+            ++g_launches;
+            rc = enqueue_sp(w->ring16[slot], e0, n, &cc, false, w->result(), w->overflow(), nullptr, w, s, g0, g1,
+                            last && n_chunks == 1);
+        }
         if (rc) return rc;
         TCR_CUDA(cudaEventRecord(w->consumed[slot], s));
     }

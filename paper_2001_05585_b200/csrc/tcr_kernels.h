@@ -21,6 +21,7 @@ constexpr uint64_t kGroupElemsTarget = 1ull << 16;
 constexpr int kSpWarps = 8;            // warps per CTA of the single-pass kernel
 constexpr int kSpThreads = kSpWarps * 32;
 constexpr int kMaxChunksPerGroup = 256;
+constexpr int kMaxChunksGenm = 4096;     // chunk table of the m != 16 engine (small chunks)
 
 struct SpGeometry {
     uint32_t m, R, W;          // fragment side, chain length, warps per logical block (B/32)
@@ -54,7 +55,8 @@ struct SpParams {
     // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
     // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
-    // cp.async engine: 8 = no prefetch across group boundaries (results unchanged).
+    // cp.async engine: 8 = prefetch across a CTA's group boundaries (measured slower: 6.02 vs
+    // 6.44 TB/s interleaved A/B, gpurun_out/exp11; results unchanged).
     int32_t debug_mode;
 };
 
@@ -76,6 +78,13 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
 // group range including the ragged tail (zero-fill copies).  binary16 input.
 int async_max_grid(uint32_t R);
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
+
+// Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.
+bool genm_supported(const SpGeometry& g);
+cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s);
+
+// fp32 -> binary16 (RNE, from_single) conversion of count elements.
+cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, uint64_t count, cudaStream_t s);
 cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
 int single_pass_m16_max_grid(bool f32_input, uint32_t R);
 

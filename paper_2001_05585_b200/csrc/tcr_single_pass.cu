@@ -437,7 +437,8 @@ SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B) {
     uint32_t G = 1;
     while (uint64_t(G) * g.block_elems < kGroupElemsTarget) G <<= 1;
     // keep the per-group chunk table in shared memory
-    while (G > 1 && uint64_t(G) * g.W > uint64_t(kMaxChunksPerGroup)) G >>= 1;
+    const uint64_t cap = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
+    while (G > 1 && uint64_t(G) * g.W > cap) G >>= 1;
     g.G = G;
     g.group_elems = uint64_t(G) * g.block_elems;
     g.n_groups = (g.n_blocks + G - 1) / G;

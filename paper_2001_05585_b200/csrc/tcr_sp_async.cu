@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
         if constexpr (RT > 0) {
             if (static_ok && gi < full_groups) {
                 const uint64_t gn = gi + gridDim.x;
-                const bool next_static = gn < p.group_end && gn < full_groups && p.debug_mode != 8;
+                const bool next_static = gn < p.group_end && gn < full_groups && p.debug_mode == 8;
                 as_group_static<RT, D>(p, gi, ring, s_chunk, ovf, !prefetched, next_static, gn);
                 prefetched = next_static;
             } else {

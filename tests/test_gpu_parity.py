@@ -316,3 +316,71 @@ def test_full_size_against_golden(dist, seed, lgn, engine):
                 assert err_exact / a <= 1e-6 and err_ref / a <= 1e-6
     del x
     torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------------------------- fragment sides m != 16
+
+GENM = [(2, 1, 128), (2, 2, 64), (2, 4, 32), (4, 1, 128), (4, 4, 128), (4, 3, 96), (4, 1, 1024), (8, 1, 128),
+        (8, 2, 256), (8, 4, 32), (8, 8, 64), (32, 1, 128), (32, 3, 32), (64, 1, 64), (128, 1, 32)]
+
+
+@pytest.mark.parametrize("m,R,B", GENM)
+def test_genm_integers_exact_and_blocks(oracle, m, R, B):
+    x = oracle.generate("integers", 3, (1 << 20) + 333)
+    xd = torch.from_numpy(x).to(DEV).half()
+    cfg = T.ReductionConfig(m=m, R=R, B=B)
+    for fin in (T.Finalize.tree, T.Finalize.ordered, T.Finalize.atomic):
+        o = T.reduce(xd, T.ReductionConfig(m=m, R=R, B=B, finalize=fin))
+        assert o.value == oracle.oracle64(x) and not o.overflow, (m, R, B, fin)
+    _, ref_blocks = oracle.single_pass(x, threads=8, want_blocks=True, m=m, R=R, B=B)
+    got = T.block_results(xd, cfg).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), ref_blocks.view(np.uint32))
+
+
+@pytest.mark.parametrize("m,R,B", GENM)
+@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1)])
+def test_genm_float_vs_reference(oracle, m, R, B, dist, seed):
+    h = oracle.generate_f16(dist, seed, (1 << 20) + 4097)
+    xd = to_dev_f16(h)
+    _, ref_blocks = oracle.single_pass(h, threads=8, want_blocks=True, m=m, R=R, B=B)
+    got = T.block_results(xd, T.ReductionConfig(m=m, R=R, B=B)).cpu().numpy()
+    same = (got.view(np.uint32) == ref_blocks.view(np.uint32)).mean()
+    diff = np.abs(got.astype(np.float64) - ref_blocks).max()
+    print(f"\nm={m} R={R} B={B} {dist}: bit-identical blocks {same:.6f} max abs diff {diff:.3e}")
+    assert same >= 0.99 and diff <= 2.0 ** -4
+    ref = oracle.single_pass(h, threads=8, m=m, R=R, B=B)
+    o = T.reduce(xd, T.ReductionConfig(m=m, R=R, B=B, finalize=T.Finalize.ordered))
+    if same == 1.0:
+        assert o.value == ref.value
+    exact, absum = oracle.exact_sum_f16(h)
+    assert abs(o.value - ref.value) <= 2e-5 * max(abs(exact), 1e-3 * absum)
+    assert o.atomic_count == ref.atomic_count and o.mma_count == ref.mma_count
+
+
+def test_reference_default_config_goldens():
+    """reference_small.json m = 4 cases (the reference's default fragment side) through the drop-in."""
+    g = json.load(open(os.path.join(GOLDEN, "reference_small.json")))
+    import oracle as O
+    for case in g["cases"]:
+        if case.get("m") != 4 or case["dist"] is None:
+            continue
+        x = O.generate(case["dist"], case["seed"], case["n"])
+        cfg = T.ReductionConfig(m=4, R=case["R"], B=case["B"], finalize=T.Finalize.ordered,
+                                atomic_order=T.AtomicOrder(case.get("atomic_order", 0)),
+                                atomic_seed=case.get("atomic_seed", 0))
+        got = T.reduce(x, cfg)   # host fp32 drop-in path
+        exp = case["outcome"]
+        print(f"\n{case['tag']}: gpu {got.value!r} reference {exp['value']!r}")
+        if case["dist"] == "integers":
+            assert got.value == exp["value"]
+        else:
+            assert abs(got.value - exp["value"]) <= 2e-5 * abs(case["oracle64"]) + 1e-3
+        assert got.atomic_count == exp["atomic_count"] and got.mma_count == exp["mma_count"]
+
+
+def test_genm_unsupported_is_loud():
+    x = torch.ones(4096, device=DEV, dtype=torch.float16)
+    with pytest.raises(NotImplementedError):
+        T.reduce(x, T.ReductionConfig(m=8, R=3, B=128))
+    with pytest.raises(NotImplementedError):
+        T.reduce(x, T.ReductionConfig(m=256, R=1, B=128))
