@@ -54,6 +54,17 @@ struct Workspace {
     void* host_pinned = nullptr;  // 64 bytes of result readback
     uint16_t* conv = nullptr;  // fp32 -> binary16 staging for m != 16
     size_t conv_cap = 0;
+    // variants: tree columns, double partials, recurrence level buffers, whole-input staging
+    float* tree_cols = nullptr;
+    size_t tree_cap = 0;
+    double* dpart = nullptr;
+    size_t dpart_cap = 0;
+    float* lvl_f32 = nullptr;
+    size_t lvl_f32_cap = 0;
+    uint16_t* lvl16[2] = {nullptr, nullptr};
+    size_t lvl16_cap[2] = {0, 0};
+    float* stage = nullptr;  // host path of the non-single_pass variants
+    size_t stage_cap = 0;
     // pipelined host path
     float* ring[2] = {nullptr, nullptr};
     uint16_t* ring16[2] = {nullptr, nullptr};
@@ -66,7 +77,10 @@ struct Workspace {
     uint32_t* ticket() { return reinterpret_cast<uint32_t*>(fixed + 8); }
     uint32_t* sh_ticket() { return reinterpret_cast<uint32_t*>(fixed + 12); }
     uint32_t* sink() { return reinterpret_cast<uint32_t*>(fixed + 16); }
+    uint32_t* var_ticket() { return reinterpret_cast<uint32_t*>(fixed + 20); }
+    float* var_result() { return reinterpret_cast<float*>(fixed + 24); }
     double* exact_out() { return reinterpret_cast<double*>(fixed + 32); }
+    double* dsum_out() { return reinterpret_cast<double*>(fixed + 64); }
 };
 
 std::mutex g_mu;
@@ -311,15 +325,240 @@ int read_result(Workspace* w, cudaStream_t s, float* value, uint32_t* ovf) {
     return TCR_OK;
 }
 
+
+// ------------------------------------------------------------------ the other variants (:344-358)
+
+int sync_read(void* host, const void* dev, size_t bytes, Workspace* w, cudaStream_t s) {
+    TCR_CUDA(cudaMemcpyAsync(w->host_pinned, dev, bytes, cudaMemcpyDeviceToHost, s));
+    TCR_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(host, w->host_pinned, bytes);
+    return TCR_OK;
+}
+
+uint64_t levels_of(uint64_t n) {  // pairwise_tree levels of a pow2-padded length (reduction.hpp:90-101)
+    uint64_t P = 1, lv = 0;
+    while (P < n) {
+        P <<= 1;
+        ++lv;
+    }
+    return lv;
+}
+
+// shuffle32 (:113-122) / half_tree (:126-151): bit-exact strided pairwise tree.
+int run_tree(const void* d_x, bool f32, uint64_t n, bool half, tcr_outcome* out, Workspace* w, cudaStream_t s) {
+    if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+    int rc = ensure(&w->tree_cols, &w->tree_cap, tcr::tree_cols_needed(), s);
+    if (rc) return rc;
+    TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+    TCR_CUDA(tcr::launch_pairwise_tree(d_x, f32, n, half, w->tree_cols, w->var_result(), w->overflow(), s));
+    g_launches += 2;
+    float v;
+    uint32_t o;
+    rc = sync_read(&v, w->var_result(), 4, w, s);
+    if (rc) return rc;
+    rc = sync_read(&o, w->overflow(), 4, w, s);
+    if (rc) return rc;
+    const uint64_t lv = levels_of(n);
+    out->value = v;
+    out->overflow = half && o ? 1 : 0;
+    out->level_count = lv;
+    out->sim_steps = 4 * lv;
+    out->shuffle_count = (1ull << lv) - 1;
+    return TCR_OK;
+}
+
+// oracle64 (:106-110): binary64 sum on the device.
+int run_oracle64(const void* d_x, bool f32, uint64_t n, tcr_outcome* out, Workspace* w, cudaStream_t s) {
+    out->value = 0.0;
+    if (n == 0) return TCR_OK;   // the reference's oracle64 of an empty span is 0
+    int rc = ensure(&w->dpart, &w->dpart_cap, size_t(tcr::sm_count()) * 4, s);
+    if (rc) return rc;
+    TCR_CUDA(tcr::launch_dsum(d_x, f32, n, w->dpart, w->var_ticket(), w->dsum_out(), s));
+    ++g_launches;
+    return sync_read(&out->value, w->dsum_out(), 8, w, s);
+}
+
+// single_pass with the result read back (used by recurrence / split)
+int run_single_pass(const void* d_x, bool f32, uint64_t n, const tcr_config* c, tcr_outcome* out, Workspace* w,
+                    cudaStream_t s) {
+    TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+    const int before = g_launches;
+    int rc = sp_async(d_x, n, c, f32, w->result(), w->overflow(), s);
+    if (rc) return rc;
+    g_launches += before + 1;
+    float v;
+    uint32_t o;
+    rc = read_result(w, s, &v, &o);
+    if (rc) return rc;
+    std::memset(out, 0, sizeof *out);
+    out->value = v;
+    out->overflow = o ? 1 : 0;
+    counters(n, c, out);
+    return TCR_OK;
+}
+
+// recurrence (:189-231): levels of chained_warp_reduce with binary16 inter-level partials.  A
+// level's chunk results are single_pass block results at B = 32 (one warp chunk per block).
+int run_recurrence(const void* d_x, bool f32, uint64_t n0, const tcr_config* c, tcr_outcome* out, Workspace* w,
+                   cudaStream_t s) {
+    if (n0 == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+    const uint64_t group = uint64_t(c->m) * c->m, chunk = group * c->R;
+    std::memset(out, 0, sizeof *out);
+    tcr_config cb = *c;
+    cb.variant = TCR_SINGLE_PASS;
+    cb.B = 32;
+    cb.finalize = TCR_FINALIZE_TREE;
+    uint32_t ovf_any = 0;
+    const void* cur = d_x;
+    bool cur_f32 = f32;
+    uint64_t n = n0;
+    int nb = 0;
+    while (n >= group) {
+        const uint64_t count = (n + chunk - 1) / chunk;
+        int rc = ensure(&w->lvl_f32, &w->lvl_f32_cap, count, s);
+        if (rc) return rc;
+        rc = ensure(&w->lvl16[nb], &w->lvl16_cap[nb], count, s);
+        if (rc) return rc;
+        TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+        const tcr::SpGeometry g = tcr::make_geometry(n, cb.m, cb.R, cb.B);
+        if (cur_f32 && cb.m != 16) {
+            rc = ensure(&w->conv, &w->conv_cap, n, s);
+            if (rc) return rc;
+            TCR_CUDA(tcr::launch_convert_f32_f16(static_cast<const float*>(cur), w->conv, n, s));
+            cur = w->conv;
+            cur_f32 = false;
+        }
+        rc = enqueue_sp(cur, 0, n, &cb, cur_f32, w->result(), w->overflow(), w->lvl_f32, w, s, 0, g.n_groups, true);
+        if (rc) return rc;
+        TCR_CUDA(tcr::launch_round_level(w->lvl_f32, w->lvl16[nb], count, w->overflow(), s));
+        ++g_launches;
+        uint32_t o;
+        rc = sync_read(&o, w->overflow(), 4, w, s);
+        if (rc) return rc;
+        ovf_any |= o;
+        cur = w->lvl16[nb];
+        cur_f32 = false;
+        nb ^= 1;
+        n = count;
+        ++out->level_count;
+        out->sim_steps += 2ull * c->R + 3;
+        out->mma_count += count * (c->R + 1ull);
+    }
+    if (n == 1) {
+        if (cur_f32) {
+            float v;
+            int rc = sync_read(&v, cur, 4, w, s);
+            if (rc) return rc;
+            out->value = v;
+        } else {
+            uint16_t h;
+            int rc = sync_read(&h, cur, 2, w, s);
+            if (rc) return rc;
+            uint32_t u = uint32_t(h & 0x8000u) << 16;
+            const uint32_t e = (h >> 10) & 31u, mnt = h & 1023u;
+            float f;
+            if (e == 0) {
+                f = float(mnt) * 0x1.0p-24f;
+                std::memcpy(&u, &f, 4);
+                u |= uint32_t(h & 0x8000u) << 16;
+            } else if (e == 31) {
+                u |= 0x7F800000u | (mnt << 13);
+            } else {
+                u |= ((e + 112) << 23) | (mnt << 13);
+            }
+            std::memcpy(&f, &u, 4);
+            out->value = f;
+        }
+    } else {
+        // leftover shorter than one group: zero-padded two-step reduce with R = 1 (:218-223)
+        tcr_config c1 = cb;
+        c1.R = 1;
+        tcr_outcome o1;
+        int rc = run_single_pass(cur, cur_f32, n, &c1, &o1, w, s);
+        if (rc) return rc;
+        out->value = o1.value;
+        ovf_any |= uint32_t(o1.overflow);
+        out->sim_steps += 5;
+        out->mma_count += 2;
+    }
+    out->overflow = ovf_any ? 1 : 0;
+    return TCR_OK;
+}
+
+// split (:298-341): tensor share at R = 1 through single_pass, the rest through shuffle32.
+int run_split(const void* d_x, bool f32, uint64_t n, const tcr_config* c, tcr_outcome* out, Workspace* w,
+              cudaStream_t s) {
+    if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+    std::memset(out, 0, sizeof *out);
+    tcr_config tc = *c;
+    tc.variant = TCR_SINGLE_PASS;
+    tc.R = 1;
+    const uint64_t chunk_block = uint64_t(c->m) * c->m * (c->B / 32);
+    uint64_t tensor_len = uint64_t(c->f * double(n));
+    tensor_len = tensor_len / chunk_block * chunk_block;
+    tcr_outcome t{}, sh{};
+    float tensor_part = 0.0f, shuffle_part = 0.0f;
+    if (tensor_len > 0) {
+        int rc = run_single_pass(d_x, f32, tensor_len, &tc, &t, w, s);
+        if (rc) return rc;
+        tensor_part = float(t.value);
+        out->level_count = 1;
+    }
+    if (tensor_len < n) {
+        const char* base = static_cast<const char*>(d_x) + tensor_len * (f32 ? 4 : 2);
+        int rc = run_tree(base, f32, n - tensor_len, false, &sh, w, s);
+        if (rc) return rc;
+        shuffle_part = float(sh.value);
+        out->shuffle_count = sh.shuffle_count;
+        out->level_count = std::max<uint64_t>(out->level_count, sh.level_count);
+    }
+    if (tensor_len == 0) out->value = shuffle_part;
+    else if (tensor_len == n) out->value = tensor_part;
+    else out->value = tensor_part + shuffle_part;
+    out->overflow = t.overflow;
+    out->sim_steps = std::max(t.sim_steps, sh.sim_steps) + ((tensor_len > 0 && tensor_len < n) ? 1 : 0);
+    out->mma_count = t.mma_count;
+    out->atomic_count = t.atomic_count;
+    out->shuffle_count += t.shuffle_count;
+    return TCR_OK;
+}
+
+int run_variant(const void* d_x, bool f32, uint64_t n, const tcr_config* c, tcr_outcome* out, Workspace* w,
+                cudaStream_t s) {
+    switch (c->variant) {
+    case TCR_ORACLE64: return run_oracle64(d_x, f32, n, out, w, s);
+    case TCR_SHUFFLE32: return run_tree(d_x, f32, n, false, out, w, s);
+    case TCR_HALF_TREE: return run_tree(d_x, f32, n, true, out, w, s);
+    case TCR_RECURRENCE: {
+        int rc = validate_cfg(c);
+        if (rc) return rc;
+        rc = check_supported(c);
+        if (rc) return rc;
+        return run_recurrence(d_x, f32, n, c, out, w, s);
+    }
+    case TCR_SPLIT: {
+        if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+        int rc = validate_cfg(c);
+        if (rc) return rc;
+        rc = check_supported(c);
+        if (rc) return rc;
+        return run_split(d_x, f32, n, c, out, w, s);
+    }
+    default: return fail(TCR_INVALID_ARGUMENT, "unknown variant");
+    }
+}
+
 int reduce_device(const void* d_x, size_t n, const tcr_config* c, tcr_outcome* out, bool f32, cudaStream_t s) {
     if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
     std::memset(out, 0, sizeof *out);
     if (!c) return fail(TCR_INVALID_ARGUMENT, "null config");
-    if (c->variant != TCR_SINGLE_PASS)
-        return fail(TCR_NOT_SUPPORTED, "only the single_pass variant runs on the B200 path so far");
     Workspace* w = nullptr;
     int rc = get_ws(s, &w);
     if (rc) return rc;
+    if (c->variant != TCR_SINGLE_PASS) {
+        g_launches = 0;
+        return run_variant(d_x, f32, n, c, out, w, s);
+    }
     TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
     rc = sp_async(d_x, n, c, f32, w->result(), w->overflow(), s);
     if (rc) return rc;
@@ -419,8 +658,23 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
     if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
     std::memset(out, 0, sizeof *out);
     if (!c) return fail(TCR_INVALID_ARGUMENT, "null config");
-    if (c->variant != TCR_SINGLE_PASS)
-        return fail(TCR_NOT_SUPPORTED, "only the single_pass variant runs on the B200 path so far");
+    if (c->variant != TCR_SINGLE_PASS) {
+        // the other variants take the whole fp32 input on the device, then the same dispatcher
+        if (c->variant < TCR_ORACLE64 || c->variant > TCR_SPLIT) return fail(TCR_INVALID_ARGUMENT, "unknown variant");
+        cudaStream_t s0 = nullptr;
+        Workspace* w0 = nullptr;
+        int rc0 = get_ws(s0, &w0);
+        if (rc0) return rc0;
+        if (n == 0) {
+            if (c->variant == TCR_ORACLE64) return TCR_OK;
+            return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
+        }
+        if (!x) return fail(TCR_INVALID_ARGUMENT, "null input");
+        rc0 = ensure(&w0->stage, &w0->stage_cap, n, s0);
+        if (rc0) return rc0;
+        TCR_CUDA(cudaMemcpyAsync(w0->stage, x, n * sizeof(float), cudaMemcpyHostToDevice, s0));
+        return run_variant(w0->stage, true, n, c, out, w0, s0);
+    }
     if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
     if (!x) return fail(TCR_INVALID_ARGUMENT, "null input");
     int rc = validate_cfg(c);

@@ -83,6 +83,15 @@ cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
 bool genm_supported(const SpGeometry& g);
 cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s);
 
+// Variants (tcr_variants.cu): bit-exact strided pairwise trees (shuffle32 / half_tree), binary64
+// sum (oracle64), and the recurrence level rounding.
+uint64_t tree_cols_needed();
+cudaError_t launch_pairwise_tree(const void* x, bool f32, uint64_t n, bool half, float* cols, float* out,
+                                 uint32_t* ovf, cudaStream_t s);
+cudaError_t launch_dsum(const void* x, bool f32, uint64_t n, double* partials, uint32_t* ticket, double* out,
+                        cudaStream_t s);
+cudaError_t launch_round_level(const float* in, uint16_t* out, uint64_t count, uint32_t* ovf, cudaStream_t s);
+
 // fp32 -> binary16 (RNE, from_single) conversion of count elements.
 cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, uint64_t count, cudaStream_t s);
 cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);

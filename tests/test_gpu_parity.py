@@ -384,3 +384,91 @@ def test_genm_unsupported_is_loud():
         T.reduce(x, T.ReductionConfig(m=8, R=3, B=128))
     with pytest.raises(NotImplementedError):
         T.reduce(x, T.ReductionConfig(m=256, R=1, B=128))
+
+
+# --------------------------------------------------------------------------- the other Variants (:344-358)
+
+@pytest.mark.parametrize("n", [1, 2, 7, 1000, 65536, 65537, (1 << 20) + 3, 1 << 22])
+@pytest.mark.parametrize("dist", ["uniform", "normal", "integers"])
+def test_shuffle32_and_half_tree_bit_exact(oracle, n, dist):
+    x = oracle.generate(dist, 5, n)
+    for variant in ("shuffle32", "half_tree"):
+        ref = oracle.reduce(x, variant=variant).as_dict()
+        got_host = T.reduce(x, T.ReductionConfig(variant=T.Variant[variant]))            # fp32 host drop-in
+        got_dev = T.reduce(torch.from_numpy(x).to(DEV), T.ReductionConfig(variant=T.Variant[variant]))
+        for got in (got_host, got_dev):
+            assert (got.value == ref["value"]) or (math.isnan(got.value) and math.isnan(ref["value"])), (variant, n)
+            assert got.overflow == bool(ref["overflow"])
+            for k in ("level_count", "sim_steps", "shuffle_count"):
+                assert getattr(got, k) == ref[k], (variant, k)
+
+
+def test_half_tree_overflows_like_reference(oracle):  # test_reduction.cpp:66-77
+    assert T.reduce(np.ones(1 << 17, np.float32), T.ReductionConfig(variant=T.Variant.half_tree)).overflow
+    u = oracle.generate("uniform", 0, 1000000)
+    assert T.reduce(u, T.ReductionConfig(variant=T.Variant.half_tree)).overflow
+    assert T.reduce(np.array([1, 2, 3, 4], np.float32), T.ReductionConfig(variant=T.Variant.half_tree)).value == 10.0
+
+
+def test_oracle64_on_device(oracle):
+    for dist, seed, n in (("uniform", 3, 1000), ("normal", 1, (1 << 22) + 9), ("integers", 2, 1 << 20)):
+        x = oracle.generate(dist, seed, n)
+        got = T.reduce(x, T.ReductionConfig(variant=T.Variant.oracle64)).value
+        ref = oracle.oracle64(x)
+        assert abs(got - ref) <= 1e-12 * max(abs(ref), 1.0)
+    assert T.reduce(np.ones(1000000, np.float32), T.ReductionConfig(variant=T.Variant.oracle64)).value == 1.0e6
+
+
+@pytest.mark.parametrize("m,R,B", [(4, 1, 32), (4, 5, 32), (16, 1, 32), (16, 5, 32), (16, 3, 128), (8, 2, 64)])
+@pytest.mark.parametrize("dist,seed,n", [("normal", 17, 5000), ("normal", 1, (1 << 20) + 11), ("uniform", 0, 4096),
+                                         ("integers", 0, 1 << 20), ("uniform", 0, 1000000)])
+def test_recurrence_matches_reference(oracle, m, R, B, dist, seed, n):
+    x = oracle.generate(dist, seed, n)
+    ref = oracle.reduce(x, variant="recurrence", m=m, R=R, B=B).as_dict()
+    got = T.reduce(x, T.ReductionConfig(variant=T.Variant.recurrence, m=m, R=R, B=B))
+    assert got.overflow == bool(ref["overflow"])
+    for k in ("level_count", "sim_steps", "mma_count"):
+        assert getattr(got, k) == ref[k], k
+    if ref["overflow"]:
+        assert not math.isfinite(got.value) or not math.isfinite(ref["value"]) or got.value == ref["value"]
+    elif dist == "integers":
+        assert got.value == ref["value"]
+    else:
+        ab = float(np.abs(x.astype(np.float64)).sum())
+        assert abs(got.value - ref["value"]) <= 1e-3 * ab / max(1.0, n ** 0.5)
+
+
+def test_recurrence_reference_kats(oracle):  # test_reduction.cpp:103-117
+    o = T.reduce(np.ones(4096, np.float32), T.ReductionConfig(variant=T.Variant.recurrence, m=4, R=1, B=32))
+    assert o.value == 4096.0 and o.level_count == 3 and not o.overflow
+    seq = np.arange(1, 17, dtype=np.float32)
+    assert T.reduce(seq, T.ReductionConfig(variant=T.Variant.recurrence, m=4, R=1, B=32)).value == 136.0
+    u = oracle.generate("uniform", 0, 1000000)
+    assert T.reduce(u, T.ReductionConfig(variant=T.Variant.recurrence, m=4, R=5, B=32)).overflow
+
+
+@pytest.mark.parametrize("f", [0.0, 0.3, 0.5, 0.999, 1.0])
+@pytest.mark.parametrize("m,B", [(4, 128), (16, 1024), (16, 128)])
+def test_split_matches_reference(oracle, f, m, B):
+    for dist, seed, n in (("uniform", 11, 100000), ("integers", 1, 1 << 20), ("normal", 3, (1 << 20) + 5)):
+        x = oracle.generate(dist, seed, n)
+        ref = oracle.reduce(x, variant="split", m=m, R=1, B=B, f=f).as_dict()
+        got = T.reduce(x, T.ReductionConfig(variant=T.Variant.split, m=m, R=1, B=B, f=f,
+                                            finalize=T.Finalize.ordered))
+        for k in ("level_count", "sim_steps", "mma_count", "atomic_count", "shuffle_count"):
+            assert getattr(got, k) == ref[k], (k, f, m, B, dist)
+        assert got.overflow == bool(ref["overflow"])
+        if dist == "integers":
+            assert got.value == ref["value"]
+        else:
+            assert abs(got.value - ref["value"]) <= 2e-5 * abs(oracle.oracle64(x)) + 1e-3
+
+
+def test_split_degenerate_fractions(oracle):  # test_reduction.cpp:137-153
+    u = oracle.generate("uniform", 11, 100000)
+    cfg0 = T.ReductionConfig(variant=T.Variant.split, m=4, R=1, B=128, f=0.0)
+    assert T.reduce(u, cfg0).value == oracle.reduce(u, variant="shuffle32").value
+    aligned = oracle.generate("uniform", 12, 16 * 4 * 64)
+    cfg1 = T.ReductionConfig(variant=T.Variant.split, m=4, R=1, B=128, f=1.0, finalize=T.Finalize.ordered)
+    sp = T.ReductionConfig(m=4, R=1, B=128, finalize=T.Finalize.ordered)
+    assert T.reduce(aligned, cfg1).value == T.reduce(aligned, sp).value
