@@ -240,7 +240,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         engine = TCR_ENGINE_MMA_SYNC_REGS;
     g_engine = engine;
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
-        const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, uint64_t(tcr::async_max_grid(c->R))));
+        const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, uint64_t(tcr::async_max_grid(c->R, p.debug_mode))));
         TCR_CUDA(tcr::launch_async(p, grid, s));
         ++g_launches;
         return TCR_OK;

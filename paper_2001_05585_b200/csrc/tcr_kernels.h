@@ -76,7 +76,7 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
 
 // Per-warp cp.async pipeline engine (LDGSTS ring per warp, ldmatrix.trans + HMMA); handles any
 // group range including the ragged tail (zero-fill copies).  binary16 input.
-int async_max_grid(uint32_t R);
+int async_max_grid(uint32_t R, int debug_mode = 0);
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.

@@ -228,14 +228,13 @@ template <> struct AsDepth<3> { static constexpr int value = 12; };
 template <> struct AsDepth<4> { static constexpr int value = 16; };
 template <> struct AsDepth<5> { static constexpr int value = 10; };
 
-template <int RT>
+template <int RT, int D = AsDepth<RT>::value>
 constexpr uint32_t as_smem_bytes() {
-    return uint32_t(kAsWarps) * AsDepth<RT>::value * kAsStageBytes;
+    return uint32_t(kAsWarps) * D * kAsStageBytes;
 }
 
-template <int RT>
+template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
-    constexpr int D = AsDepth<RT>::value;
     extern __shared__ __align__(128) unsigned char s_ring[];
     __shared__ float s_chunk[kMaxChunksPerGroup];
     __shared__ float s_block[kMaxChunksPerGroup];
@@ -282,7 +281,10 @@ struct AsPick {
     uint32_t smem;
 };
 
-AsPick pick(uint32_t R) {
+AsPick pick(uint32_t R, int mode = 0) {
+    // profiling modes 9 / 10: ring depth 8 / 32 for R = 1 (default 16)
+    if (R == 1 && mode == 9) return {sp_async_kernel<1, 8>, as_smem_bytes<1, 8>()};
+    if (R == 1 && mode == 10) return {sp_async_kernel<1, 32>, as_smem_bytes<1, 32>()};
     switch (R) {
     case 1: return {sp_async_kernel<1>, as_smem_bytes<1>()};
     case 2: return {sp_async_kernel<2>, as_smem_bytes<2>()};
@@ -296,8 +298,9 @@ AsPick pick(uint32_t R) {
 bool as_attr_once() {
     static bool done = false;
     if (!done) {
+        for (int mode : {0, 9, 10})
         for (uint32_t R = 0; R <= 5; ++R) {
-            const AsPick k = pick(R);
+            const AsPick k = pick(R, mode);
             if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(k.smem)) != cudaSuccess)
                 return false;
         }
@@ -308,9 +311,9 @@ bool as_attr_once() {
 
 }  // namespace
 
-int async_max_grid(uint32_t R) {
+int async_max_grid(uint32_t R, int mode) {
     as_attr_once();
-    const AsPick k = pick(R);
+    const AsPick k = pick(R, mode);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kAsThreads, k.smem);
     if (per_sm < 1) per_sm = 1;
@@ -319,7 +322,7 @@ int async_max_grid(uint32_t R) {
 
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s) {
     if (!as_attr_once()) return cudaErrorInvalidValue;
-    const AsPick k = pick(p.R);
+    const AsPick k = pick(p.R, p.debug_mode);
     k.fn<<<grid, kAsThreads, k.smem, s>>>(p);
     return cudaGetLastError();
 }

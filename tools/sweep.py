@@ -70,7 +70,7 @@ def main():
         x = T.generate("uniform", 0, n, device=dev)
         xp = C.c_void_p(x.data_ptr())
         pts = []
-        for engine in (T.Engine.tcgen05, T.Engine.mma_sync):
+        for engine in (T.Engine.mma_sync_async, T.Engine.tcgen05, T.Engine.mma_sync, T.Engine.mma_sync_regs):
             for B in (32, 128, 256, 512, 1024):
                 for R in (1, 2, 3, 4, 5):
                     cfg = T.ReductionConfig(m=16, R=R, B=B, engine=engine)
