@@ -62,28 +62,50 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampled every ~200 ms from a thread DURING the timed region (the
-    B200_PROFILING.md clocks line); one query per sample so nothing sits in a pipe buffer."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled DURING the timed region (the B200_PROFILING.md
+    clocks line) through NVML in-process every ~2 ms (a timed region of 20 x 0.34 ms is shorter
+    than one nvidia-smi invocation); falls back to polling nvidia-smi if NVML is unavailable."""
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self.stop = threading.Event()
 
     def _loop(self):
-        while not self.stop.is_set():
-            try:
-                r = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
-                for line in r.stdout.splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
-            except Exception:
-                pass
-            self.stop.wait(0.2)
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                     N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                     N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                     N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                     N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake_slowdown"}
+            while not self.stop.is_set():
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                self.mx.append(float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+                self.stop.wait(0.002)
+            N.nvmlShutdown()
+        except Exception:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self.stop.is_set():
+                try:
+                    r = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                    f = [x.strip() for x in r.stdout.strip().split(",")]
+                    self.sm.append(float(f[0]))
+                    self.mx.append(float(f[1]))
+                    for nm, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], f[2:6]):
+                        if v.lower() == "active":
+                            self.reasons.add(nm)
+                except Exception:
+                    pass
+                self.stop.wait(0.2)
 
     def __enter__(self):
         self.t = threading.Thread(target=self._loop, daemon=True)
@@ -95,22 +117,9 @@ class Clocks:
         self.t.join(timeout=15)
 
     def summary(self):
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = [num(r[1]) for r in self.rows if len(r) >= 8 and num(r[1]) is not None]
-        mx = [num(r[2]) for r in self.rows if len(r) >= 8 and num(r[2]) is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            if len(r) >= 8:
-                for nm, v in zip(names, r[4:8]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 def cpu_reference_rate(n_sample: int, reps: int = 1):

@@ -15,6 +15,7 @@
 //                            the overflow note, the finishing MMA (HMMA.16816: sum of the 16
 //                            binary16 partials, two chunks per warp), block pairwise tree, group
 //                            tree -> group partial.  Last CTA finalises.
+#include <algorithm>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -79,39 +80,41 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 constexpr int kEpiGroups = 3;                         // epilogue warpgroups, round-robin over slots
-constexpr int kTcThreads = 64 + 128 * kEpiGroups;       // TMA warp + MMA warp + epilogue
 constexpr int kTileBufs = 8;                            // per-tile chunk/block tables in flight
+
+__host__ __device__ constexpr int tc_threads(int eg) { return 64 + 128 * eg; }  // TMA warp + MMA warp + epilogue
 
 struct SmemLayout {
     uint32_t ring_off, ones_off, bar_off, misc_off, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(uint32_t slot_bytes, uint32_t ns) {
+__host__ __device__ inline SmemLayout smem_layout(uint32_t slot_bytes, uint32_t ns, uint32_t acc = kAccBufs) {
     SmemLayout L;
     L.ring_off = 0;
     L.ones_off = slot_bytes * ns;
     L.bar_off = L.ones_off + 1024;
-    L.misc_off = L.bar_off + 8 * (2 * ns + 2 * kAccBufs) + 16;
+    L.misc_off = L.bar_off + 8 * (2 * ns + 2 * acc) + 16;
     // s_chunk[kTileBufs][256] + s_block[kTileBufs][256] + s_scratch[32] + s_done[kTileBufs] + s_own[4] + s_last
     L.total = L.misc_off + 4 * (2 * kTileBufs * kMaxChunksPerGroup + 32 + kTileBufs + 8) + 1024;  // +1024 align slack
     return L;
 }
 
-template <int Q>
-__global__ void __launch_bounds__(kTcThreads, 1)
+// Q MMA-groups per slot, EG epilogue warpgroups, ACC TMEM accumulator buffers, CPS CTAs per SM.
+template <int Q, int EG = kEpiGroups, int ACC = kAccBufs, int CPS = 1>
+__global__ void __launch_bounds__(tc_threads(EG), CPS)
 tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const uint32_t ns, const uint64_t n_tiles) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t R = p.R, W = p.W, G = p.G;
     const uint32_t slot_bytes = 4096u * Q * R;
-    const SmemLayout L = smem_layout(slot_bytes, ns);
+    const SmemLayout L = smem_layout(slot_bytes, ns, ACC);
     unsigned char* ring = smem + L.ring_off;
     uint16_t* ones = reinterpret_cast<uint16_t*>(smem + L.ones_off);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
     uint64_t* empty = full + ns;
     uint64_t* tfull = empty + ns;
-    uint64_t* tempty = tfull + kAccBufs;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAccBufs);
+    uint64_t* tempty = tfull + ACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
     float* s_chunk = reinterpret_cast<float*>(smem + L.misc_off);             // [kTileBufs][256]
     float* s_block = s_chunk + kTileBufs * kMaxChunksPerGroup;                 // [kTileBufs][256]
     float* s_scratch = s_block + kTileBufs * kMaxChunksPerGroup;               // [32]
@@ -132,15 +135,15 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < kAccBufs; ++i) {
+        for (int i = 0; i < ACC; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
-    constexpr uint32_t ncols = acc_cols * kAccBufs <= 32 ? 32 : acc_cols * kAccBufs <= 64 ? 64
-                             : acc_cols * kAccBufs <= 128 ? 128 : acc_cols * kAccBufs <= 256 ? 256 : 512;
+    constexpr uint32_t ncols = acc_cols * ACC <= 32 ? 32 : acc_cols * ACC <= 64 ? 64
+                             : acc_cols * ACC <= 128 ? 128 : acc_cols * ACC <= 256 ? 256 : 512;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(ncols));
@@ -183,7 +186,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
             for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
                     const uint32_t rs = t % ns, ph = (t / ns) & 1;
-                    const uint32_t ab = t % kAccBufs, aph = (t / kAccBufs) & 1;
+                    const uint32_t ab = t % ACC, aph = (t / ACC) & 1;
                     mbar_wait(&full[rs], ph);
                     if (p.debug_mode == 1) {
                         mbar_arrive(&empty[rs]);
@@ -215,9 +218,9 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
             }
         }
     } else {
-        // ================= epilogue: warpgroup eg takes slots t = eg (mod kEpiGroups)
+        // ================= epilogue: warpgroup eg takes slots t = eg (mod EG)
         uint64_t n_tiles_epi = n_tiles;
-        const uint32_t ew = warp - kEpiWarp0;         // 0 .. 4*kEpiGroups-1
+        const uint32_t ew = warp - kEpiWarp0;         // 0 .. 4*EG-1
         const uint32_t eg = ew >> 2, w4 = ew & 3u;    // warpgroup, warp within it
         const uint32_t qw = warp & 3u;                // TMEM lane quarter this warp may access
         const uint32_t c = lane & 3u;
@@ -230,8 +233,8 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
             const uint32_t buf = k % kTileBufs;
             float* chunks = s_chunk + buf * kMaxChunksPerGroup;
             for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
-                if (t % kEpiGroups != eg) continue;
-                const uint32_t ab = t % kAccBufs, aph = (t / kAccBufs) & 1;
+                if (t % EG != eg) continue;
+                const uint32_t ab = t % ACC, aph = (t / ACC) & 1;
                 mbar_wait(&tfull[ab], aph);
                 tc_fence_after();
                 uint32_t v[Q];
@@ -293,7 +296,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
     tc_fence_after();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
 
-    finalize_last_cta(p, s_scratch, s_last, 256);
+    finalize_last_cta(p, s_scratch, s_last, EG >= 2 ? 256 : 128);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -344,18 +347,29 @@ cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    const SmemLayout L = smem_layout(4096u * Q * g.R, ns);
     static bool attr_set = false;
     if (!attr_set) {
-        for (auto fn : {tc05_kernel<1>, tc05_kernel<2>, tc05_kernel<4>}) {
+        for (auto fn : {tc05_kernel<1>, tc05_kernel<2>, tc05_kernel<4>, tc05_kernel<1, 1, 4, 2>, tc05_kernel<2, 1, 4, 2>,
+                        tc05_kernel<4, 1, 4, 2>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             if (e != cudaSuccess) return e;
         }
         attr_set = true;
     }
-    if (Q == 4) tc05_kernel<4><<<grid, kTcThreads, L.total, s>>>(map, p, ns, n_tiles);
-    else if (Q == 2) tc05_kernel<2><<<grid, kTcThreads, L.total, s>>>(map, p, ns, n_tiles);
-    else tc05_kernel<1><<<grid, kTcThreads, L.total, s>>>(map, p, ns, n_tiles);
+    if (p.debug_mode == 11) {
+        // profiling: two CTAs per SM (half ring, one epilogue warpgroup, 4 accumulators each)
+        const uint32_t ns2 = ns / 2 < 2 ? 2 : ns / 2;
+        const SmemLayout L2 = smem_layout(4096u * Q * g.R, ns2, 4);
+        const int grid2 = int(std::min<uint64_t>(n_tiles, 2ull * sm_count()));
+        if (Q == 4) tc05_kernel<4, 1, 4, 2><<<grid2, tc_threads(1), L2.total, s>>>(map, p, ns2, n_tiles);
+        else if (Q == 2) tc05_kernel<2, 1, 4, 2><<<grid2, tc_threads(1), L2.total, s>>>(map, p, ns2, n_tiles);
+        else tc05_kernel<1, 1, 4, 2><<<grid2, tc_threads(1), L2.total, s>>>(map, p, ns2, n_tiles);
+        return cudaGetLastError();
+    }
+    const SmemLayout L = smem_layout(4096u * Q * g.R, ns);
+    if (Q == 4) tc05_kernel<4><<<grid, tc_threads(kEpiGroups), L.total, s>>>(map, p, ns, n_tiles);
+    else if (Q == 2) tc05_kernel<2><<<grid, tc_threads(kEpiGroups), L.total, s>>>(map, p, ns, n_tiles);
+    else tc05_kernel<1><<<grid, tc_threads(kEpiGroups), L.total, s>>>(map, p, ns, n_tiles);
     return cudaGetLastError();
 }
 
