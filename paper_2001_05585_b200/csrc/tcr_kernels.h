@@ -56,7 +56,8 @@ struct SpParams {
     // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
     // cp.async engine: 8 = prefetch across a CTA's group boundaries (measured slower: 6.02 vs
-    // 6.44 TB/s interleaved A/B, gpurun_out/exp11; results unchanged).
+    // 6.44 TB/s interleaved A/B, gpurun_out/exp11; results unchanged); 9 / 10 = ring depth 8 / 32
+    // for R = 1; 12 = disable the warp-blocks path (CTA-barrier block stage).
     int32_t debug_mode;
 };
 

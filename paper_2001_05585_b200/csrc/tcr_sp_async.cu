@@ -220,6 +220,120 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
     if (!prefetch_next) cp_async_wait<0>();
 }
 
+
+constexpr int kAsBufs = 4;   // per-group block tables in flight (warp-blocks mode)
+
+// Warp-blocks mode: warp w owns the contiguous chunks [w*Cpw, (w+1)*Cpw) of the group, where
+// Cpw = Cg/8 is a whole number of logical blocks, so the reference's block tree (:253) runs in
+// registers (shfl_down over pow2(W)-lane segments) and no CTA barrier is needed: the warp that
+// completes a group last (shared counter) runs the group tree.  Fragments stream contiguously.
+template <int RT, int D>
+__device__ __forceinline__ void as_group_warpblocks(const SpParams& p, uint64_t gi, uint32_t k_iter, uint32_t ring_saddr,
+                                                    float* s_blocks, uint32_t* s_done, volatile uint32_t* s_gen,
+                                                    bool& ovf) {
+    static_assert(D % (2 * RT) == 0, "static path needs 2*RT | depth");
+    constexpr uint32_t CPI = D / RT;
+    constexpr uint64_t CE = uint64_t(RT) * 256u;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned c = lane & 3u;
+    const uint32_t W = p.W, G = p.G;
+    const uint32_t Cg = G * W;
+    const uint32_t Cpw = Cg / kAsWarps;
+    const uint32_t iters = Cpw / CPI;
+    uint32_t P = 1;
+    while (P < W) P <<= 1;
+    const uint32_t bpb = 32u / P;                 // blocks per 32-lane batch
+    const uint32_t b0 = warp * (Cpw / W);         // first group-local block of this warp
+    const uint32_t buf = k_iter % kAsBufs;
+    float* blocks = s_blocks + buf * kMaxChunksPerGroup;
+    // the buffer must have been released by the tree of iteration k_iter - kAsBufs
+    if (lane == 0)
+        while (s_gen[buf] != k_iter - kAsBufs) { }
+    __syncwarp();
+    const uint16_t* gp = static_cast<const uint16_t*>(p.x) + (gi * uint64_t(Cg) + uint64_t(warp) * Cpw) * CE + 8u * lane;
+    const uint32_t cp_dst = ring_saddr + swz(lane >> 1, lane & 1u);
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_base = ring_saddr + swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+#pragma unroll
+    for (int u = 0; u < D - 1; ++u) {
+        cp_async16(cp_dst + u * kAsStageBytes, gp + uint64_t(u) * 256u, 16u);
+        cp_async_commit();
+    }
+    float held = 0.0f;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint16_t* gq = gp + uint64_t(it) * D * 256u;
+        uint32_t a01p = 0, a23p = 0;
+        float acc[4];
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+            if (it + 1 < iters || u == 0)
+                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + uint64_t(u + D - 1) * 256u, 16u);
+            cp_async_commit();
+            cp_async_wait<D - 1>();
+            __syncwarp();
+            uint32_t d0, d1, d2, d3;
+            ldsm_x4_trans(ld_base + u * kAsStageBytes, d0, d1, d2, d3);
+            if (u % RT == 0) acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
+            if (u % RT == RT - 1) {
+                const uint32_t pk = uint32_t(f32_to_h(acc[0])) | (uint32_t(f32_to_h(acc[2])) << 16);
+                const uint32_t vA = __shfl_sync(kFull, pk, 8 * c);
+                const uint32_t vB = __shfl_sync(kFull, pk, 8 * c + 4);
+                const uint32_t a01 = prmt(vA, vB, 0x5410), a23 = prmt(vA, vB, 0x7632);
+                if ((u / RT) % 2 == 0) {
+                    a01p = a01;
+                    a23p = a23;
+                } else {
+                    float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                    mma_16816(fin, a01p, a01, a23p, a23, kOnesF16x2, kOnesF16x2);
+                    ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t ci = it * CPI + u / RT - 1 + h;      // warp-local chunk
+                        const uint32_t bl = ci / W, j = ci - bl * W;
+                        if (lane == (bl % bpb) * P + j) held = h ? fin[2] : fin[0];
+                        if (j == W - 1 && (bl % bpb == bpb - 1 || ci == Cpw - 1)) {
+                            // flush: pairwise trees over the P-lane segments (reduction.hpp:90-101)
+                            float v = held;
+                            for (uint32_t off = P >> 1; off >= 1; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+                            const uint32_t seg = lane / P;
+                            const uint32_t blk = bl - (bl % bpb) + seg;
+                            if (lane % P == 0 && seg <= bl % bpb) {
+                                blocks[b0 + blk] = v;
+                                const uint64_t gb = gi * G + b0 + blk;
+                                if (gb < p.n_blocks) {
+                                    if (p.block_partials) p.block_partials[gb] = v;
+                                    if (p.finalize == kFinAtomic) atomicAdd(p.result, v);
+                                }
+                            }
+                            held = 0.0f;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    // group stage: the last warp to finish runs the adjacent tree over the G block results
+    __syncwarp();
+    uint32_t last = 0;
+    if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_done[buf], 1u) == kAsWarps - 1;
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+        __threadfence_block();
+        tile_tree_group(p, gi, blocks);
+        __syncwarp();
+        if (lane == 0) {
+            s_done[buf] = 0;
+            __threadfence_block();
+            s_gen[buf] = k_iter;
+        }
+    }
+}
+
 // Ring depth per chain length: 2*R | D keeps every stage index and chunk pair compile-time.
 template <int RT> struct AsDepth { static constexpr int value = 8; };
 template <> struct AsDepth<1> { static constexpr int value = 16; };
@@ -238,6 +352,9 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     extern __shared__ __align__(128) unsigned char s_ring[];
     __shared__ float s_chunk[kMaxChunksPerGroup];
     __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ float s_wblocks[kAsBufs * kMaxChunksPerGroup];
+    __shared__ uint32_t s_done[kAsBufs];
+    __shared__ uint32_t s_gen[kAsBufs];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
     const unsigned warp = threadIdx.x >> 5;
@@ -245,10 +362,25 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     bool ovf = false;
     const uint64_t full_groups = p.n / (uint64_t(p.G) * p.W * p.chunk_elems);
     const uint32_t Cg = p.G * p.W;
-    bool static_ok = false;
-    if constexpr (RT > 0) static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % D == 0;
+    bool static_ok = false, warp_blocks = false;
+    if constexpr (RT > 0) {
+        static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % D == 0;
+        warp_blocks = static_ok && ((Cg / kAsWarps) % p.W == 0) && p.debug_mode != 12;
+    }
+    if (threadIdx.x < kAsBufs) {
+        s_done[threadIdx.x] = 0;
+        s_gen[threadIdx.x] = uint32_t(threadIdx.x) - kAsBufs;   // "iteration buf - kAsBufs completed"
+    }
+    __syncthreads();
     bool prefetched = false;   // this group's first D-1 fragments are already in flight
-    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+    uint32_t k_iter = 0;
+    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x, ++k_iter) {
+        if constexpr (RT > 0) {
+            if (warp_blocks && gi < full_groups) {
+                as_group_warpblocks<RT, D>(p, gi, k_iter, ring, s_wblocks, s_done, s_gen, ovf);
+                continue;
+            }
+        }
         if constexpr (RT > 0) {
             if (static_ok && gi < full_groups) {
                 const uint64_t gn = gi + gridDim.x;
