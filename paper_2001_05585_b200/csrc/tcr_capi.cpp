@@ -63,6 +63,8 @@ struct Workspace {
     size_t lvl_f32_cap = 0;
     uint16_t* lvl16[2] = {nullptr, nullptr};
     size_t lvl16_cap[2] = {0, 0};
+    float* chunk_res = nullptr;  // interleaved stream engine
+    size_t chunk_res_cap = 0;
     float* stage = nullptr;  // host path of the non-single_pass variants
     size_t stage_cap = 0;
     // pipelined host path
@@ -239,6 +241,15 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     if ((g0 != 0 || g1 != g.n_groups) && (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC))
         engine = TCR_ENGINE_MMA_SYNC_REGS;
     g_engine = engine;
+    if (engine == TCR_ENGINE_MMA_SYNC_ASYNC && p.debug_mode == 13 && tcr::stream_supported(c->R) && g0 == 0 &&
+        g1 == g.n_groups) {
+        const uint64_t n_chunks = g.n_groups * uint64_t(g.G) * g.W;
+        rc = ensure(&w->chunk_res, &w->chunk_res_cap, n_chunks, s);
+        if (rc) return rc;
+        TCR_CUDA(tcr::launch_stream(p, w->chunk_res, n_chunks, s));
+        g_launches += 2;
+        return TCR_OK;
+    }
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
         const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, uint64_t(tcr::async_max_grid(c->R, p.debug_mode))));
         TCR_CUDA(tcr::launch_async(p, grid, s));

@@ -57,7 +57,8 @@ struct SpParams {
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
     // cp.async engine: 8 = prefetch across a CTA's group boundaries (measured slower: 6.02 vs
     // 6.44 TB/s interleaved A/B, gpurun_out/exp11; results unchanged); 9 / 10 = ring depth 8 / 32
-    // for R = 1; 12 = disable the warp-blocks path (CTA-barrier block stage).
+    // for R = 1; 12 = disable the warp-blocks path (CTA-barrier block stage); 13 = interleaved
+    // stream + tree kernel.
     int32_t debug_mode;
 };
 
@@ -78,6 +79,10 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
 // Per-warp cp.async pipeline engine (LDGSTS ring per warp, ldmatrix.trans + HMMA); handles any
 // group range including the ragged tail (zero-fill copies).  binary16 input.
 int async_max_grid(uint32_t R, int debug_mode = 0);
+// Interleaved-stream variant of the cp.async engine: chunk results to chunk_res[n_chunks]
+// (GPU-wide interleaved chunk order), then a tree kernel (two launches).  R in 1..5.
+bool stream_supported(uint32_t R);
+cudaError_t launch_stream(const SpParams& p, float* chunk_res, uint64_t n_chunks, cudaStream_t s);
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.

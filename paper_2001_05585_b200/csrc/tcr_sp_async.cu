@@ -14,6 +14,7 @@
 // without holding registers, and the zero-fill form of cp.async gives the reference's zero
 // padding (reduction.hpp:244-245) for the ragged tail for free.  The destination of each
 // 16-byte line is XOR-swizzled on row bit 2 so the transposing ldmatrix is bank-conflict free.
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include "tcr_device.cuh"
@@ -334,6 +335,107 @@ __device__ __forceinline__ void as_group_warpblocks(const SpParams& p, uint64_t 
     }
 }
 
+
+// ===================================================================== interleaved stream engine
+// Two launches.  (1) sp_stream_kernel: every warp of the GPU takes global chunks gw, gw + TW,
+// gw + 2 TW, ... (TW = all warps of the grid), so at each step the whole GPU reads one
+// contiguous window of TW fragments -- the same DRAM-friendly sweep as a grid-stride read --
+// and writes one fp32 chunk result per chunk.  (2) sp_tree_kernel: per group, the reference's
+// block trees and the group tree over those chunk results, then the last-CTA finaliser.
+// The extra traffic is 8 bytes per chunk (1.6 % at R = 1).
+template <int RT, int D>
+__global__ void __launch_bounds__(kAsThreads) sp_stream_kernel(const SpParams p, float* chunk_res, uint64_t n_chunks) {
+    extern __shared__ __align__(128) unsigned char s_ring[];
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned c = lane & 3u;
+    const uint64_t TW = uint64_t(gridDim.x) * kAsWarps;
+    const uint64_t gw = uint64_t(blockIdx.x) * kAsWarps + warp;
+    const uint32_t ring = smem_u32(s_ring) + warp * D * kAsStageBytes;
+    constexpr uint64_t CE = uint64_t(RT) * 256u;
+    const uint64_t my_chunks = gw < n_chunks ? (n_chunks - gw + TW - 1) / TW : 0;
+    const uint64_t F = my_chunks * RT;
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint64_t n = p.n;
+    const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_off = swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+    bool ovf = false;
+    auto issue = [&](uint64_t f) {
+        if (f < F) {
+            const uint64_t k = f / RT, r = f - k * RT;
+            const uint64_t e = (gw + k * TW) * CE + r * 256u + 8u * lane;
+            const uint32_t bytes = e + 8 <= n ? 16u : (e < n ? uint32_t(n - e) * 2u : 0u);
+            cp_async16(ring + uint32_t(f % D) * kAsStageBytes + cp_dst, x + (e < n ? e : 0), bytes);
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int f = 0; f < D - 1; ++f) issue(uint64_t(f));
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t r = 0, pend = 0;
+    uint64_t ci = 0;
+    uint32_t a01p = 0, a23p = 0;
+    for (uint64_t f = 0; f < F; ++f) {
+        issue(f + D - 1);
+        cp_async_wait<D - 1>();
+        __syncwarp();
+        uint32_t d0, d1, d2, d3;
+        ldsm_x4_trans(ring + uint32_t(f % D) * kAsStageBytes + ld_off, d0, d1, d2, d3);
+        mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
+        if (++r == RT) {
+            const uint32_t pk = uint32_t(f32_to_h(acc[0])) | (uint32_t(f32_to_h(acc[2])) << 16);
+            const uint32_t vA = __shfl_sync(kFull, pk, 8 * c);
+            const uint32_t vB = __shfl_sync(kFull, pk, 8 * c + 4);
+            const uint32_t a01 = prmt(vA, vB, 0x5410), a23 = prmt(vA, vB, 0x7632);
+            if (pend) {
+                float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_16816(fin, a01p, a01, a23p, a23, kOnesF16x2, kOnesF16x2);
+                ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
+                if (lane == 0) {
+                    chunk_res[gw + (ci - 1) * TW] = fin[0];
+                    chunk_res[gw + ci * TW] = fin[2];
+                }
+                pend = 0;
+            } else {
+                a01p = a01;
+                a23p = a23;
+                pend = 1;
+            }
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            r = 0;
+            ++ci;
+        }
+    }
+    if (pend) {
+        float fin[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_16816(fin, a01p, a01p, a23p, a23p, kOnesF16x2, kOnesF16x2);
+        ovf |= !isfinite(fin[0]);
+        if (lane == 0) chunk_res[gw + (ci - 1) * TW] = fin[0];
+    }
+    cp_async_wait<0>();
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+}
+
+__global__ void __launch_bounds__(kAsThreads) sp_tree_kernel(const SpParams p, const float* chunk_res) {
+    __shared__ float s_chunk[kMaxChunksPerGroup];
+    __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ float s_scratch[32];
+    __shared__ int s_last;
+    const unsigned warp = threadIdx.x >> 5;
+    const uint32_t Cg = p.G * p.W;
+    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+        for (uint32_t i = threadIdx.x; i < Cg; i += blockDim.x) s_chunk[i] = __ldcg(chunk_res + gi * Cg + i);
+        __syncthreads();
+        tile_trees_blocks(p, gi, s_chunk, s_block, warp, kAsWarps);
+        __syncthreads();
+        if (warp == 0) tile_tree_group(p, gi, s_block);
+        __syncthreads();
+    }
+    __threadfence();
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kAsThreads);
+}
+
 // Ring depth per chain length: 2*R | D keeps every stage index and chunk pair compile-time.
 template <int RT> struct AsDepth { static constexpr int value = 8; };
 template <> struct AsDepth<1> { static constexpr int value = 16; };
@@ -441,7 +543,60 @@ bool as_attr_once() {
     return true;
 }
 
+using StreamKernel = void (*)(SpParams, float*, uint64_t);
+
+StreamKernel pick_stream(uint32_t R) {
+    switch (R) {
+    case 1: return sp_stream_kernel<1, AsDepth<1>::value>;
+    case 2: return sp_stream_kernel<2, AsDepth<2>::value>;
+    case 3: return sp_stream_kernel<3, AsDepth<3>::value>;
+    case 4: return sp_stream_kernel<4, AsDepth<4>::value>;
+    case 5: return sp_stream_kernel<5, AsDepth<5>::value>;
+    default: return nullptr;
+    }
+}
+
+uint32_t stream_smem(uint32_t R) {
+    switch (R) {
+    case 1: return as_smem_bytes<1>();
+    case 2: return as_smem_bytes<2>();
+    case 3: return as_smem_bytes<3>();
+    case 4: return as_smem_bytes<4>();
+    default: return as_smem_bytes<5>();
+    }
+}
+
 }  // namespace
+
+bool stream_supported(uint32_t R) { return pick_stream(R) != nullptr; }
+
+cudaError_t launch_stream(const SpParams& p, float* chunk_res, uint64_t n_chunks, cudaStream_t s) {
+    StreamKernel fn = pick_stream(p.R);
+    if (!fn) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        for (uint32_t R = 1; R <= 5; ++R) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(pick_stream(R), cudaFuncAttributeMaxDynamicSharedMemorySize, int(stream_smem(R)));
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kAsThreads, stream_smem(p.R));
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t want = (n_chunks + kAsWarps - 1) / kAsWarps;
+    const int grid = int(std::min<uint64_t>(want, uint64_t(per_sm) * sm_count()));
+    fn<<<grid, kAsThreads, stream_smem(p.R), s>>>(p, chunk_res, n_chunks);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    int per_sm_t = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, sp_tree_kernel, kAsThreads, 0);
+    const uint64_t groups = p.group_end - p.group_begin;
+    const int grid_t = int(std::min<uint64_t>(groups, uint64_t(per_sm_t < 1 ? 1 : per_sm_t) * sm_count()));
+    sp_tree_kernel<<<grid_t, kAsThreads, 0, s>>>(p, chunk_res);
+    return cudaGetLastError();
+}
 
 int async_max_grid(uint32_t R, int mode) {
     as_attr_once();
