@@ -57,8 +57,9 @@ struct SpParams {
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
     // cp.async engine: 8 = prefetch across a CTA's group boundaries (measured slower: 6.02 vs
     // 6.44 TB/s interleaved A/B, gpurun_out/exp11; results unchanged); 9 / 10 = ring depth 8 / 32
-    // for R = 1; 12 = disable the warp-blocks path (CTA-barrier block stage); 13 = interleaved
-    // stream + tree kernel.
+    // for R = 1; 12 = warp-blocks path (per-warp contiguous chunks, in-register block trees, no CTA
+    // barrier: 4.58 vs 6.42 TB/s, gpurun_out/exp14); 13 = GPU-wide interleaved stream + tree kernel
+    // (4.80 TB/s, exp15).  Both kept for the record; results are identical to the default.
     int32_t debug_mode;
 };
 

@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     bool static_ok = false, warp_blocks = false;
     if constexpr (RT > 0) {
         static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % D == 0;
-        warp_blocks = static_ok && ((Cg / kAsWarps) % p.W == 0) && p.debug_mode != 12;
+        warp_blocks = static_ok && ((Cg / kAsWarps) % p.W == 0) && p.debug_mode == 12;
     }
     if (threadIdx.x < kAsBufs) {
         s_done[threadIdx.x] = 0;
