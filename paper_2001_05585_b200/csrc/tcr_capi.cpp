@@ -251,7 +251,10 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         return TCR_OK;
     }
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
-        const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, uint64_t(tcr::async_max_grid(c->R, p.debug_mode))));
+        uint64_t maxg = uint64_t(tcr::async_max_grid(c->R, p.debug_mode));
+        if (const char* e = std::getenv("TCR_CTAS_PER_SM"))  // profiling knob
+            maxg = std::min<uint64_t>(maxg, uint64_t(std::atoi(e)) * tcr::sm_count());
+        const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, maxg));
         TCR_CUDA(tcr::launch_async(p, grid, s));
         ++g_launches;
         return TCR_OK;

@@ -20,6 +20,8 @@
 // sum, or the paper's atomicAdd.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tcr_device.cuh"
 #include "tcr_kernels.h"
 
@@ -435,7 +437,9 @@ SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B) {
     g.n_blocks = (n + g.block_elems - 1) / g.block_elems;
     if (g.n_blocks < 1) g.n_blocks = 1;
     uint32_t G = 1;
-    while (uint64_t(G) * g.block_elems < kGroupElemsTarget) G <<= 1;
+    uint64_t target = kGroupElemsTarget;
+    if (const char* e = std::getenv("TCR_GROUP_TARGET")) target = std::strtoull(e, nullptr, 10);  // profiling knob
+    while (uint64_t(G) * g.block_elems < target) G <<= 1;
     // keep the per-group chunk table in shared memory
     const uint64_t cap = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
     while (G > 1 && uint64_t(G) * g.W > cap) G >>= 1;
