@@ -286,7 +286,40 @@ __global__ void convert_kernel(const float* in, uint16_t* out, uint64_t count) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) out[i] = f32_to_h(in[i]);
 }
 
+// Streaming-read probe through cp.async (LDGSTS) instead of LDG: same grid-stride 512-byte
+// warp rows, a per-warp 8-stage shared-memory ring (profiling: the LDGSTS path's ceiling).
+__global__ void __launch_bounds__(256) read_probe_async_kernel(const uint4* x, uint64_t n16, uint32_t* sink) {
+    __shared__ __align__(128) uint4 ring[8][8][32];
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const uint64_t TW = uint64_t(gridDim.x) * 8;
+    const uint64_t gw = uint64_t(blockIdx.x) * 8 + warp;
+    const uint64_t rows = n16 / 32;
+    uint32_t acc = 0;
+    auto issue = [&](uint64_t k) {
+        const uint64_t row = gw + k * TW;
+        if (row < rows) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&ring[warp][k & 7][lane]));
+            asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst), "l"(x + row * 32 + lane) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int k = 0; k < 7; ++k) issue(uint64_t(k));
+    for (uint64_t k = 0; gw + k * TW < rows; ++k) {
+        issue(k + 7);
+        asm volatile("cp.async.wait_group 7;" ::: "memory");
+        const uint4 v = ring[warp][k & 7][lane];
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (acc == 0x9E3779B9u) sink[0] = acc;
+}
+
 }  // namespace
+
+cudaError_t launch_read_probe_async(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s) {
+    read_probe_async_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(x), bytes / 16, sink);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, uint64_t count, cudaStream_t s) {
     if (count == 0) return cudaSuccess;

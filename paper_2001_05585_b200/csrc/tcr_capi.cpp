@@ -824,7 +824,12 @@ int tcr_read_probe_async(const void* d_x, size_t bytes, void* stream) {
     Workspace* w = nullptr;
     int rc = get_ws(s, &w);
     if (rc) return rc;
-    TCR_CUDA(tcr::launch_read_probe(d_x, bytes, w->sink(), tcr::sm_count() * 8, s));
+    const char* mode = std::getenv("TCR_PROBE");  // profiling: "async" = cp.async probe, N CTAs/SM
+    const int per_sm = std::getenv("TCR_PROBE_CTAS") ? std::atoi(std::getenv("TCR_PROBE_CTAS")) : 8;
+    if (mode && std::string(mode) == "async")
+        TCR_CUDA(tcr::launch_read_probe_async(d_x, bytes, w->sink(), tcr::sm_count() * per_sm, s));
+    else
+        TCR_CUDA(tcr::launch_read_probe(d_x, bytes, w->sink(), tcr::sm_count() * per_sm, s));
     return TCR_OK;
 }
 

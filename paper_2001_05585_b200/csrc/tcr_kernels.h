@@ -120,6 +120,7 @@ int shuffle_max_grid();
 
 // Pure streaming-read probe: the achievable read bandwidth ceiling.
 cudaError_t launch_read_probe(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s);
+cudaError_t launch_read_probe_async(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s);
 
 // CUB DeviceReduce::Sum comparators.
 size_t cub_temp_bytes(uint64_t n, bool half_out);
