@@ -168,25 +168,33 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
     const uint32_t ld_base = ring_saddr + swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
     // global element offset of warp-local fragment g (chunk g/RT, fragment g%RT)
 #define TCR_FRAG_OFF(g) (uint64_t((g) / RT) * kAsWarps * CE + uint64_t((g) % RT) * 256u)
+    // iteration rotation: CTAs start their sweep of the group at different offsets so that
+    // concurrent CTAs do not hit the same DRAM channel phase (profiling mode 14)
+    const uint32_t rot = p.debug_mode == 14 ? uint32_t(blockIdx.x % iters) : 0u;
+    const uint64_t ITB = uint64_t(CPI) * kAsWarps * CE;     // elements per outer iteration
     if (prologue) {
+        const uint16_t* g0 = gp + uint64_t(rot) * ITB;
 #pragma unroll
         for (int u = 0; u < D - 1; ++u) {
-            cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
+            cp_async16(cp_dst + u * kAsStageBytes, g0 + TCR_FRAG_OFF(u), 16u);
             cp_async_commit();
         }
     }
     const uint16_t* gn = static_cast<const uint16_t*>(p.x) + (gnext * uint64_t(Cg) + warp) * CE + 8u * lane;
     float* out = s_chunk + warp;
+    uint32_t ip = rot;                                         // physical iteration
     for (uint32_t it = 0; it < iters; ++it) {
-        const uint16_t* gq = gp + uint64_t(it) * CPI * kAsWarps * CE;
+        const uint32_t ipn = ip + 1 == iters ? 0u : ip + 1;
+        const uint16_t* gq = gp + uint64_t(ip) * ITB;
+        const uint16_t* gqn = gp + uint64_t(ipn) * ITB;
         uint32_t a01p = 0, a23p = 0;
         float acc[4];
 #pragma unroll
         for (int u = 0; u < D; ++u) {
             // refill the stage consumed one step ago with fragment it*D + u + D-1
             if (it + 1 < iters || u == 0)
-                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + TCR_FRAG_OFF(u + D - 1),
-                           16u);
+                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes,
+                           u == 0 ? gq + TCR_FRAG_OFF(D - 1) : gqn + TCR_FRAG_OFF(u - 1), 16u);
             else if (prefetch_next)   // stage u-1 <- fragment u-1 of the next group
                 cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gn + TCR_FRAG_OFF(u - 1), 16u);
             cp_async_commit();
@@ -209,13 +217,14 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
                     mma_16816(fin, a01p, a01, a23p, a23, kOnesF16x2, kOnesF16x2);
                     ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
                     if (lane == 0) {
-                        const uint32_t ci = it * CPI + u / RT;     // odd chunk of the pair
+                        const uint32_t ci = ip * CPI + u / RT;     // odd chunk of the pair
                         out[(ci - 1) * kAsWarps] = fin[0];
                         out[ci * kAsWarps] = fin[2];
                     }
                 }
             }
         }
+        ip = ipn;
     }
 #undef TCR_FRAG_OFF
     if (!prefetch_next) cp_async_wait<0>();
