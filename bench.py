@@ -267,6 +267,7 @@ def main():
     # comparators (rank 0 view, same input): warp-shuffle CUDA-core kernel, CUB, read probe
     comparators = None
     if not args.no_comparators:
+      try:
         comparators = {}
         outc = torch.zeros(2, dtype=torch.float32, device=dev)
 
@@ -295,10 +296,13 @@ def main():
             "speedup_vs_warp_shuffle": t_sh / kms,
             "speedup_vs_cub_float": t_cf / kms,
         }
+      except Exception as exc:  # optional section: never lose the contract line
+        comparators = {"error": repr(exc)}
 
     # end-to-end through the reference-facing drop-in (host fp32 in pinned memory)
     e2e = None
     if not args.no_e2e:
+      try:
         xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
         xh.copy_(T.generate("uniform", 0, n, device=dev, dtype="float32", first=rank * n).cpu())
         torch.cuda.empty_cache()
@@ -330,13 +334,18 @@ def main():
                "path": "tcr_reduce_f32_host (pinned fp32 host input, pipelined H2D + fused convert/reduce)",
                "clock": "host wall clock around synchronous calls, max over ranks"}
         del xh
+      except Exception as exc:
+        e2e = {"error": repr(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+      try:
         v, kind, cores, val, times = cpu_reference_rate(1 << 26)
         cpu = {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind,
                "sample": "uniform[0,1) seed 0, n=2^26 (bounded sample of the 2^30 workload), m=16 R=1 B=1024",
                "seconds": times[0]}
+      except Exception as exc:
+        cpu = {"error": repr(exc)}
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")

@@ -184,20 +184,26 @@ __device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t ti
 }
 
 __device__ __forceinline__ void tile_tree_group(const SpParams& p, uint64_t tile, const float* blocks) {
+    // adjacent tree over the G (power of two) block results: each lane a contiguous segment
+    // (streaming binary-counter stack), then the xor tree across lanes
     const uint32_t G = p.G;
     const unsigned lane = lane_id();
     if (!p.group_partials) return;
     const uint32_t seg = G >= 32 ? G / 32 : 1;
     float x = 0.0f;
     if (lane * seg < G) {
-        float loc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? blocks[lane * seg + i] : 0.0f;
-#pragma unroll
-        for (int w2 = 1; w2 < 8; w2 <<= 1)
-#pragma unroll
-            for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
-        x = loc[0];
+        if (seg == 1) {
+            x = blocks[lane];
+        } else {
+            float stk[16];
+            int top = 0;
+            for (uint32_t i = 0; i < seg; ++i) {
+                float v = blocks[lane * seg + i];
+                for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
+                stk[top++] = v;
+            }
+            x = stk[0];
+        }
     }
     x = warp_tree_xor(x);
     if (lane == 0) p.group_partials[tile] = x;

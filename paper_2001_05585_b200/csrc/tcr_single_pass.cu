@@ -441,7 +441,8 @@ SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B) {
     if (const char* e = std::getenv("TCR_GROUP_TARGET")) target = std::strtoull(e, nullptr, 10);  // profiling knob
     while (uint64_t(G) * g.block_elems < target) G <<= 1;
     // keep the per-group chunk table in shared memory
-    const uint64_t cap = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
+    uint64_t cap = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
+    if (const char* e = std::getenv("TCR_GROUP_CAP")) cap = std::strtoull(e, nullptr, 10);  // profiling knob
     while (G > 1 && uint64_t(G) * g.W > cap) G >>= 1;
     g.G = G;
     g.group_elems = uint64_t(G) * g.block_elems;

@@ -30,6 +30,7 @@ using namespace pipe;
 constexpr int kAsWarps = 8;
 constexpr int kAsThreads = 32 * kAsWarps;
 constexpr int kAsStageBytes = 512;
+constexpr int kAsMaxChunks = 1024;                  // chunk table (allows larger groups)
 
 // L2 prefetch granularity of the 16-byte copies (PF: 0 none, 128, 256 bytes)
 template <int PF = 256>
@@ -461,8 +462,8 @@ constexpr uint32_t as_smem_bytes() {
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
     extern __shared__ __align__(128) unsigned char s_ring[];
-    __shared__ float s_chunk[kMaxChunksPerGroup];
-    __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ float s_chunk[kAsMaxChunks];
+    __shared__ float s_block[kAsMaxChunks];
     __shared__ float s_wblocks[kAsBufs * kMaxChunksPerGroup];
     __shared__ uint32_t s_done[kAsBufs];
     __shared__ uint32_t s_gen[kAsBufs];

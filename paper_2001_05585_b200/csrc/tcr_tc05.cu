@@ -192,7 +192,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
                         mbar_arrive(&empty[rs]);
                         continue;
                     }
-                    if (p.debug_mode < 3) mbar_wait(&tempty[ab], aph ^ 1);
+                    if (!(p.debug_mode >= 3 && p.debug_mode <= 5)) mbar_wait(&tempty[ab], aph ^ 1);
                     tc_fence_after();
                     const uint32_t sbase = smem_u32(ring + size_t(rs) * slot_bytes);
 #pragma unroll
@@ -226,7 +226,7 @@ tc05_kernel(const __grid_constant__ CUtensorMap tmap, const SpParams p, const ui
         const uint32_t c = lane & 3u;
         const int bar_id = 1 + int(eg);
         uint32_t t = 0, k = 0;
-        if (p.debug_mode == 1 || p.debug_mode >= 3) n_tiles_epi = 0;
+        if (p.debug_mode == 1 || (p.debug_mode >= 3 && p.debug_mode <= 5)) n_tiles_epi = 0;
         uint32_t P = 1;
         while (P < W) P <<= 1;
         for (uint64_t tile = blockIdx.x; tile < n_tiles_epi; tile += gridDim.x, ++k) {
