@@ -472,3 +472,22 @@ def test_split_degenerate_fractions(oracle):  # test_reduction.cpp:137-153
     cfg1 = T.ReductionConfig(variant=T.Variant.split, m=4, R=1, B=128, f=1.0, finalize=T.Finalize.ordered)
     sp = T.ReductionConfig(m=4, R=1, B=128, finalize=T.Finalize.ordered)
     assert T.reduce(aligned, cfg1).value == T.reduce(aligned, sp).value
+
+
+# --------------------------------------------------------------------------- 64-bit sizes (BASELINE cfg 5: 2^34)
+
+@pytest.mark.parametrize("engine", [T.Engine.mma_sync_async, T.Engine.tcgen05, T.Engine.mma_sync_regs])
+def test_beyond_32bit_indices(engine):
+    """n > 2^32 elements (8+ GiB binary16): 64-bit element / chunk indexing in every engine."""
+    n = (1 << 32) + 12345
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3 * n:
+        pytest.skip("not enough device memory")
+    x = T.generate("uniform", 7, n)
+    exact, _ = T.exact_sum(x)
+    o = T.reduce(x, cfg16(R=1, B=1024, engine=engine))
+    assert not o.overflow
+    assert abs(o.value - exact) / exact <= 1e-5
+    assert o.atomic_count == -(-n // 8192)
+    del x
+    torch.cuda.empty_cache()
