@@ -486,7 +486,17 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     __syncthreads();
     bool prefetched = false;   // this group's first D-1 fragments are already in flight
     uint32_t k_iter = 0;
-    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x, ++k_iter) {
+    // group order: strided over CTAs (default) or, in profiling mode 15, one contiguous range of
+    // groups per CTA with the stream prefetching across group boundaries
+    const bool contiguous = p.debug_mode == 15;
+    const uint64_t ngr = p.group_end - p.group_begin;
+    const uint64_t per = (ngr + gridDim.x - 1) / gridDim.x;
+    const uint64_t g_first = contiguous ? p.group_begin + blockIdx.x * per : p.group_begin + blockIdx.x;
+    const uint64_t g_last = contiguous ? (p.group_begin + (blockIdx.x + 1) * per < p.group_end
+                                              ? p.group_begin + (blockIdx.x + 1) * per : p.group_end)
+                                       : p.group_end;
+    const uint64_t g_step = contiguous ? 1 : gridDim.x;
+    for (uint64_t gi = g_first; gi < g_last; gi += g_step, ++k_iter) {
         if constexpr (RT > 0) {
             if (warp_blocks && gi < full_groups) {
                 as_group_warpblocks<RT, D>(p, gi, k_iter, ring, s_wblocks, s_done, s_gen, ovf);
@@ -495,8 +505,8 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
         }
         if constexpr (RT > 0) {
             if (static_ok && gi < full_groups) {
-                const uint64_t gn = gi + gridDim.x;
-                const bool next_static = gn < p.group_end && gn < full_groups && p.debug_mode == 8;
+                const uint64_t gn = gi + g_step;
+                const bool next_static = gn < g_last && gn < full_groups && (p.debug_mode == 8 || contiguous);
                 as_group_static<RT, D>(p, gi, ring, s_chunk, ovf, !prefetched, next_static, gn);
                 prefetched = next_static;
             } else {
