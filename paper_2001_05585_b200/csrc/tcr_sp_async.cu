@@ -30,7 +30,6 @@ using namespace pipe;
 constexpr int kAsWarps = 8;
 constexpr int kAsThreads = 32 * kAsWarps;
 constexpr int kAsStageBytes = 512;
-constexpr int kAsMaxChunks = 1024;                  // chunk table (allows larger groups)
 
 // L2 prefetch granularity of the 16-byte copies (PF: 0 none, 128, 256 bytes)
 template <int PF = 256>
@@ -233,6 +232,7 @@ __device__ __forceinline__ void as_group_static(const SpParams& p, uint64_t gi, 
 
 
 constexpr int kAsBufs = 4;   // per-group block tables in flight (warp-blocks mode)
+constexpr int kWbMaxBlocks = 256;
 
 // Warp-blocks mode: warp w owns the contiguous chunks [w*Cpw, (w+1)*Cpw) of the group, where
 // Cpw = Cg/8 is a whole number of logical blocks, so the reference's block tree (:253) runs in
@@ -256,7 +256,7 @@ __device__ __forceinline__ void as_group_warpblocks(const SpParams& p, uint64_t 
     const uint32_t bpb = 32u / P;                 // blocks per 32-lane batch
     const uint32_t b0 = warp * (Cpw / W);         // first group-local block of this warp
     const uint32_t buf = k_iter % kAsBufs;
-    float* blocks = s_blocks + buf * kMaxChunksPerGroup;
+    float* blocks = s_blocks + buf * kWbMaxBlocks;
     // the buffer must have been released by the tree of iteration k_iter - kAsBufs
     if (lane == 0)
         while (s_gen[buf] != k_iter - kAsBufs) { }
@@ -462,9 +462,9 @@ constexpr uint32_t as_smem_bytes() {
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
     extern __shared__ __align__(128) unsigned char s_ring[];
-    __shared__ float s_chunk[kAsMaxChunks];
-    __shared__ float s_block[kAsMaxChunks];
-    __shared__ float s_wblocks[kAsBufs * kMaxChunksPerGroup];
+    __shared__ float s_chunk[kMaxChunksPerGroup];
+    __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ float s_wblocks[kAsBufs * kWbMaxBlocks];
     __shared__ uint32_t s_done[kAsBufs];
     __shared__ uint32_t s_gen[kAsBufs];
     __shared__ float s_scratch[32];
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     bool static_ok = false, warp_blocks = false;
     if constexpr (RT > 0) {
         static_ok = (Cg % kAsWarps == 0) && ((Cg / kAsWarps) * RT) % D == 0;
-        warp_blocks = static_ok && ((Cg / kAsWarps) % p.W == 0) && p.debug_mode == 12;
+        warp_blocks = static_ok && ((Cg / kAsWarps) % p.W == 0) && p.G <= uint32_t(kWbMaxBlocks) && p.debug_mode == 12;
     }
     if (threadIdx.x < kAsBufs) {
         s_done[threadIdx.x] = 0;

@@ -31,7 +31,7 @@ using namespace pipe;
 
 constexpr int kEpiWarp0 = 2;
 constexpr int kAccBufs = 8;         // TMEM accumulator ring depth
-constexpr uint32_t kRingBytes = 192 * 1024;
+constexpr uint32_t kRingBytes = 160 * 1024;
 
 // UMMA shared-memory matrix descriptor (sm_100: version 1 at bits 46-47).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -80,7 +80,7 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 constexpr int kEpiGroups = 3;                         // epilogue warpgroups, round-robin over slots
-constexpr int kTileBufs = 8;                            // per-tile chunk/block tables in flight
+constexpr int kTileBufs = 4;                            // per-tile chunk/block tables in flight
 
 __host__ __device__ constexpr int tc_threads(int eg) { return 64 + 128 * eg; }  // TMA warp + MMA warp + epilogue
 
