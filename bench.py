@@ -231,6 +231,7 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step(False)
     launches_per_step = lib.tcr_last_launch_count()
+    engine_used = T.Engine(lib.tcr_last_engine()).name
     barrier()
     with Clocks(local) as clk:
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -360,6 +361,7 @@ def main():
             "config": {"workload": "BASELINE configs[1]: single_pass chained-MMA reduction, n=2^30 fp16 per GPU, "
                                    "m=16 R=%d B=%d, uniform[0,1) seed 0" % (args.R, args.B),
                        "n_per_gpu": n, "n_total": world * n, "m": 16, "R": args.R, "B": args.B,
+                       "engine": engine_used,
                        "parallelism": f"shard{world}" + ("+nccl_allreduce" if world > 1 else ""),
                        "l2": "input 2 GiB per GPU > 126 MB L2: no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

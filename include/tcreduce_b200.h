@@ -123,6 +123,16 @@ int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* c
 int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* cfg, float* d_result,
                               uint32_t* d_overflow, void* cuda_stream);
 
+/* Single-process multi-GPU single_pass (BASELINE configs[4]): shard i -- d_x[i],
+ * n[i] binary16 elements resident on device devices[i] -- is reduced by its GPU with the same
+ * kernels, then ONE ncclAllReduce(sum) combines the ngpu fp32 partials over NVLink/NVSwitch
+ * (communicators are created once per device list and cached).  Every shard but the last must
+ * hold a multiple of tcr_group_elems(cfg) elements (so the global block partition is the
+ * single-GPU one); out gets the combined value, the OR of the overflow flags and the reference
+ * counters of the total length. */
+int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const int32_t* devices, int32_t ngpu,
+                           const tcr_config* cfg, tcr_outcome* out);
+
 /* Parity hook: per-block fp32 results of single_pass (the reference's block_results,
  * reduction.hpp:248-255) into d_blocks[tcr_block_count(n, cfg)]. */
 int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* cfg, float* d_blocks,

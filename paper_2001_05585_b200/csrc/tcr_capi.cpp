@@ -20,6 +20,11 @@
 
 #include "tcr_kernels.h"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <vector>
+
 namespace {
 
 thread_local std::string g_err;
@@ -645,6 +650,121 @@ int tcr_reduce_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, tc
 
 int tcr_reduce_f32_device(const float* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
     return reduce_device(d_x, n, c, out, true, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+namespace {
+
+// NCCL is resolved lazily with dlopen: no link-time dependency, and inside a PyTorch process the
+// already-loaded libnccl.so.2 is reused instead of a second copy.
+struct Nccl {
+    decltype(&ncclCommInitAll) comm_init_all = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+    bool ok = false;
+};
+
+const Nccl& nccl() {
+    static Nccl n = [] {
+        Nccl r;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return r;
+        r.comm_init_all = reinterpret_cast<decltype(&ncclCommInitAll)>(dlsym(h, "ncclCommInitAll"));
+        r.group_start = reinterpret_cast<decltype(&ncclGroupStart)>(dlsym(h, "ncclGroupStart"));
+        r.group_end = reinterpret_cast<decltype(&ncclGroupEnd)>(dlsym(h, "ncclGroupEnd"));
+        r.all_reduce = reinterpret_cast<decltype(&ncclAllReduce)>(dlsym(h, "ncclAllReduce"));
+        r.error_string = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        r.ok = r.comm_init_all && r.group_start && r.group_end && r.all_reduce && r.error_string;
+        return r;
+    }();
+    return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const int32_t* devices, int32_t ngpu,
+                           const tcr_config* c, tcr_outcome* out) {
+    g_launches = 0;
+    if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
+    std::memset(out, 0, sizeof *out);
+    if (!d_x || !n || !devices || ngpu < 1) return fail(TCR_INVALID_ARGUMENT, "bad shard description");
+    int rc = validate_cfg(c);
+    if (rc) return rc;
+    if (c->variant != TCR_SINGLE_PASS) return fail(TCR_NOT_SUPPORTED, "sharded reduce implements single_pass");
+    rc = check_supported(c);
+    if (rc) return rc;
+    uint64_t total = 0;
+    const uint64_t ge = tcr::make_geometry(1, c->m, c->R, c->B).group_elems;
+    for (int i = 0; i < ngpu; ++i) {
+        if (n[i] == 0 || !d_x[i]) return fail(TCR_INVALID_ARGUMENT, "empty shard");
+        if (i + 1 < ngpu && n[i] % ge != 0)
+            return fail(TCR_INVALID_ARGUMENT, "shards must be multiples of tcr_group_elems except the last");
+        total += n[i];
+    }
+    const Nccl& N = nccl();
+    if (!N.ok) return fail(TCR_NCCL_ERROR, "libnccl.so.2 not found");
+    int dev0 = 0;
+    TCR_CUDA(cudaGetDevice(&dev0));
+    // communicator cache keyed by the device list
+    static std::mutex mu;
+    static std::map<std::vector<int>, std::vector<ncclComm_t>> comms;
+    std::vector<int> key(devices, devices + ngpu);
+    std::vector<ncclComm_t>* cm = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = comms.find(key);
+        if (it == comms.end()) {
+            std::vector<ncclComm_t> v(static_cast<size_t>(ngpu));
+            const ncclResult_t r = N.comm_init_all(v.data(), ngpu, key.data());
+            if (r != ncclSuccess) return fail(TCR_NCCL_ERROR, std::string("ncclCommInitAll: ") + N.error_string(r));
+            it = comms.emplace(key, std::move(v)).first;
+        }
+        cm = &it->second;
+    }
+    tcr_config cc = *c;
+    if (cc.finalize == TCR_FINALIZE_ORDERED) cc.finalize = TCR_FINALIZE_TREE;  // per shard; combine below
+    std::vector<Workspace*> ws(static_cast<size_t>(ngpu));
+    int launches = 0;
+    for (int i = 0; i < ngpu; ++i) {
+        TCR_CUDA(cudaSetDevice(devices[i]));
+        rc = get_ws(nullptr, &ws[size_t(i)]);
+        if (rc) return rc;
+        TCR_CUDA(cudaMemsetAsync(ws[size_t(i)]->overflow(), 0, 4, nullptr));
+        rc = sp_async(d_x[i], n[i], &cc, false, ws[size_t(i)]->result(), ws[size_t(i)]->overflow(), nullptr);
+        if (rc) return rc;
+        launches += g_launches;
+    }
+    ncclResult_t r = N.group_start();
+    for (int i = 0; r == ncclSuccess && i < ngpu; ++i) {
+        float* v = ws[size_t(i)]->result();
+        r = N.all_reduce(v, v, 1, ncclFloat, ncclSum, (*cm)[size_t(i)], nullptr);
+    }
+    const ncclResult_t r2 = N.group_end();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(TCR_NCCL_ERROR, std::string("ncclAllReduce: ") + N.error_string(r != ncclSuccess ? r : r2));
+    uint32_t ovf = 0;
+    float value = 0.0f;
+    for (int i = ngpu - 1; i >= 0; --i) {
+        TCR_CUDA(cudaSetDevice(devices[i]));
+        float v;
+        uint32_t o;
+        rc = read_result(ws[size_t(i)], nullptr, &v, &o);
+        if (rc) return rc;
+        ovf |= o;
+        value = v;  // identical on every rank after the all-reduce; keep device 0's
+    }
+    TCR_CUDA(cudaSetDevice(dev0));
+    g_launches = launches;
+    out->value = value;
+    out->overflow = ovf ? 1 : 0;
+    counters(total, c, out);
+    return TCR_OK;
 }
 
 int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_blocks,

@@ -491,3 +491,32 @@ def test_beyond_32bit_indices(engine):
     assert o.atomic_count == -(-n // 8192)
     del x
     torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------------------------- NCCL sharded C ABI
+
+def test_sharded_c_abi_single_gpu(oracle):
+    """tcr_reduce_f16_sharded: per-device kernels + one ncclAllReduce (1 device here; the driver's
+    multi-GPU runs use the same call path per rank through bench.py / torch.distributed)."""
+    import ctypes as C
+    from paper_2001_05585_b200 import _capi
+    from paper_2001_05585_b200 import sharded as S
+    cfg = cfg16(R=1, B=1024)
+    ge = S.group_elems(cfg)
+    n0, n1 = 3 * ge, ge + 777
+    h = oracle.generate_f16("uniform", 4, n0 + n1)
+    xd = to_dev_f16(h)
+    parts = (C.c_void_p * 1)(C.c_void_p(xd.data_ptr()))
+    ns = (C.c_size_t * 1)(n0 + n1)
+    devs = (C.c_int32 * 1)(0)
+    out = _capi.tcr_outcome()
+    c = cfg.to_c()
+    _capi.check(_capi.load().tcr_reduce_f16_sharded(parts, ns, devs, 1, C.byref(c), C.byref(out)))
+    ref = T.reduce(xd, cfg)
+    assert out.value == ref.value and out.atomic_count == ref.atomic_count
+    # bad shard alignment is an invalid argument
+    parts2 = (C.c_void_p * 2)(C.c_void_p(xd.data_ptr()), C.c_void_p(xd[n0:].data_ptr()))
+    ns2 = (C.c_size_t * 2)(n0 + 5, n1)
+    devs2 = (C.c_int32 * 2)(0, 0)
+    rc = _capi.load().tcr_reduce_f16_sharded(parts2, ns2, devs2, 2, C.byref(c), C.byref(out))
+    assert rc == _capi.TCR_INVALID_ARGUMENT
