@@ -24,6 +24,7 @@
 
 #include "tcr_device.cuh"
 #include "tcr_kernels.h"
+#include "tcr_pipeline.cuh"
 
 namespace tcr {
 
@@ -344,23 +345,8 @@ __global__ void __launch_bounds__(kSpThreads, 3) sp16_kernel(const SpParams p) {
         }
         __syncthreads();
 
-        // ---- group stage: adjacent tree over the G block results (power of two)
-        if (warp == 0 && p.group_partials) {
-            const uint32_t seg = G >= 32 ? G / 32 : 1;
-            float v = 0.0f;
-            if (lane * seg < G) {
-                float loc[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) loc[i] = (uint32_t(i) < seg) ? s_block[lane * seg + i] : 0.0f;
-#pragma unroll
-                for (int w2 = 1; w2 < 8; w2 <<= 1)
-#pragma unroll
-                    for (int i = 0; i < 8; i += 2 * w2) loc[i] = loc[i] + loc[i + w2];
-                v = loc[0];
-            }
-            v = warp_tree_xor(v);
-            if (lane == 0) p.group_partials[gi] = v;
-        }
+        // ---- group stage: adjacent tree over the G block results (power of two, any G)
+        if (warp == 0) pipe::tile_tree_group(p, gi, s_block);
         __syncthreads();
     }
 
