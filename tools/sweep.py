@@ -85,6 +85,18 @@ def main():
                                 "launches": lib.tcr_last_launch_count()})
                     csv_rows.append(("uniform", 0, n, "single_pass", 16, R, B, val, med, engine.name))
                     print(json.dumps(pts[-1]), flush=True)
+        # fragment sides m != 16 (selector-matrix engine), the reference default m = 4 first
+        mpts = []
+        for (m, R, B) in ((4, 1, 128), (4, 4, 128), (2, 1, 128), (8, 1, 128), (8, 4, 128), (32, 1, 128), (64, 1, 128),
+                          (128, 1, 128)):
+            cfg = T.ReductionConfig(m=m, R=R, B=B)
+            c = cfg.to_c()
+            med, best = time_fn(lambda: _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(c), rp, op, sp)),
+                                args.reps)
+            torch.cuda.synchronize()
+            mpts.append({"m": m, "R": R, "B": B, "ms": med, "gelem_s": n / med / 1e6, "gb_s": 2 * n / med / 1e6,
+                         "frac_hbm": 2 * n / med / 1e6 / peak, "value": res[0].item()})
+            print(json.dumps(mpts[-1]), flush=True)
         comps = {}
         comps["warp_shuffle_fp32"] = time_fn(lambda: _capi.check(lib.tcr_shuffle_f16_async(xp, n, rp, sp)), args.reps)[0]
         comps["cub_half_in_float_acc"] = time_fn(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 0, rp, sp)),
@@ -92,7 +104,7 @@ def main():
         comps["cub_half_in_half_acc"] = time_fn(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 1, rp, sp)),
                                                 args.reps)[0]
         comps["read_probe"] = time_fn(lambda: _capi.check(lib.tcr_read_probe_async(xp, 2 * n, sp)), args.reps)[0]
-        out["sweep"] = {"n": n, "dist": "uniform s0", "points": pts,
+        out["sweep"] = {"n": n, "dist": "uniform s0", "points": pts, "m_points": mpts,
                         "comparators_ms": comps,
                         "comparators_gelem_s": {k: n / v / 1e6 for k, v in comps.items()}}
         best = min(pts, key=lambda p: p["ms"])
