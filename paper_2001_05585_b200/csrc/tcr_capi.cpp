@@ -68,8 +68,10 @@ struct Workspace {
     size_t lvl_f32_cap = 0;
     uint16_t* lvl16[2] = {nullptr, nullptr};
     size_t lvl16_cap[2] = {0, 0};
-    float* chunk_res = nullptr;  // interleaved stream engine
-    size_t chunk_res_cap = 0;
+    float* block_scratch = nullptr;  // split work units of the cp.async engine
+    size_t bs_cap = 0;
+    uint32_t* group_count = nullptr;  // kept zero between launches
+    size_t gc_cap = 0;
     float* stage = nullptr;  // host path of the non-single_pass variants
     size_t stage_cap = 0;
     // pipelined host path
@@ -119,6 +121,15 @@ int ensure(T** p, size_t* cap, size_t count, cudaStream_t s) {
     const size_t want = std::max<size_t>(count, 1024);
     TCR_CUDA(cudaMalloc(reinterpret_cast<void**>(p), want * sizeof(T)));
     *cap = want;
+    return TCR_OK;
+}
+
+template <typename T>
+int ensure_zero(T** p, size_t* cap, size_t count, cudaStream_t s) {
+    if (*cap >= count) return TCR_OK;
+    const int rc = ensure(p, cap, count, s);
+    if (rc) return rc;
+    TCR_CUDA(cudaMemsetAsync(*p, 0, *cap * sizeof(T), s));
     return TCR_OK;
 }
 
@@ -229,6 +240,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     p.atomic_order = c->atomic_order;
     p.atomic_seed = c->atomic_seed;
     if (const char* dm = std::getenv("TCR_DEBUG_MODE")) p.debug_mode = std::atoi(dm);
+    p.split = 1;
     if (c->finalize == TCR_FINALIZE_ATOMIC && g0 == 0) {
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
         ++g_launches;
@@ -246,20 +258,21 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     if ((g0 != 0 || g1 != g.n_groups) && (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC))
         engine = TCR_ENGINE_MMA_SYNC_REGS;
     g_engine = engine;
-    if (engine == TCR_ENGINE_MMA_SYNC_ASYNC && p.debug_mode == 13 && tcr::stream_supported(c->R) && g0 == 0 &&
-        g1 == g.n_groups) {
-        const uint64_t n_chunks = g.n_groups * uint64_t(g.G) * g.W;
-        rc = ensure(&w->chunk_res, &w->chunk_res_cap, n_chunks, s);
-        if (rc) return rc;
-        TCR_CUDA(tcr::launch_stream(p, w->chunk_res, n_chunks, s));
-        g_launches += 2;
-        return TCR_OK;
-    }
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
         uint64_t maxg = uint64_t(tcr::async_max_grid(c->R, p.debug_mode));
         if (const char* e = std::getenv("TCR_CTAS_PER_SM"))  // profiling knob
             maxg = std::min<uint64_t>(maxg, uint64_t(std::atoi(e)) * tcr::sm_count());
-        const int grid = int(std::min<uint64_t>(p.group_end - p.group_begin, maxg));
+        const uint64_t groups = p.group_end - p.group_begin;
+        p.split = tcr::async_split(g, groups, int(maxg));
+        if (p.split > 1) {
+            rc = ensure(&w->block_scratch, &w->bs_cap, g.n_groups * g.G, s);
+            if (rc) return rc;
+            rc = ensure_zero(&w->group_count, &w->gc_cap, g.n_groups, s);
+            if (rc) return rc;
+            p.block_scratch = w->block_scratch;
+            p.group_count = w->group_count;
+        }
+        const int grid = int(std::min<uint64_t>(groups * p.split, maxg));
         TCR_CUDA(tcr::launch_async(p, grid, s));
         ++g_launches;
         return TCR_OK;

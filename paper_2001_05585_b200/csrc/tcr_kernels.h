@@ -51,15 +51,20 @@ struct SpParams {
     int32_t finalize;
     int32_t atomic_order;
     uint64_t atomic_seed;
+    // Work units of the cp.async engine: every group is split into `split` (power of two, divides
+    // G) pieces of G/split whole blocks so that the unit count balances over the grid.  With
+    // split > 1 the piece's block results go to block_scratch[n_groups*G] and the CTA completing
+    // a group (group_count[n_groups], zero on entry and on exit) runs its group tree.  The tree
+    // -- and so the TREE result -- is the same for every split.
+    uint32_t split;
+    float* block_scratch;
+    uint32_t* group_count;
     // Profiling hook (env TCR_DEBUG_MODE, never set in production): tcgen05 engine only --
     // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
     // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
-    // cp.async engine: 8 = prefetch across a CTA's group boundaries (measured slower: 6.02 vs
-    // 6.44 TB/s interleaved A/B, gpurun_out/exp11; results unchanged); 9 / 10 = ring depth 8 / 32
-    // for R = 1; 12 = warp-blocks path (per-warp contiguous chunks, in-register block trees, no CTA
-    // barrier: 4.58 vs 6.42 TB/s, gpurun_out/exp14); 13 = GPU-wide interleaved stream + tree kernel
-    // (4.80 TB/s, exp15).  Both kept for the record; results are identical to the default.
+    // cp.async engine: 8 = prefetch across a CTA's unit boundaries; 9 / 10 = ring depth 8 / 32
+    // for R = 1.  Results are identical to the default in modes 8-10.
     int32_t debug_mode;
 };
 
@@ -80,11 +85,10 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
 // Per-warp cp.async pipeline engine (LDGSTS ring per warp, ldmatrix.trans + HMMA); handles any
 // group range including the ragged tail (zero-fill copies).  binary16 input.
 int async_max_grid(uint32_t R, int debug_mode = 0);
-// Interleaved-stream variant of the cp.async engine: chunk results to chunk_res[n_chunks]
-// (GPU-wide interleaved chunk order), then a tree kernel (two launches).  R in 1..5.
-bool stream_supported(uint32_t R);
-cudaError_t launch_stream(const SpParams& p, float* chunk_res, uint64_t n_chunks, cudaStream_t s);
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
+// Pieces per group for the cp.async engine over `groups` groups on `grid` CTAs (cost model:
+// ceil(units / grid) x (unit elements + per-unit overhead)); env TCR_SPLIT overrides.
+uint32_t async_split(const SpGeometry& g, uint64_t groups, int grid);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.
 bool genm_supported(const SpGeometry& g);

@@ -160,21 +160,21 @@ __device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_sc
     if (threadIdx.x == 0) *p.ticket = 0u;
 }
 
-// Block stage (reference pairwise tree over W chunk results, reduction.hpp:253, :90-101) and
-// group stage (adjacent tree over G block results) for one tile, by `nwarps` warps starting at
-// warp index w0 of the caller's warp set (w = caller's index in that set).
-__device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t tile, const float* chunks,
-                                                  float* blocks, uint32_t w, uint32_t nwarps) {
-    const uint32_t W = p.W, G = p.G;
+// Block stage (reference pairwise tree over W chunk results, reduction.hpp:253, :90-101) for the
+// nblk logical blocks starting at global block block0, by `nwarps` warps (w = caller's index in
+// that set): chunk results chunks[b*W + j] -> blocks[b].
+__device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t block0, uint32_t nblk,
+                                                   const float* chunks, float* blocks, uint32_t w, uint32_t nwarps) {
+    const uint32_t W = p.W;
     const unsigned lane = lane_id();
     uint32_t P = 1;
     while (P < W) P <<= 1;
-    for (uint32_t b = w; b < G; b += nwarps) {
+    for (uint32_t b = w; b < nblk; b += nwarps) {
         float x = lane < W ? chunks[b * W + lane] : 0.0f;
         for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
         if (lane == 0) {
             blocks[b] = x;
-            const uint64_t gb = tile * G + b;
+            const uint64_t gb = block0 + b;
             if (gb < p.n_blocks) {
                 if (p.block_partials) p.block_partials[gb] = x;
                 if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
@@ -183,22 +183,34 @@ __device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t ti
     }
 }
 
+// Block stage for one whole group (tile) of G blocks.
+__device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t tile, const float* chunks,
+                                                  float* blocks, uint32_t w, uint32_t nwarps) {
+    range_trees_blocks(p, tile * p.G, p.G, chunks, blocks, w, nwarps);
+}
+
+// Group stage: adjacent tree over the G (power of two) block results of group `tile`, by one
+// warp: each lane a contiguous segment (streaming binary-counter stack), then the xor tree
+// across lanes.  GLOBAL: `blocks` lives in global memory written by other CTAs (L2 loads).
+template <bool GLOBAL = false>
 __device__ __forceinline__ void tile_tree_group(const SpParams& p, uint64_t tile, const float* blocks) {
-    // adjacent tree over the G (power of two) block results: each lane a contiguous segment
-    // (streaming binary-counter stack), then the xor tree across lanes
     const uint32_t G = p.G;
     const unsigned lane = lane_id();
     if (!p.group_partials) return;
     const uint32_t seg = G >= 32 ? G / 32 : 1;
+    auto ld = [&](uint32_t i) -> float {
+        if constexpr (GLOBAL) return __ldcg(blocks + i);
+        else return blocks[i];
+    };
     float x = 0.0f;
     if (lane * seg < G) {
         if (seg == 1) {
-            x = blocks[lane];
+            x = ld(lane);
         } else {
             float stk[16];
             int top = 0;
             for (uint32_t i = 0; i < seg; ++i) {
-                float v = blocks[lane * seg + i];
+                float v = ld(lane * seg + i);
                 for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
                 stk[top++] = v;
             }

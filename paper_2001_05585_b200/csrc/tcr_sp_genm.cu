@@ -30,7 +30,7 @@ using namespace pipe;
 
 constexpr int kGmWarps = 8;
 constexpr int kGmThreads = 32 * kGmWarps;
-constexpr int kGmTrDepth = 16;                // transposed stream: 512-byte tile stages per warp
+constexpr int kGmTrDepth = 8;                 // transposed stream: 512-byte tile stages per warp
 
 __device__ __forceinline__ void cp16(uint32_t saddr, const void* g, uint32_t bytes) {
     asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
@@ -93,7 +93,7 @@ struct NatShape {
     uint32_t L, CR, unit_rows, chunks_per_unit;
 };
 
-template <int M, int NU>   // NU = units in flight per warp (ring depth)
+template <int M>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, const NatShape S) {
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ float s_scratch[32];
@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
     const unsigned g = lane >> 2, c = lane & 3u;
     const uint32_t R = p.R;
     const uint32_t unit_bytes = S.unit_rows * 32u;
-    float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * uint32_t(NU) * unit_bytes);
+    float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * 2u * unit_bytes);
     float* s_block = s_chunk + kMaxChunksGenm;
-    const uint32_t buf0 = smem_u32(dsm) + warp * uint32_t(NU) * unit_bytes;
+    const uint32_t buf0 = smem_u32(dsm) + warp * 2u * unit_bytes;
     const uint64_t chunk_el = uint64_t(R) * M * M;
     const uint32_t Cg = p.G * p.W;
     const uint32_t units = (Cg + S.chunks_per_unit - 1) / S.chunks_per_unit;
@@ -135,15 +135,14 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
             }
             cp_commit();
         };
-        // ring of NU unit buffers: unit k of this warp (u = warp + k*8) lives in buffer k % NU
-#pragma unroll
-        for (int k = 0; k < NU - 1; ++k) issue(warp + uint32_t(k) * kGmWarps, uint32_t(k));
-        uint32_t k = 0;
-        for (uint32_t u = warp; u < units; u += kGmWarps, ++k) {
-            issue(u + uint32_t(NU - 1) * kGmWarps, (k + NU - 1) % NU);
-            cp_wait<NU - 1>();
+        uint32_t b = 0;
+        uint32_t u = warp;
+        issue(u, 0);
+        for (; u < units; u += kGmWarps, b ^= 1u) {
+            issue(u + kGmWarps, b ^ 1u);
+            cp_wait<1>();
             __syncwarp();
-            const uint32_t base = buf0 + (k % NU) * unit_bytes;
+            const uint32_t base = buf0 + b * unit_bytes;
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             const uint32_t steps = S.L > 0 ? S.L : 1u;
             for (uint32_t i = 0; i < steps; ++i) {
@@ -363,13 +362,8 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) 
     if (g.m == 2 || g.m == 4) {
         NatShape S;
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
-        // ring depth: as many units as fit 8 KiB per warp (>= 2)
-        const uint32_t ub = S.unit_rows * 32u;
-        const int NU = ub <= 512 ? 16 : ub <= 1024 ? 8 : ub <= 2048 ? 4 : 2;
-        const uint32_t dyn = kGmWarps * uint32_t(NU) * ub + 2u * kMaxChunksGenm * 4u;
-        void (*fn)(SpParams, NatShape) = nullptr;
-        if (g.m == 2) fn = NU == 16 ? gm_nat_kernel<2, 16> : NU == 8 ? gm_nat_kernel<2, 8> : NU == 4 ? gm_nat_kernel<2, 4> : gm_nat_kernel<2, 2>;
-        else fn = NU == 16 ? gm_nat_kernel<4, 16> : NU == 8 ? gm_nat_kernel<4, 8> : NU == 4 ? gm_nat_kernel<4, 4> : gm_nat_kernel<4, 2>;
+        const uint32_t dyn = kGmWarps * 2u * S.unit_rows * 32u + 2u * kMaxChunksGenm * 4u;
+        auto fn = g.m == 2 ? gm_nat_kernel<2> : gm_nat_kernel<4>;
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
         if (e != cudaSuccess) return e;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGmThreads, dyn);

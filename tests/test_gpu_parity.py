@@ -520,3 +520,31 @@ def test_sharded_c_abi_single_gpu(oracle):
     devs2 = (C.c_int32 * 2)(0, 0)
     rc = _capi.load().tcr_reduce_f16_sharded(parts2, ns2, devs2, 2, C.byref(c), C.byref(out))
     assert rc == _capi.TCR_INVALID_ARGUMENT
+
+
+# --------------------------------------------------------------------------- split work units
+
+@pytest.mark.parametrize("R,B", [(1, 1024), (3, 256), (4, 128), (5, 32), (6, 64)])
+def test_split_units_identical(oracle, R, B, monkeypatch):
+    """The cp.async engine splits groups into pieces for grid balance (TCR_SPLIT forces the
+    piece count): values, block results and overflow are identical for every split."""
+    cfg = cfg16(R=R, B=B, engine=T.Engine.mma_sync_async)
+    from paper_2001_05585_b200 import sharded as S
+    n = 37 * S.group_elems(cfg) + 4097
+    h = oracle.generate_f16("normal", 9, n)
+    xd = to_dev_f16(h)
+    base = {}
+    for split in ("1", "2", "4", "8", "64"):
+        monkeypatch.setenv("TCR_SPLIT", split)
+        for fin in (T.Finalize.tree, T.Finalize.ordered):
+            o = T.reduce(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync_async, finalize=fin))
+            assert base.setdefault(fin, o.value) == o.value, (split, fin)
+        blocks = T.block_results(xd, cfg).cpu().numpy()
+        if "blocks" in base:
+            assert np.array_equal(blocks.view(np.uint32), base["blocks"].view(np.uint32))
+        else:
+            base["blocks"] = blocks
+    # twice in a row with the group counters reused
+    monkeypatch.setenv("TCR_SPLIT", "4")
+    assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
+    assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
