@@ -259,9 +259,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         engine = TCR_ENGINE_MMA_SYNC_REGS;
     g_engine = engine;
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
-        uint64_t maxg = uint64_t(tcr::async_max_grid(c->R, p.debug_mode));
-        if (const char* e = std::getenv("TCR_CTAS_PER_SM"))  // profiling knob
-            maxg = std::min<uint64_t>(maxg, uint64_t(std::atoi(e)) * tcr::sm_count());
+        const uint64_t maxg = uint64_t(tcr::async_max_grid(c->R, p.debug_mode));
         const uint64_t groups = p.group_end - p.group_begin;
         p.split = tcr::async_split(g, groups, int(maxg));
         if (p.split > 1) {

@@ -63,8 +63,8 @@ struct SpParams {
     // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
     // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
     // K-major, 5 = as 3 with N = 64 (timing only; results are not meaningful in modes 1-5).
-    // cp.async engine: 8 = prefetch across a CTA's unit boundaries; 9 / 10 = ring depth 8 / 32
-    // for R = 1.  Results are identical to the default in modes 8-10.
+    // cp.async engine: 9 / 10 = ring depth 8 / 32 for R = 1, 11 = depth 12 / 10 for R = 3 / 5
+    // (results identical).
     int32_t debug_mode;
 };
 

@@ -151,12 +151,11 @@ __device__ __forceinline__ void as_unit(const SpParams& p, uint64_t c0, uint32_t
 
 // Static fast path: a unit entirely inside n, RT in 1..5 with 2*RT | D, and every warp's
 // fragment count a multiple of D.  Stage indices, chunk boundaries and finishing pairs are
-// compile-time.  prefetch_next (profiling mode 8): the last D-1 refills fetch the first D-1
-// fragments of the CTA's next unit (chunk cn), so the stream does not drain across the trees.
+// compile-time.  (Prefetching the next unit's first fragments across the trees was measured
+// slower, 6.20 vs 6.81 TB/s; so was a CTA barrier every ring turn.)
 template <int RT, int D>
 __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, uint32_t Cu, uint32_t ring_saddr,
-                                               float* s_chunk, bool& ovf, bool prologue, bool prefetch_next,
-                                               uint64_t cn) {
+                                               float* s_chunk, bool& ovf) {
     static_assert(D % (2 * RT) == 0, "static path needs 2*RT | depth");
     constexpr uint32_t CPI = D / RT;                 // chunks per outer iteration
     constexpr uint64_t CE = uint64_t(RT) * 256u;     // chunk elements
@@ -170,14 +169,11 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
     // global element offset of warp-local fragment g (chunk g/RT, fragment g%RT)
 #define TCR_FRAG_OFF(g) (uint64_t((g) / RT) * kAsWarps * CE + uint64_t((g) % RT) * 256u)
     constexpr uint64_t ITB = uint64_t(CPI) * kAsWarps * CE;     // elements per outer iteration
-    if (prologue) {
 #pragma unroll
-        for (int u = 0; u < D - 1; ++u) {
-            cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
-            cp_async_commit();
-        }
+    for (int u = 0; u < D - 1; ++u) {
+        cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
+        cp_async_commit();
     }
-    const uint16_t* gn = static_cast<const uint16_t*>(p.x) + (cn + warp) * CE + 8u * lane;
     float* out = s_chunk + warp;
     for (uint32_t it = 0; it < iters; ++it) {
         const uint16_t* gq = gp + uint64_t(it) * ITB;
@@ -188,8 +184,6 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
             // refill the stage consumed one step ago with fragment it*D + u + D-1
             if (it + 1 < iters || u == 0)
                 cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + TCR_FRAG_OFF(u + D - 1), 16u);
-            else if (prefetch_next)   // stage u-1 <- fragment u-1 of the next unit
-                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gn + TCR_FRAG_OFF(u - 1), 16u);
             cp_async_commit();
             cp_async_wait<D - 1>();
             __syncwarp();
@@ -219,16 +213,16 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
         }
     }
 #undef TCR_FRAG_OFF
-    if (!prefetch_next) cp_async_wait<0>();
+    cp_async_wait<0>();
 }
 
 // Ring depth per chain length: 2*R | D keeps every stage index and chunk pair compile-time.
 template <int RT> struct AsDepth { static constexpr int value = 8; };
 template <> struct AsDepth<1> { static constexpr int value = 16; };
 template <> struct AsDepth<2> { static constexpr int value = 16; };
-template <> struct AsDepth<3> { static constexpr int value = 12; };
+template <> struct AsDepth<3> { static constexpr int value = 24; };   // 12: -0..3 % (mode 11)
 template <> struct AsDepth<4> { static constexpr int value = 16; };
-template <> struct AsDepth<5> { static constexpr int value = 10; };
+template <> struct AsDepth<5> { static constexpr int value = 20; };   // 10: -3..5 % (mode 11)
 
 int as_depth(uint32_t R) {
     switch (R) {
@@ -254,7 +248,7 @@ constexpr uint32_t as_smem_bytes() {
 // Persistent CTAs over work units u = group_begin*S .. group_end*S (strided by the grid, so
 // concurrent CTAs read neighbouring units).  Per unit: stream -> chunk results -> block trees
 // (reduction.hpp:253) -> group tree, either in place (S = 1) or by the CTA that completes the
-// group (S > 1).  Warps 1-7 start the next unit while warp 0 runs the group tree.
+// group (S > 1).
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
     extern __shared__ __align__(128) unsigned char s_ring[];
@@ -270,24 +264,17 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     const uint64_t full_units = p.n / (uint64_t(Cu) * p.chunk_elems);
     bool static_ok = false;
     if constexpr (RT > 0) static_ok = static_unit(Cu, RT, D);
-    const bool pf = p.debug_mode == 8;
-    bool prefetched = false;   // this unit's first D-1 fragments are already in flight
     const uint64_t u_end = p.group_end * S;
     for (uint64_t u = p.group_begin * S + blockIdx.x; u < u_end; u += gridDim.x) {
         const uint64_t c0 = u * Cu;
+        bool done = false;
         if constexpr (RT > 0) {
             if (static_ok && u < full_units) {
-                const uint64_t un = u + gridDim.x;
-                const bool next_static = pf && un < u_end && un < full_units;
-                as_unit_static<RT, D>(p, c0, Cu, ring, s_chunk, ovf, !prefetched, next_static, un * Cu);
-                prefetched = next_static;
-            } else {
-                as_unit<RT, D>(p, c0, Cu, ring, s_chunk, ovf);
-                prefetched = false;
+                as_unit_static<RT, D>(p, c0, Cu, ring, s_chunk, ovf);
+                done = true;
             }
-        } else {
-            as_unit<RT, D>(p, c0, Cu, ring, s_chunk, ovf);
         }
+        if (!done) as_unit<RT, D>(p, c0, Cu, ring, s_chunk, ovf);
         __syncthreads();
         range_trees_blocks(p, u * Gu, Gu, s_chunk, s_block, warp, kAsWarps);
         __syncthreads();
@@ -306,8 +293,7 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
                 if (lane_id() == 0) p.group_count[gi] = 0u;
             }
         }
-        // no barrier here: the next unit's first writes to s_block / s_glast come after the
-        // barriers above, which warp 0 reaches only after its group tree
+        __syncthreads();
     }
     if (__any_sync(kFull, ovf) && lane_id() == 0) atomicOr(p.overflow, 1u);
     __threadfence();
@@ -326,6 +312,9 @@ AsPick pick(uint32_t R, int mode = 0) {
     // profiling modes 9 / 10: ring depth 8 / 32 for R = 1 (default 16)
     if (R == 1 && mode == 9) return {sp_async_kernel<1, 8>, as_smem_bytes<1, 8>()};
     if (R == 1 && mode == 10) return {sp_async_kernel<1, 32>, as_smem_bytes<1, 32>()};
+    // profiling mode 11: the shallower rings of the odd chain lengths
+    if (R == 3 && mode == 11) return {sp_async_kernel<3, 12>, as_smem_bytes<3, 12>()};
+    if (R == 5 && mode == 11) return {sp_async_kernel<5, 10>, as_smem_bytes<5, 10>()};
     switch (R) {
     case 1: return {sp_async_kernel<1>, as_smem_bytes<1>()};
     case 2: return {sp_async_kernel<2>, as_smem_bytes<2>()};
@@ -339,10 +328,13 @@ AsPick pick(uint32_t R, int mode = 0) {
 bool as_attr_once() {
     static bool done = false;
     if (!done) {
-        for (int mode : {0, 9, 10})
+        for (int mode : {0, 9, 10, 11})
         for (uint32_t R = 0; R <= 5; ++R) {
             const AsPick k = pick(R, mode);
-            if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(k.smem)) != cudaSuccess)
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, k.fn);
+            if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024 - int(fa.sharedSizeBytes)) != cudaSuccess)
                 return false;
         }
         done = true;
@@ -350,9 +342,10 @@ bool as_attr_once() {
     return true;
 }
 
-// Measured per-unit cost (drain + trees + prologue) in element-equivalents: 2^16- vs 2^18-element
-// groups at n = 2^30 (6.42 vs 6.82 TB/s) put it near 5.5 K elements; rounded up.
-constexpr double kUnitOverheadElems = 8192.0;
+// Work units per CTA below which the grid's tail (the last CTAs still streaming) starves HBM:
+// measured at n = 2^28 (R = 3: 2.3 groups per CTA, 5.22 -> 5.66 TB/s with S = 2; R = 1: 3.5
+// groups per CTA, S = 2 neutral) and n = 2^30 (>= 9 groups per CTA: splitting costs 1-3 %).
+constexpr double kMinUnitsPerCta = 3.0;
 
 }  // namespace
 
@@ -367,34 +360,50 @@ uint32_t async_split(const SpGeometry& g, uint64_t groups, int grid) {
     }
     const int D = as_depth(g.R);
     const bool st1 = static_unit(Cg, g.R, D);
-    uint32_t best = 1;
-    double best_t = 0.0;
-    for (uint32_t S = 1; S <= g.G && S <= 64; S *= 2) {
-        if (S > 1 && st1 && !static_unit(Cg / S, g.R, D)) break;   // never leave the static path
-        const uint64_t U = groups * S;
-        const uint64_t per = (U + uint64_t(grid) - 1) / uint64_t(grid);
-        const double t = double(per) * (double(g.group_elems) / S + kUnitOverheadElems);
-        if (S == 1 || t < 0.98 * best_t) {
-            best = S;
-            best_t = t;
-        }
-    }
-    return best;
+    uint32_t S = 1;
+    while (double(groups) * S < kMinUnitsPerCta * grid && S * 2 <= g.G && S < 64 &&
+           (!st1 || static_unit(Cg / (S * 2), g.R, D)))   // never leave the static path
+        S *= 2;
+    return S;
+}
+
+// CTAs per SM: two 64 KiB rings per SM measured best (n = 2^30, R = 1: 2/SM 312.8 us, 3/SM
+// 332.5 us, 1/SM 540 us); the launch pads dynamic shared memory so that no SM takes a third
+// CTA.  Env TCR_CTAS_PER_SM overrides (profiling).
+int as_ctas_per_sm() {
+    int cps = 2;
+    if (const char* e = std::getenv("TCR_CTAS_PER_SM")) cps = std::max(1, std::atoi(e));
+    return cps;
+}
+
+uint32_t as_launch_smem(const AsPick& k, int cps) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k.fn);
+    int dev = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    // the largest footprint that still lets cps CTAs (each with 1 KiB reserved) share the SM
+    const long fit = long(per_sm) / cps - 1024 - long(fa.sharedSizeBytes);
+    const long cap = 227 * 1024 - long(fa.sharedSizeBytes);
+    long want = std::min(fit, cap);
+    want -= want % 128;
+    return uint32_t(std::max<long>(long(k.smem), want));
 }
 
 int async_max_grid(uint32_t R, int mode) {
     as_attr_once();
     const AsPick k = pick(R, mode);
+    const int cps = as_ctas_per_sm();
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kAsThreads, k.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kAsThreads, as_launch_smem(k, cps));
     if (per_sm < 1) per_sm = 1;
-    return per_sm * sm_count();
+    return std::min(per_sm, cps) * sm_count();
 }
 
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s) {
     if (!as_attr_once()) return cudaErrorInvalidValue;
     const AsPick k = pick(p.R, p.debug_mode);
-    k.fn<<<grid, kAsThreads, k.smem, s>>>(p);
+    k.fn<<<grid, kAsThreads, as_launch_smem(k, as_ctas_per_sm()), s>>>(p);
     return cudaGetLastError();
 }
 

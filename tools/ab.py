@@ -4,6 +4,7 @@
     python tools/ab.py [--n 1073741824] [--rounds 7] [--reps 10] SPEC [SPEC ...]
 
 SPEC = label:engine:R:B[:ENV=VAL,...]  e.g.  async:4:1:1024  tc05:2:1:1024:TCR_DEBUG_MODE=3
+(LIB=path in the ENV list times another build of libtcreduce_b200.so, e.g. a previous commit's)
 Rounds alternate between the specs so clock / thermal drift hits all of them alike; the
 median over rounds of the per-round mean kernel time is reported (CUDA events on the
 launch stream, inputs 2 GiB > L2).
@@ -17,6 +18,22 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+
+def _load_other(path):
+    import shutil
+    import tempfile
+    from paper_2001_05585_b200 import _capi
+    # a distinct file name so the dynamic loader does not hand back the in-tree library
+    tmp = os.path.join(tempfile.mkdtemp(), "libtcr_ab_%d.so" % abs(hash(path)))
+    shutil.copy(path, tmp)
+    lib = C.CDLL(tmp)
+    for name, (res, args) in _capi.SIGNATURES.items():
+        if hasattr(lib, name):
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return lib
 
 
 def main():
@@ -43,11 +60,12 @@ def main():
         parts = s.split(":")
         env = dict(kv.split("=") for kv in parts[4].split(",")) if len(parts) > 4 and parts[4] else {}
         cfg = T.ReductionConfig(m=16, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])))
-        specs.append((parts[0], cfg.to_c(), env))
+        lib_path = env.pop("LIB", None)
+        specs.append((parts[0], cfg.to_c(), env, _capi.load() if lib_path is None else _load_other(lib_path)))
     times = {s[0]: [] for s in specs}
     vals = {}
     for rnd in range(a.rounds):
-        for label, c, env in specs:
+        for label, c, env, lib in specs:
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
             try:
@@ -68,7 +86,7 @@ def main():
                     else:
                         os.environ[k] = v
     out = {}
-    for label, _, _ in specs:
+    for label, _, _, _ in specs:
         ms = statistics.median(times[label])
         out[label] = {"ms_median": ms, "ms_min": min(times[label]), "gelem_s": a.n / ms / 1e6,
                       "tb_s": 2 * a.n / ms / 1e9, "value": vals[label]}
