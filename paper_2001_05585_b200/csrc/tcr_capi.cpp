@@ -72,6 +72,8 @@ struct Workspace {
     size_t bs_cap = 0;
     uint32_t* group_count = nullptr;  // kept zero between launches
     size_t gc_cap = 0;
+    unsigned long long* work_counter = nullptr;  // kept zero between launches
+    size_t wc_cap = 0;
     float* stage = nullptr;  // host path of the non-single_pass variants
     size_t stage_cap = 0;
     // pipelined host path
@@ -260,9 +262,8 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     g_engine = engine;
     if (engine == TCR_ENGINE_MMA_SYNC_ASYNC) {
         const uint64_t maxg = uint64_t(tcr::async_max_grid(c->R, p.debug_mode));
-        const uint64_t groups = p.group_end - p.group_begin;
-        p.split = tcr::async_split(g, groups, int(maxg));
-        if (p.split > 1) {
+        const bool dyn = tcr::async_plan(g, &p, int(maxg));
+        if (p.split > 1 || p.split_tail > 1) {
             rc = ensure(&w->block_scratch, &w->bs_cap, g.n_groups * g.G, s);
             if (rc) return rc;
             rc = ensure_zero(&w->group_count, &w->gc_cap, g.n_groups, s);
@@ -270,7 +271,13 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
             p.block_scratch = w->block_scratch;
             p.group_count = w->group_count;
         }
-        const int grid = int(std::min<uint64_t>(groups * p.split, maxg));
+        if (dyn) {
+            rc = ensure_zero(&w->work_counter, &w->wc_cap, 1, s);
+            if (rc) return rc;
+            p.work_counter = w->work_counter;
+        }
+        const uint64_t units = (p.tail_group - p.group_begin) * p.split + (p.group_end - p.tail_group) * p.split_tail;
+        const int grid = int(std::min<uint64_t>(units, maxg));
         TCR_CUDA(tcr::launch_async(p, grid, s));
         ++g_launches;
         return TCR_OK;

@@ -51,14 +51,18 @@ struct SpParams {
     int32_t finalize;
     int32_t atomic_order;
     uint64_t atomic_seed;
-    // Work units of the cp.async engine: every group is split into `split` (power of two, divides
-    // G) pieces of G/split whole blocks so that the unit count balances over the grid.  With
-    // split > 1 the piece's block results go to block_scratch[n_groups*G] and the CTA completing
-    // a group (group_count[n_groups], zero on entry and on exit) runs its group tree.  The tree
-    // -- and so the TREE result -- is the same for every split.
-    uint32_t split;
+    // Work units of the cp.async engine.  Groups [group_begin, tail_group) are split into
+    // `split` pieces of G/split whole blocks, the tail groups [tail_group, group_end) into
+    // `split_tail` pieces (small units at the end balance the grid).  Pieces of one group put
+    // their block results in block_scratch[n_groups*G] and the CTA completing the group
+    // (group_count[n_groups], zero on entry and exit) runs its group tree: the tree -- and so
+    // the TREE result -- does not depend on the split.  work_counter (zero on entry and exit)
+    // hands units out dynamically; null = grid-stride order.
+    uint32_t split, split_tail;
+    uint64_t tail_group;
     float* block_scratch;
     uint32_t* group_count;
+    unsigned long long* work_counter;
     // Profiling hook (env TCR_DEBUG_MODE, never set in production): tcgen05 engine only --
     // 1 = TMA stream only (no MMA / epilogue), 2 = 1-D bulk copies instead of the tensor map,
     // 3 = TMA + MMA without the epilogue (accumulators overwritten unread), 4 = as 3 with A read
@@ -86,9 +90,10 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
 // group range including the ragged tail (zero-fill copies).  binary16 input.
 int async_max_grid(uint32_t R, int debug_mode = 0);
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
-// Pieces per group for the cp.async engine over `groups` groups on `grid` CTAs (cost model:
-// ceil(units / grid) x (unit elements + per-unit overhead)); env TCR_SPLIT overrides.
-uint32_t async_split(const SpGeometry& g, uint64_t groups, int grid);
+// Work-unit plan of the cp.async engine over groups [p.group_begin, p.group_end) on `grid`
+// CTAs: sets split, split_tail, tail_group; returns whether units are handed out dynamically.
+// Env TCR_SPLIT / TCR_TAIL_SPLIT / TCR_SCHED override (profiling).
+bool async_plan(const SpGeometry& g, SpParams* p, int grid);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.
 bool genm_supported(const SpGeometry& g);

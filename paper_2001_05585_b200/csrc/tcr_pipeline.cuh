@@ -96,11 +96,22 @@ __device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, flo
     if (threadIdx.x < nthr && lo < P) {
         float stk[40];
         int top = 0;
-        for (uint64_t i = 0; i < seg; ++i) {
-            const uint64_t idx = lo + i;
-            float v = idx < count ? __ldcg(vals + idx) : 0.0f;
-            for (uint64_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
-            stk[top++] = v;
+        // batches of 8 independent L2 loads in flight, then the same streaming stack order
+        for (uint64_t i0 = 0; i0 < seg; i0 += 8) {
+            float v8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t idx = lo + i0 + k;
+                v8[k] = (i0 + k < seg && idx < count) ? __ldcg(vals + idx) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (i0 + k < seg) {
+                    float v = v8[k];
+                    for (uint64_t b = i0 + k; b & 1; b >>= 1) v = stk[--top] + v;
+                    stk[top++] = v;
+                }
+            }
         }
         acc = stk[0];
     }

@@ -149,10 +149,16 @@ __device__ __forceinline__ void as_unit(const SpParams& p, uint64_t c0, uint32_t
 }
 
 
-// Static fast path: a unit entirely inside n, RT in 1..5 with 2*RT | D, and every warp's
-// fragment count a multiple of D.  Stage indices, chunk boundaries and finishing pairs are
-// compile-time.  (Prefetching the next unit's first fragments across the trees was measured
-// slower, 6.20 vs 6.81 TB/s; so was a CTA barrier every ring turn.)
+// Static fast path: a unit entirely inside n, RT in 1..5 with 2*RT | D, every warp's fragment
+// count a multiple of D and its chunk count a multiple of 8.  Stage indices and chunk
+// boundaries are compile-time.
+//
+// Column-sum form: with A = ones (16x16) and B = M split into its column halves, the two
+// HMMA.16816 give every lane (g, c) C[2c], C[2c+1] and C[2c+8], C[2c+9] -- exactly the B
+// fragment of column g of the finishing MMA.  The same k positions are summed as in the
+// M^T x ones form of as_unit (bit-identical results), but no shuffles are needed: lane group g
+// keeps chunk (8i + g)'s binary16 partials and ONE finishing HMMA (A = ones) per 8 chunks
+// returns their 8 results (lane c: chunks 2c, 2c+1).
 template <int RT, int D>
 __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, uint32_t Cu, uint32_t ring_saddr,
                                                float* s_chunk, bool& ovf) {
@@ -160,14 +166,14 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
     constexpr uint32_t CPI = D / RT;                 // chunks per outer iteration
     constexpr uint64_t CE = uint64_t(RT) * 256u;     // chunk elements
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-    const unsigned c = lane & 3u;
+    const unsigned g = lane >> 2, c = lane & 3u;
     const uint32_t iters = Cu / kAsWarps / CPI;
     const uint16_t* gp = static_cast<const uint16_t*>(p.x) + (c0 + warp) * CE + 8u * lane;
     const uint32_t cp_dst = ring_saddr + swz(lane >> 1, lane & 1u);
     const uint32_t mi = lane >> 3;
     const uint32_t ld_base = ring_saddr + swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
-    // global element offset of warp-local fragment g (chunk g/RT, fragment g%RT)
-#define TCR_FRAG_OFF(g) (uint64_t((g) / RT) * kAsWarps * CE + uint64_t((g) % RT) * 256u)
+    // global element offset of warp-local fragment f (chunk f/RT, fragment f%RT)
+#define TCR_FRAG_OFF(f) (uint64_t((f) / RT) * kAsWarps * CE + uint64_t((f) % RT) * 256u)
     constexpr uint64_t ITB = uint64_t(CPI) * kAsWarps * CE;     // elements per outer iteration
 #pragma unroll
     for (int u = 0; u < D - 1; ++u) {
@@ -175,10 +181,10 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
         cp_async_commit();
     }
     float* out = s_chunk + warp;
+    uint32_t bb0 = 0, bb1 = 0;   // finishing-MMA B fragment: column g = chunk 8i + g
     for (uint32_t it = 0; it < iters; ++it) {
         const uint16_t* gq = gp + uint64_t(it) * ITB;
-        uint32_t a01p = 0, a23p = 0;
-        float acc[4];
+        float lo[4], hi[4];
 #pragma unroll
         for (int u = 0; u < D; ++u) {
             // refill the stage consumed one step ago with fragment it*D + u + D-1
@@ -189,24 +195,27 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
             __syncwarp();
             uint32_t d0, d1, d2, d3;
             ldsm_x4_trans(ld_base + u * kAsStageBytes, d0, d1, d2, d3);
-            if (u % RT == 0) acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-            mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
+            if (u % RT == 0) lo[0] = lo[1] = lo[2] = lo[3] = hi[0] = hi[1] = hi[2] = hi[3] = 0.f;
+            // C_r = ones x M_r + C_{r-1} (reduction.hpp:177): columns 0-7 and 8-15
+            mma_16816(lo, kOnesF16x2, kOnesF16x2, kOnesF16x2, kOnesF16x2, d0, d2);
+            mma_16816(hi, kOnesF16x2, kOnesF16x2, kOnesF16x2, kOnesF16x2, d1, d3);
             if (u % RT == RT - 1) {
-                const uint32_t pk = uint32_t(f32_to_h(acc[0])) | (uint32_t(f32_to_h(acc[2])) << 16);
-                const uint32_t vA = __shfl_sync(kFull, pk, 8 * c);
-                const uint32_t vB = __shfl_sync(kFull, pk, 8 * c + 4);
-                const uint32_t a01 = prmt(vA, vB, 0x5410), a23 = prmt(vA, vB, 0x7632);
-                if ((u / RT) % 2 == 0) {
-                    a01p = a01;
-                    a23p = a23;
-                } else {
+                const uint32_t ci = it * CPI + u / RT;          // warp-local chunk
+                const uint32_t k = ci & 7u;
+                // C_R -> binary16 (:179-181), kept by the lanes of group g = k
+                const uint32_t b0 = pack_h2(lo[0], lo[1]), b1 = pack_h2(hi[0], hi[1]);
+                if (g == k) {
+                    bb0 = b0;
+                    bb1 = b1;
+                }
+                if (k == 7) {
+                    // finishing MMA (:182) for chunks ci-7 .. ci
                     float fin[4] = {0.f, 0.f, 0.f, 0.f};
-                    mma_16816(fin, a01p, a01, a23p, a23, kOnesF16x2, kOnesF16x2);
-                    ovf |= !isfinite(fin[0]) || !isfinite(fin[2]);
-                    if (lane == 0) {
-                        const uint32_t ci = it * CPI + u / RT;     // odd chunk of the pair
-                        out[(ci - 1) * kAsWarps] = fin[0];
-                        out[ci * kAsWarps] = fin[2];
+                    mma_16816(fin, kOnesF16x2, kOnesF16x2, kOnesF16x2, kOnesF16x2, bb0, bb1);
+                    ovf |= !isfinite(fin[0]) || !isfinite(fin[1]);
+                    if (g == 0) {
+                        out[(ci - 7 + 2 * c) * kAsWarps] = fin[0];
+                        out[(ci - 6 + 2 * c) * kAsWarps] = fin[1];
                     }
                 }
             }
@@ -236,7 +245,7 @@ int as_depth(uint32_t R) {
 }
 
 __host__ __device__ inline bool static_unit(uint32_t Cu, uint32_t R, int D) {
-    return R >= 1 && R <= 5 && Cu % kAsWarps == 0 && (Cu / kAsWarps) * R >= uint32_t(D) &&
+    return R >= 1 && R <= 5 && Cu % (8 * kAsWarps) == 0 && (Cu / kAsWarps) * R >= uint32_t(D) &&
            ((Cu / kAsWarps) * R) % uint32_t(D) == 0;
 }
 
@@ -256,33 +265,61 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     __shared__ float s_block[kMaxChunksPerGroup];
     __shared__ float s_scratch[32];
     __shared__ int s_last, s_glast;
+    __shared__ unsigned long long s_next;
     const unsigned warp = threadIdx.x >> 5;
     const uint32_t ring = smem_u32(s_ring) + warp * D * kAsStageBytes;
     bool ovf = false;
-    const uint32_t S = p.split, G = p.G;
-    const uint32_t Cu = G * p.W / S, Gu = G / S;
-    const uint64_t full_units = p.n / (uint64_t(Cu) * p.chunk_elems);
-    bool static_ok = false;
-    if constexpr (RT > 0) static_ok = static_unit(Cu, RT, D);
-    const uint64_t u_end = p.group_end * S;
-    for (uint64_t u = p.group_begin * S + blockIdx.x; u < u_end; u += gridDim.x) {
-        const uint64_t c0 = u * Cu;
+    const uint32_t G = p.G, Cg = G * p.W;
+    // unit space: groups [group_begin, tail_group) in `split` pieces, then the tail groups
+    // [tail_group, group_end) in `split_tail` smaller pieces
+    const uint64_t u_main = (p.tail_group - p.group_begin) * p.split;
+    const uint64_t u_total = u_main + (p.group_end - p.tail_group) * p.split_tail;
+    const bool dyn = p.work_counter != nullptr;
+    uint64_t u;
+    if (dyn) {
+        if (threadIdx.x == 0) s_next = atomicAdd(p.work_counter, 1ull);
+        __syncthreads();
+        u = s_next;
+    } else {
+        u = blockIdx.x;
+    }
+    while (u < u_total) {
+        // thread 0 claims the next unit now; the atomic's latency hides behind this unit's stream
+        unsigned long long nxt = u + gridDim.x;
+        if (dyn && threadIdx.x == 0) nxt = atomicAdd(p.work_counter, 1ull);
+        uint64_t gi;
+        uint32_t S, piece;
+        if (u < u_main) {
+            S = p.split;
+            gi = p.group_begin + u / S;
+            piece = uint32_t(u % S);
+        } else {
+            S = p.split_tail;
+            gi = p.tail_group + (u - u_main) / S;
+            piece = uint32_t((u - u_main) % S);
+        }
+        const uint32_t Cu = Cg / S, Gu = G / S;
+        const uint64_t c0 = gi * Cg + uint64_t(piece) * Cu;
+        const uint64_t b0 = gi * G + uint64_t(piece) * Gu;
         bool done = false;
         if constexpr (RT > 0) {
-            if (static_ok && u < full_units) {
+            if (static_unit(Cu, RT, D) && (c0 + Cu) * p.chunk_elems <= p.n) {
                 as_unit_static<RT, D>(p, c0, Cu, ring, s_chunk, ovf);
                 done = true;
             }
         }
         if (!done) as_unit<RT, D>(p, c0, Cu, ring, s_chunk, ovf);
         __syncthreads();
-        range_trees_blocks(p, u * Gu, Gu, s_chunk, s_block, warp, kAsWarps);
+        if (dyn && threadIdx.x == 0) {
+            s_next = nxt;
+            if (nxt == u_total + gridDim.x - 1) *p.work_counter = 0ull;   // the last claim: reset
+        }
+        range_trees_blocks(p, b0, Gu, s_chunk, s_block, warp, kAsWarps);
         __syncthreads();
-        const uint64_t gi = u / S;
         if (S == 1) {
             if (warp == 0) tile_tree_group(p, gi, s_block);
         } else {
-            for (uint32_t b = threadIdx.x; b < Gu; b += kAsThreads) p.block_scratch[u * Gu + b] = s_block[b];
+            for (uint32_t b = threadIdx.x; b < Gu; b += kAsThreads) p.block_scratch[b0 + b] = s_block[b];
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) s_glast = atomicAdd(p.group_count + gi, 1u) == S - 1;
@@ -294,6 +331,7 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
             }
         }
         __syncthreads();
+        u = dyn ? s_next : nxt;
     }
     if (__any_sync(kFull, ovf) && lane_id() == 0) atomicOr(p.overflow, 1u);
     __threadfence();
@@ -346,25 +384,49 @@ bool as_attr_once() {
 // measured at n = 2^28 (R = 3: 2.3 groups per CTA, 5.22 -> 5.66 TB/s with S = 2; R = 1: 3.5
 // groups per CTA, S = 2 neutral) and n = 2^30 (>= 9 groups per CTA: splitting costs 1-3 %).
 constexpr double kMinUnitsPerCta = 3.0;
+// The last kTailUnitsPerCta x grid units are pieces of 1/kTailSplit group, handed out
+// dynamically (first come, first served), so the grid finishes within a small piece.
+constexpr uint32_t kTailSplit = 4;   // measured: 8 costs 1-4 % (small pieces drain), 2 gains less
+constexpr uint32_t kTailUnitsPerCta = 2;
+constexpr bool kDynamicSchedule = true;
 
 }  // namespace
 
-uint32_t async_split(const SpGeometry& g, uint64_t groups, int grid) {
-    if (groups == 0 || grid < 1) return 1;
+bool async_plan(const SpGeometry& g, SpParams* p, int grid) {
+    const uint64_t groups = p->group_end - p->group_begin;
+    p->split = p->split_tail = 1;
+    p->tail_group = p->group_end;
+    if (groups == 0 || grid < 1) return false;
     const uint32_t Cg = g.G * g.W;
-    if (const char* e = std::getenv("TCR_SPLIT")) {   // profiling knob
-        uint32_t S = 1;
-        const uint32_t want = uint32_t(std::strtoul(e, nullptr, 10));
-        while (S * 2 <= want && S * 2 <= g.G) S *= 2;
-        return S;
-    }
     const int D = as_depth(g.R);
     const bool st1 = static_unit(Cg, g.R, D);
+    auto ok = [&](uint32_t S) {   // S pieces of whole blocks that keep the static path
+        return S <= g.G && S <= 64 && (!st1 || static_unit(Cg / S, g.R, D));
+    };
+    auto env_pow2 = [&](const char* name, uint32_t dflt) {
+        const char* e = std::getenv(name);
+        if (!e) return dflt;
+        const uint32_t want = uint32_t(std::strtoul(e, nullptr, 10));
+        uint32_t S = 1;
+        while (S * 2 <= want && S * 2 <= g.G) S *= 2;
+        return S;
+    };
     uint32_t S = 1;
-    while (double(groups) * S < kMinUnitsPerCta * grid && S * 2 <= g.G && S < 64 &&
-           (!st1 || static_unit(Cg / (S * 2), g.R, D)))   // never leave the static path
-        S *= 2;
-    return S;
+    while (double(groups) * S < kMinUnitsPerCta * grid && ok(S * 2)) S *= 2;
+    S = env_pow2("TCR_SPLIT", S);
+    uint32_t St = S;
+    while (St < kTailSplit && ok(St * 2)) St *= 2;
+    St = std::max(S, env_pow2("TCR_TAIL_SPLIT", St));
+    p->split = S;
+    p->split_tail = St;
+    if (St > S) {
+        const uint64_t tail = std::min<uint64_t>(groups, (uint64_t(kTailUnitsPerCta) * grid + St - 1) / St);
+        p->tail_group = p->group_end - tail;
+        if (p->tail_group == p->group_begin) p->split = St;
+    }
+    bool dyn = kDynamicSchedule;
+    if (const char* e = std::getenv("TCR_SCHED")) dyn = std::atoi(e) != 0;
+    return dyn;
 }
 
 // CTAs per SM: two 64 KiB rings per SM measured best (n = 2^30, R = 1: 2/SM 312.8 us, 3/SM

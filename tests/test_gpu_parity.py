@@ -526,19 +526,23 @@ def test_sharded_c_abi_single_gpu(oracle):
 
 @pytest.mark.parametrize("R,B", [(1, 1024), (3, 256), (4, 128), (5, 32), (6, 64)])
 def test_split_units_identical(oracle, R, B, monkeypatch):
-    """The cp.async engine splits groups into pieces for grid balance (TCR_SPLIT forces the
-    piece count): values, block results and overflow are identical for every split."""
+    """The cp.async engine splits groups into pieces for grid balance and hands units out
+    dynamically (TCR_SPLIT / TCR_TAIL_SPLIT / TCR_SCHED force the plan): values and block
+    results are identical for every plan."""
     cfg = cfg16(R=R, B=B, engine=T.Engine.mma_sync_async)
     from paper_2001_05585_b200 import sharded as S
     n = 37 * S.group_elems(cfg) + 4097
     h = oracle.generate_f16("normal", 9, n)
     xd = to_dev_f16(h)
     base = {}
-    for split in ("1", "2", "4", "8", "64"):
+    for split, tail, sched in (("1", "1", "0"), ("1", "1", "1"), ("2", "2", "0"), ("4", "8", "1"), ("1", "8", "0"),
+                               ("8", "64", "1"), ("64", "64", "0")):
         monkeypatch.setenv("TCR_SPLIT", split)
+        monkeypatch.setenv("TCR_TAIL_SPLIT", tail)
+        monkeypatch.setenv("TCR_SCHED", sched)
         for fin in (T.Finalize.tree, T.Finalize.ordered):
             o = T.reduce(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync_async, finalize=fin))
-            assert base.setdefault(fin, o.value) == o.value, (split, fin)
+            assert base.setdefault(fin, o.value) == o.value, (split, tail, sched, fin)
         blocks = T.block_results(xd, cfg).cpu().numpy()
         if "blocks" in base:
             assert np.array_equal(blocks.view(np.uint32), base["blocks"].view(np.uint32))
