@@ -16,6 +16,8 @@
 // 16-byte line is XOR-swizzled on row bit 2 so the transposing ldmatrix is bank-conflict free.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "tcr_device.cuh"
@@ -429,6 +431,8 @@ bool async_plan(const SpGeometry& g, SpParams* p, int grid) {
     return dyn;
 }
 
+namespace {
+
 // CTAs per SM: two 64 KiB rings per SM measured best (n = 2^30, R = 1: 2/SM 312.8 us, 3/SM
 // 332.5 us, 1/SM 540 us); the launch pads dynamic shared memory so that no SM takes a third
 // CTA.  Env TCR_CTAS_PER_SM overrides (profiling).
@@ -438,7 +442,7 @@ int as_ctas_per_sm() {
     return cps;
 }
 
-uint32_t as_launch_smem(const AsPick& k, int cps) {
+uint32_t as_launch_smem_uncached(const AsPick& k, int cps) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, k.fn);
     int dev = 0, per_sm = 0;
@@ -452,20 +456,41 @@ uint32_t as_launch_smem(const AsPick& k, int cps) {
     return uint32_t(std::max<long>(long(k.smem), want));
 }
 
+// (kernel, CTAs per SM) -> launch smem and resident CTAs per SM, queried once (the runtime
+// queries cost microseconds of host time per call otherwise)
+struct AsLaunch {
+    AsKernel fn;
+    int cps;
+    uint32_t smem;
+    int per_sm;
+};
+
+AsLaunch as_launch(const AsPick& k, int cps) {
+    static std::mutex mu;
+    static std::vector<AsLaunch> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const AsLaunch& a : cache)
+        if (a.fn == k.fn && a.cps == cps) return a;
+    AsLaunch a{k.fn, cps, as_launch_smem_uncached(k, cps), 0};
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.per_sm, k.fn, kAsThreads, a.smem);
+    if (a.per_sm < 1) a.per_sm = 1;
+    cache.push_back(a);
+    return a;
+}
+
+}  // namespace
+
 int async_max_grid(uint32_t R, int mode) {
     as_attr_once();
-    const AsPick k = pick(R, mode);
     const int cps = as_ctas_per_sm();
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kAsThreads, as_launch_smem(k, cps));
-    if (per_sm < 1) per_sm = 1;
-    return std::min(per_sm, cps) * sm_count();
+    const AsLaunch a = as_launch(pick(R, mode), cps);
+    return std::min(a.per_sm, cps) * sm_count();
 }
 
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s) {
     if (!as_attr_once()) return cudaErrorInvalidValue;
     const AsPick k = pick(p.R, p.debug_mode);
-    k.fn<<<grid, kAsThreads, as_launch_smem(k, as_ctas_per_sm()), s>>>(p);
+    k.fn<<<grid, kAsThreads, as_launch(k, as_ctas_per_sm()).smem, s>>>(p);
     return cudaGetLastError();
 }
 
