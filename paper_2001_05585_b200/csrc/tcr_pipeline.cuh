@@ -174,10 +174,56 @@ __device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_sc
 // Block stage (reference pairwise tree over W chunk results, reduction.hpp:253, :90-101) for the
 // nblk logical blocks starting at global block block0, by `nwarps` warps (w = caller's index in
 // that set): chunk results chunks[b*W + j] -> blocks[b].
+//   W <= 8: one block per LANE (the tree in registers, v[i] += v[i + len/2] over pow2(W));
+//   W > 8:  one block per warp (shfl_down offsets pow2(W)/2 .. 1 pair the same operands).
+__device__ __forceinline__ void publish_block(const SpParams& p, uint64_t gb, float x) {
+    if (gb < p.n_blocks) {
+        if (p.block_partials) p.block_partials[gb] = x;
+        if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
+    }
+}
+
+template <int PW>   // pow2(W) <= 8
+__device__ __forceinline__ float lane_block_tree(const float* chunks, uint32_t W, uint32_t b) {
+    float v[PW];
+    const float* src = chunks + b * W;
+    if (W == uint32_t(PW) && PW == 8) {
+        const float4 a = reinterpret_cast<const float4*>(src)[0], c = reinterpret_cast<const float4*>(src)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4 % PW] = c.x; v[5 % PW] = c.y; v[6 % PW] = c.z; v[7 % PW] = c.w;
+    } else if (W == uint32_t(PW) && PW == 4) {
+        const float4 a = reinterpret_cast<const float4*>(src)[0];
+        v[0] = a.x; v[1 % PW] = a.y; v[2 % PW] = a.z; v[3 % PW] = a.w;
+    } else if (W == uint32_t(PW) && PW == 2) {
+        const float2 a = reinterpret_cast<const float2*>(src)[0];
+        v[0] = a.x; v[1 % PW] = a.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < PW; ++j) v[j] = uint32_t(j) < W ? src[j] : 0.0f;
+    }
+#pragma unroll
+    for (int len = PW; len > 1; len >>= 1)
+#pragma unroll
+        for (int i = 0; i < len / 2; ++i) v[i] += v[i + len / 2];
+    return v[0];
+}
+
 __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t block0, uint32_t nblk,
                                                    const float* chunks, float* blocks, uint32_t w, uint32_t nwarps) {
     const uint32_t W = p.W;
     const unsigned lane = lane_id();
+    if (W <= 8) {
+        for (uint32_t b = w * 32u + lane; b < nblk; b += nwarps * 32u) {
+            float x;
+            if (W == 1) x = chunks[b];
+            else if (W == 2) x = lane_block_tree<2>(chunks, W, b);
+            else if (W <= 4) x = lane_block_tree<4>(chunks, W, b);
+            else x = lane_block_tree<8>(chunks, W, b);
+            blocks[b] = x;
+            publish_block(p, block0 + b, x);
+        }
+        return;
+    }
     uint32_t P = 1;
     while (P < W) P <<= 1;
     for (uint32_t b = w; b < nblk; b += nwarps) {
@@ -185,11 +231,7 @@ __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t b
         for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);
         if (lane == 0) {
             blocks[b] = x;
-            const uint64_t gb = block0 + b;
-            if (gb < p.n_blocks) {
-                if (p.block_partials) p.block_partials[gb] = x;
-                if (p.finalize == kFinAtomic) atomicAdd(p.result, x);
-            }
+            publish_block(p, block0 + b, x);
         }
     }
 }

@@ -307,8 +307,8 @@ __device__ __forceinline__ void sp16_group_fast(const SpParams& p, uint64_t gi, 
 
 template <bool F32IN, int RT>
 __global__ void __launch_bounds__(kSpThreads, 3) sp16_kernel(const SpParams p) {
-    __shared__ float s_chunk[kMaxChunksPerGroup];
-    __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ __align__(16) float s_chunk[kMaxChunksPerGroup];
+    __shared__ __align__(16) float s_block[kMaxChunksPerGroup];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
 
@@ -329,20 +329,7 @@ __global__ void __launch_bounds__(kSpThreads, 3) sp16_kernel(const SpParams p) {
         __syncthreads();
 
         // ---- block stage: reference pairwise tree over the W warp results (:253, :90-101)
-        uint32_t P = 1;
-        while (P < W) P <<= 1;
-        for (uint32_t b = warp; b < G; b += kSpWarps) {
-            float v = lane < W ? s_chunk[b * W + lane] : 0.0f;
-            for (uint32_t off = P >> 1; off >= 1; off >>= 1) v += __shfl_down_sync(kFull, v, off);
-            if (lane == 0) {
-                s_block[b] = v;
-                const uint64_t gb = gi * G + b;
-                if (gb < p.n_blocks) {
-                    if (p.block_partials) p.block_partials[gb] = v;
-                    if (p.finalize == kFinAtomic) atomicAdd(p.result, v);
-                }
-            }
-        }
+        pipe::tile_trees_blocks(p, gi, s_chunk, s_block, warp, kSpWarps);
         __syncthreads();
 
         // ---- group stage: adjacent tree over the G block results (power of two, any G)

@@ -263,8 +263,8 @@ constexpr uint32_t as_smem_bytes() {
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
     extern __shared__ __align__(128) unsigned char s_ring[];
-    __shared__ float s_chunk[kMaxChunksPerGroup];
-    __shared__ float s_block[kMaxChunksPerGroup];
+    __shared__ __align__(16) float s_chunk[kMaxChunksPerGroup];
+    __shared__ __align__(16) float s_block[kMaxChunksPerGroup];
     __shared__ float s_scratch[32];
     __shared__ int s_last, s_glast;
     __shared__ unsigned long long s_next;
