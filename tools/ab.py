@@ -4,7 +4,8 @@
     python tools/ab.py [--n 1073741824] [--rounds 7] [--reps 10] SPEC [SPEC ...]
 
 SPEC = label:engine:R:B[:ENV=VAL,...]  e.g.  async:4:1:1024  tc05:2:1:1024:TCR_DEBUG_MODE=3
-(LIB=path in the ENV list times another build of libtcreduce_b200.so, e.g. a previous commit's)
+(LIB=path in the ENV list times another build of libtcreduce_b200.so, e.g. a previous commit's;
+M=m sets the fragment side, default 16)
 Rounds alternate between the specs so clock / thermal drift hits all of them alike; the
 median over rounds of the per-round mean kernel time is reported (CUDA events on the
 launch stream, inputs 2 GiB > L2).
@@ -59,8 +60,9 @@ def main():
     for s in a.specs:
         parts = s.split(":")
         env = dict(kv.split("=") for kv in parts[4].split(",")) if len(parts) > 4 and parts[4] else {}
-        cfg = T.ReductionConfig(m=16, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])))
         lib_path = env.pop("LIB", None)
+        m = int(env.pop("M", 16))
+        cfg = T.ReductionConfig(m=m, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])))
         specs.append((parts[0], cfg.to_c(), env, _capi.load() if lib_path is None else _load_other(lib_path)))
     times = {s[0]: [] for s in specs}
     vals = {}
