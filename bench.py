@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT, help="elements per GPU")
+    ap.add_argument("--m", type=int, default=16, help="fragment side (16 = the hardware fragment)")
     ap.add_argument("--R", type=int, default=1)
     ap.add_argument("--B", type=int, default=1024)
     ap.add_argument("--engine", type=int, default=0)
@@ -155,8 +156,8 @@ def run_reference(args):
 
     def step():
         if kind == "reference":
-            return O.ref_single_pass_parallel(x, cores, m=16, R=args.R, B=args.B)
-        return O.single_pass(x, threads=cores, m=16, R=args.R, B=args.B)
+            return O.ref_single_pass_parallel(x, cores, m=args.m, R=args.R, B=args.B)
+        return O.single_pass(x, threads=cores, m=args.m, R=args.R, B=args.B)
 
     for _ in range(args.warmup):
         step()
@@ -169,7 +170,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f16 in, f32 accumulate (CPU emulation)", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "single_pass m=16 R=%d B=%d uniform[0,1) seed 0" % (args.R, args.B),
+            "config": {"workload": "single_pass m=%d R=%d B=%d uniform[0,1) seed 0" % (args.m, args.R, args.B),
                        "n_per_step": n_sample, "n_target": args.n, "parallelism": "host threads"},
             "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind,
                              "sample": f"n={n_sample} per step (bounded sample of the n=2^30 workload)"},
@@ -198,7 +199,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     lib = _capi.load()
     n = args.n
-    cfg = T.ReductionConfig(m=16, R=args.R, B=args.B, engine=T.Engine(args.engine))
+    cfg = T.ReductionConfig(m=args.m, R=args.R, B=args.B, engine=T.Engine(args.engine))
     c_cfg = cfg.to_c()
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)
@@ -359,8 +360,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f16 in, f32 accumulate (tensor core)", "data": "synthetic",
             "config": {"workload": "BASELINE configs[1]: single_pass chained-MMA reduction, n=2^30 fp16 per GPU, "
-                                   "m=16 R=%d B=%d, uniform[0,1) seed 0" % (args.R, args.B),
-                       "n_per_gpu": n, "n_total": world * n, "m": 16, "R": args.R, "B": args.B,
+                                   "m=%d R=%d B=%d, uniform[0,1) seed 0" % (args.m, args.R, args.B),
+                       "n_per_gpu": n, "n_total": world * n, "m": args.m, "R": args.R, "B": args.B,
                        "engine": engine_used,
                        "parallelism": f"shard{world}" + ("+nccl_allreduce" if world > 1 else ""),
                        "l2": "input 2 GiB per GPU > 126 MB L2: no flush needed"},

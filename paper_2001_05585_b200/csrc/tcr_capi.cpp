@@ -157,9 +157,8 @@ int check_supported(const tcr_config* c) {
         const tcr::SpGeometry g = tcr::make_geometry(1u << 20, c->m, c->R, c->B);
         if (!tcr::genm_supported(g))
             return fail(TCR_NOT_SUPPORTED, "fragment side m=" + std::to_string(c->m) + " with R=" + std::to_string(c->R) +
-                                               " is not implemented on the B200 path (supported: m=16 any R; m in "
-                                               "{4,32,64,128} any R; m=8 with R in {1,2} or 4|R; m=2 with R in "
-                                               "{1,2} or 4|R)");
+                                               " exceeds the B200 path's index limits (R*m^2 too large for the "
+                                               "32-bit per-chunk cursors)");
     }
     if (c->engine < TCR_ENGINE_AUTO || c->engine > TCR_ENGINE_MMA_SYNC_ASYNC)
         return fail(TCR_INVALID_ARGUMENT, "unknown engine");

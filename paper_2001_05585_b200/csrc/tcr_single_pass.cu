@@ -417,6 +417,9 @@ SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B) {
     uint64_t cap = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
     if (const char* e = std::getenv("TCR_GROUP_CAP")) cap = std::strtoull(e, nullptr, 10);  // profiling knob
     while (G > 1 && uint64_t(G) * g.W > cap) G >>= 1;
+    // m in {2, 8}: up to 4 chunks share a period of the selector layout (tcr_sp_genm.cu), so a
+    // group must hold a multiple of 4 chunks
+    if ((m == 2 || m == 8) && G < 4) G = 4;
     g.G = G;
     g.group_elems = uint64_t(G) * g.block_elems;
     g.n_groups = (g.n_blocks + G - 1) / G;

@@ -30,7 +30,7 @@ using namespace pipe;
 
 constexpr int kGmWarps = 8;
 constexpr int kGmThreads = 32 * kGmWarps;
-constexpr int kGmTrDepth = 8;                 // transposed stream: 512-byte tile stages per warp
+constexpr int kGmTrDepth = 16;                // transposed stream: 512-byte tile stages per warp
 
 __device__ __forceinline__ void cp16(uint32_t saddr, const void* g, uint32_t bytes) {
     asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
@@ -88,104 +88,151 @@ __device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, f
 }
 
 // ===================================================================== natural layout, m in {2, 4}
-// Unit = 16 A-rows.  L >= 1: rows per chunk (unit = 16 chunks); L == 0: CR chunks per row.
+// A PERIOD is lcm(16, chunk) elements = PR 16-element rows holding CP whole chunks (m = 4: one
+// chunk of R rows; m = 2: CP = 4 / gcd(4, R) chunks, which may straddle rows).  A row i of an
+// MMA = row rho of period i, so a unit = 16 periods and the chain over the PR rows of a period
+// accumulates in D with B[k][n] = [element 16 rho + k of the period is column j of chunk slot
+// q, n = q m + j].  Stages: row blocks of RB (a power of two <= 16) rows of all 16 periods.
 struct NatShape {
-    uint32_t L, CR, unit_rows, chunks_per_unit;
+    uint32_t PR, CP;           // rows and chunks per period
+    uint32_t RB;               // rows per stage
+    uint32_t chunks_per_unit;  // 16 * CP
 };
 
-template <int M>
+// RBC > 0: compile-time fast path for PR == RBC (one stage per unit, shifts instead of
+// divisions, a ring of ND = max(2, 8 / RBC) stages); RBC == 0: any PR (row blocks of S.RB).
+template <int RBC>
+__host__ __device__ constexpr int nat_depth() { return RBC == 0 ? 2 : (8 / RBC > 2 ? 8 / RBC : 2); }
+
+template <int M, int RBC>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, const NatShape S) {
+    constexpr int ND = nat_depth<RBC>();
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
     const uint32_t R = p.R;
-    const uint32_t unit_bytes = S.unit_rows * 32u;
-    float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * 2u * unit_bytes);
-    float* s_block = s_chunk + kMaxChunksGenm;
-    const uint32_t buf0 = smem_u32(dsm) + warp * 2u * unit_bytes;
-    const uint64_t chunk_el = uint64_t(R) * M * M;
+    const uint32_t RB = RBC ? uint32_t(RBC) : S.RB;
+    const uint32_t PR = RBC ? uint32_t(RBC) : S.PR;
+    const uint32_t nblk = RBC ? 1u : (PR + RB - 1) / RB;               // stages per unit
+    const uint32_t stage_bytes = 16u * RB * 32u;
+    float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * ND * stage_bytes);
+    float* s_block = s_chunk + p.G * p.W;
+    const uint32_t ring = smem_u32(dsm) + warp * ND * stage_bytes;
+    const uint32_t ce = R * M * M;                                    // chunk elements
+    const uint32_t period_el = PR * 16u;
     const uint32_t Cg = p.G * p.W;
     const uint32_t units = (Cg + S.chunks_per_unit - 1) / S.chunks_per_unit;
+    const bool straddle = S.CP > 1 && PR > 1;
     const uint16_t* x = static_cast<const uint16_t*>(p.x);
-    // selector B: thread holds B[2c][g], B[2c+1][g], B[2c+8][g], B[2c+9][g]
-    auto bsel = [&](uint32_t k) -> bool {
-        if (S.L > 0) return (k % M) == g && g < M;
-        const uint32_t q = k / uint32_t(R * M * M);
-        return q * M + (k % M) == g;
+    // selector B for period row rho: thread holds B[2c][g], B[2c+1][g], B[2c+8][g], B[2c+9][g]
+    auto bsel = [&](uint32_t rho, uint32_t k) -> bool {
+        const uint32_t e = 16u * rho + k;                             // element of the period
+        return (e / ce) * M + (e % M) == g;
     };
-    const uint32_t b0 = sel2(bsel(2 * c), bsel(2 * c + 1)), b1 = sel2(bsel(2 * c + 8), bsel(2 * c + 9));
-    // ldmatrix (non-transposed) row supplied by this lane: A row rho, column half
-    const uint32_t rho = (lane & 7u) + 8u * ((lane >> 3) & 1u), half = lane >> 4;
+    uint32_t b0 = sel2(bsel(0, 2 * c), bsel(0, 2 * c + 1)), b1 = sel2(bsel(0, 2 * c + 8), bsel(0, 2 * c + 9));
+    // ldmatrix (non-transposed) row supplied by this lane: A row (period) rho8, column half.
+    // Stage layout: 16-byte unit u = 2 (period * rb + row) + half, stored at u ^ (period & 7)
+    // (a bijection for rb a power of two; the 8 periods of one ldmatrix phase hit 8 bank groups).
+    const uint32_t rho8 = (lane & 7u) + 8u * ((lane >> 3) & 1u), half = lane >> 4;
     bool ovf = false;
 
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
-        const uint64_t gel0 = gi * uint64_t(Cg) * chunk_el;               // first element of the group
-        const uint64_t gel1 = gel0 + uint64_t(Cg) * chunk_el;
+        const uint64_t gel0 = gi * uint64_t(Cg) * ce;                     // first element of the group
+        const uint64_t gel1 = gel0 + uint64_t(Cg) * ce;
         const uint64_t lim = gel1 < p.n ? gel1 : p.n;
-        auto issue = [&](uint32_t u, uint32_t b) {
-            if (u < units) {
-                const uint64_t e_unit = gel0 + uint64_t(u) * S.chunks_per_unit * chunk_el;
-                for (uint32_t piece = lane; piece < S.unit_rows * 2u; piece += 32) {
-                    const uint64_t e = e_unit + uint64_t(piece) * 8u;
-                    const uint32_t bytes = e + 8 <= lim ? 16u : (e < lim ? uint32_t(lim - e) * 2u : 0u);
-                    cp16(buf0 + b * unit_bytes + piece * 16u, x + (e < lim ? e : 0), bytes);
+        // every load in range: the units cover exactly the group (16 * CP | Cg) and it is whole
+        const bool full = gel1 <= p.n && Cg % S.chunks_per_unit == 0;
+        const uint32_t my_units = units > warp ? (units - warp + kGmWarps - 1) / kGmWarps : 0;
+        const uint32_t F = my_units * nblk;                               // stages this warp streams
+        uint32_t iu = 0, iblk = 0, islot = 0;                             // issue cursor
+        auto issue = [&]() {
+            if (iu < my_units) {
+                const uint32_t r0 = iblk * RB, rb = RBC ? uint32_t(RBC) : min(RB, PR - r0);
+                const uint64_t e_unit = gel0 + uint64_t(warp + iu * kGmWarps) * 16u * period_el + r0 * 16u;
+                const uint32_t dst = ring + islot * stage_bytes;
+#pragma unroll
+                for (uint32_t t = 0; t < (RBC ? uint32_t(RBC) : 16u); ++t) {
+                    if (!RBC && t >= rb) break;
+                    const uint32_t piece = lane + 32u * t;
+                    const uint32_t per = piece / (2u * rb), rr = piece % (2u * rb);   // shifts: rb pow2
+                    const uint64_t e = e_unit + per * period_el + rr * 8u;
+                    if (full) {
+                        cp16(dst + ((piece ^ (per & 7u)) * 16u), x + e, 16u);
+                    } else {
+                        const uint32_t bytes = e + 8 <= lim ? 16u : (e < lim ? uint32_t(lim - e) * 2u : 0u);
+                        cp16(dst + ((piece ^ (per & 7u)) * 16u), x + (e < lim ? e : 0), bytes);
+                    }
+                }
+                if (++iblk == nblk) {
+                    iblk = 0;
+                    ++iu;
                 }
             }
             cp_commit();
+            islot = islot + 1 == uint32_t(ND) ? 0 : islot + 1;
         };
-        uint32_t b = 0;
-        uint32_t u = warp;
-        issue(u, 0);
-        for (; u < units; u += kGmWarps, b ^= 1u) {
-            issue(u + kGmWarps, b ^ 1u);
-            cp_wait<1>();
+#pragma unroll
+        for (int f = 0; f < ND - 1; ++f) issue();
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t cu = 0, cblk = 0, cslot = 0;                             // consume cursor
+        for (uint32_t f = 0; f < F; ++f) {
+            issue();
+            cp_wait<ND - 1>();
             __syncwarp();
-            const uint32_t base = buf0 + b * unit_bytes;
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            const uint32_t steps = S.L > 0 ? S.L : 1u;
-            for (uint32_t i = 0; i < steps; ++i) {
-                const uint32_t row = S.L > 0 ? rho * S.L + i : rho;
+            const uint32_t base = ring + cslot * stage_bytes;
+            cslot = cslot + 1 == uint32_t(ND) ? 0 : cslot + 1;
+            const uint32_t r0 = cblk * RB, rb = RBC ? uint32_t(RBC) : min(RB, PR - r0);
+#pragma unroll
+            for (uint32_t i = 0; i < (RBC ? uint32_t(RBC) : 16u); ++i) {
+                if (!RBC && i >= rb) break;
+                if (straddle) {
+                    const uint32_t rho = r0 + i;
+                    b0 = sel2(bsel(rho, 2 * c), bsel(rho, 2 * c + 1));
+                    b1 = sel2(bsel(rho, 2 * c + 8), bsel(rho, 2 * c + 9));
+                }
+                const uint32_t unit16 = 2u * (rho8 * rb + i) + half;
                 uint32_t d0, d1, d2, d3;
-                ldsm4(base + row * 32u + half * 16u, d0, d1, d2, d3);
+                ldsm4(base + ((unit16 ^ (rho8 & 7u)) * 16u), d0, d1, d2, d3);
                 mma_16816(acc, d0, d1, d2, d3, b0, b1);   // C_i = A_i x Bsel + C_{i-1}
             }
             __syncwarp();
-            // acc: (row g, col 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
-            const uint32_t cu0 = u * S.chunks_per_unit;
-            if (S.L > 0) {
-                // chunk = A row; partial j in column j (j < M): lanes c = 0 (j 0,1) and c = 1 (j 2,3)
+            const uint32_t u = cu;
+            if (++cblk < nblk) continue;
+            cblk = 0;
+            ++cu;
+            // unit complete. acc: (period g, col 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
+            const uint32_t cu0 = (warp + u * kGmWarps) * S.chunks_per_unit;
+            if (M == 4) {
+                // one chunk per period; partial j in column j: lanes c = 0 (j 0,1) and c = 1 (j 2,3)
                 const float h0 = h_round(acc[0]), h1 = h_round(acc[1]), h2 = h_round(acc[2]), h3 = h_round(acc[3]);
                 const float n0 = __shfl_down_sync(kFull, h0, 1), n1 = __shfl_down_sync(kFull, h1, 1);
                 const float n2 = __shfl_down_sync(kFull, h2, 1), n3 = __shfl_down_sync(kFull, h3, 1);
                 if (c == 0) {
                     // ascending-j fp32 sum from 0.0f, then + 0 (fragment.hpp:89-92)
-                    float ra = 0.0f, rb = 0.0f;
-                    ra = ra + h0; ra = ra + h1;
-                    rb = rb + h2; rb = rb + h3;
-                    if (M == 4) {
-                        ra = ra + n0; ra = ra + n1;
-                        rb = rb + n2; rb = rb + n3;
-                    }
+                    float ra = 0.0f, rb2 = 0.0f;
+                    ra = ra + h0; ra = ra + h1; ra = ra + n0; ra = ra + n1;
+                    rb2 = rb2 + h2; rb2 = rb2 + h3; rb2 = rb2 + n2; rb2 = rb2 + n3;
                     ra = ra + 0.0f;
-                    rb = rb + 0.0f;
-                    ovf |= !isfinite(ra) || !isfinite(rb);
+                    rb2 = rb2 + 0.0f;
+                    ovf |= !isfinite(ra) || !isfinite(rb2);
                     if (cu0 + g < Cg) s_chunk[cu0 + g] = ra;
-                    if (cu0 + g + 8 < Cg) s_chunk[cu0 + g + 8] = rb;
+                    if (cu0 + g + 8 < Cg) s_chunk[cu0 + g + 8] = rb2;
                 }
             } else {
-                // M == 2, CR chunks per row: lane (g, q) owns chunk q of rows g and g+8
-                if (c < S.CR) {
-                    float ra = 0.0f, rb = 0.0f;
+                // M == 2: lane (g, q) owns chunk slot q of periods g and g+8 (columns 2q, 2q+1)
+                if (c < S.CP) {
+                    float ra = 0.0f, rb2 = 0.0f;
                     ra = ra + h_round(acc[0]); ra = ra + h_round(acc[1]); ra = ra + 0.0f;
-                    rb = rb + h_round(acc[2]); rb = rb + h_round(acc[3]); rb = rb + 0.0f;
-                    ovf |= !isfinite(ra) || !isfinite(rb);
-                    const uint32_t ca = cu0 + g * S.CR + c, cb = cu0 + (g + 8) * S.CR + c;
+                    rb2 = rb2 + h_round(acc[2]); rb2 = rb2 + h_round(acc[3]); rb2 = rb2 + 0.0f;
+                    ovf |= !isfinite(ra) || !isfinite(rb2);
+                    const uint32_t ca = cu0 + g * S.CP + c, cb = cu0 + (g + 8) * S.CP + c;
                     if (ca < Cg) s_chunk[ca] = ra;
-                    if (cb < Cg) s_chunk[cb] = rb;
+                    if (cb < Cg) s_chunk[cb] = rb2;
                 }
             }
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
         }
         cp_wait<0>();
         group_epilogue(p, gi, s_chunk, s_block);
@@ -197,36 +244,54 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
 }
 
 // ================================================================ transposed tiles, m = 8 or 16*S
-// Item = K consecutive 256-element tiles holding CPT whole chunks (m = 8, R in {1,2,4}) or one
-// chunk (m = 8 with 4 | R, and m >= 32).
+// Item = K consecutive 256-element tiles holding CPT whole chunks: m = 8 -> lcm(16, 4R) segments
+// (CPT = 4 / gcd(4, R); a chunk may straddle tiles, so the selector follows the tile), m >= 32
+// -> one chunk.
 struct TrShape {
     uint32_t K;      // tiles per item
     uint32_t CPT;    // chunks per item
+};
+
+// Chunk results leave the MMA accumulators through a per-warp staging area instead of
+// warp shuffles: each lane stores its binary16-rounded partials (row = chunk, column = j), and
+// once a batch of chunks is staged each lane sums ONE chunk's row in ascending j (fragment.hpp:
+// 89-92).  Row strides (12 floats for m = 8, m + 4 otherwise) keep the 128-bit row reads
+// conflict free.
+template <int MM>
+struct TrStage {
+    static constexpr uint32_t SW = MM == 8 ? 12u : uint32_t(MM) + 4u;           // row stride
+    static constexpr uint32_t ROWS = MM == 8 ? 32u : (1024u / MM < 32u ? 1024u / MM : 32u);
+    static constexpr uint32_t FLOATS = ROWS * SW;                                 // per warp
 };
 
 template <int MM>   // 8, 32, 64, 128
 __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, const TrShape S) {
     constexpr int D = kGmTrDepth;
     constexpr uint32_t SG = MM >= 32 ? MM / 16 : 1;    // column groups per chunk (m >= 32)
-    extern __shared__ __align__(128) unsigned char s_ring[];   // [kGmWarps][D][512] + tables
+    using ST = TrStage<MM>;
+    extern __shared__ __align__(128) unsigned char s_ring[];   // [kGmWarps][D][512], staging, tables
     __shared__ float s_scratch[32];
     __shared__ int s_last;
-    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
-    float* s_block = s_chunk + kMaxChunksGenm;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
     const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    float* s_stage = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512) + warp * ST::FLOATS;
+    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512) + kGmWarps * ST::FLOATS;
     const uint32_t Cg = p.G * p.W;
+    float* s_block = s_chunk + Cg;
     const uint32_t items = Cg / S.CPT;
     const uint32_t R = p.R;
+    // staged rows per batch: chunks (m = 8: CPT per item) or items (m >= 32, one chunk each)
+    const uint32_t batch_items = MM == 8 ? 32u / S.CPT : ST::ROWS;
     const uint16_t* x = static_cast<const uint16_t*>(p.x);
-    // selector rows kappa in {2c, 2c+1, 2c+8, 2c+9}, column n = g
-    auto bsel = [&](uint32_t k) -> bool {
+    // selector rows kappa in {2c, 2c+1, 2c+8, 2c+9} of tile kt of the item, column n = g
+    auto bsel = [&](uint32_t kt, uint32_t k) -> bool {
         if (MM >= 32) return (k % SG) == g;
-        if (S.CPT > 1) return (k / (4u * R)) == g;   // m = 8: chunk slot of tile row k
+        if (S.CPT > 1) return ((16u * kt + k) / (4u * R)) == g;   // m = 8: chunk slot of segment
         return g == 0;
     };
-    const uint32_t b0 = sel2(bsel(2 * c), bsel(2 * c + 1)), b1 = sel2(bsel(2 * c + 8), bsel(2 * c + 9));
+    uint32_t b0 = sel2(bsel(0, 2 * c), bsel(0, 2 * c + 1)), b1 = sel2(bsel(0, 2 * c + 8), bsel(0, 2 * c + 9));
+    const bool straddle = MM == 8 && S.CPT > 1 && S.K > 1;      // m = 8, R odd or R = 2 mod 4
     // swizzled 16-byte lines (conflict-free transposing ldmatrix), as in tcr_sp_async.cu
     auto swz = [](uint32_t k, uint32_t h) { return 32u * k + 16u * (h ^ ((k >> 2) & 1u)); };
     const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
@@ -236,62 +301,194 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
 
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
         const uint64_t tile0 = gi * uint64_t(items) * S.K;          // first tile of the group
+        const bool full = (tile0 + uint64_t(items) * S.K) * 256u <= p.n;
         const uint32_t my_items = items > warp ? (items - warp + kGmWarps - 1) / kGmWarps : 0;
-        const uint32_t F = my_items * S.K;                            // tiles this warp streams
-        auto tile_of = [&](uint32_t f) -> uint64_t {                  // warp-local stream -> tile
-            const uint32_t it = f / S.K, k = f - it * S.K;
-            return tile0 + uint64_t(warp + it * kGmWarps) * S.K + k;
-        };
-        auto issue = [&](uint32_t f) {
-            if (f < F) {
-                const uint64_t e = tile_of(f) * 256u + 8u * lane;
-                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
-                cp16(ring + (f % D) * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+        uint32_t iit = 0, ik = 0, islot = 0;                          // issue cursor
+        auto issue = [&]() {
+            if (iit < my_items) {
+                const uint64_t e = (tile0 + uint64_t(warp + iit * kGmWarps) * S.K + ik) * 256u + 8u * lane;
+                if (full) {
+                    cp16(ring + islot * 512u + cp_dst, x + e, 16u);
+                } else {
+                    const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                    cp16(ring + islot * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+                }
+                if (++ik == S.K) {
+                    ik = 0;
+                    ++iit;
+                }
             }
             cp_commit();
+            islot = islot + 1 == uint32_t(D) ? 0 : islot + 1;
         };
-#pragma unroll
-        for (int f = 0; f < D - 1; ++f) issue(uint32_t(f));
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t k_in_item = 0, it = 0;
-        for (uint32_t f = 0; f < F; ++f) {
-            issue(f + D - 1);
-            cp_wait<D - 1>();
+        // finish a staged batch of `nb` items starting at item-of-warp index it0
+        auto flush = [&](uint32_t it0, uint32_t nb) {
             __syncwarp();
-            uint32_t d0, d1, d2, d3;
-            ldsm4t(ring + (f % D) * 512u + ld_off, d0, d1, d2, d3);
-            __syncwarp();
-            mma_16816(acc, d0, d1, d2, d3, b0, b1);
-            if (++k_in_item < S.K) continue;
-            // ---- item complete: acc = (j16 = g, n = 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
-            const uint32_t item = warp + it * kGmWarps;
-            if (MM == 8) {
-                // partial(chunk slot n, j8 = g) = D[g][n] + D[g+8][n]
-                const float pe = h_round(acc[0] + acc[2]), po = h_round(acc[1] + acc[3]);
-                for (uint32_t sl = 0; sl < S.CPT; ++sl) {
-                    const float src = (sl & 1u) ? po : pe;
-                    float r = 0.0f;
-                    for (uint32_t j = 0; j < 8; ++j) r = r + __shfl_sync(kFull, src, 4 * j + (sl >> 1));
-                    r = r + 0.0f;
-                    ovf |= !isfinite(r);
-                    if (lane == 0) s_chunk[item * S.CPT + sl] = r;
-                }
-            } else {
-                const float h[4] = {h_round(acc[0]), h_round(acc[1]), h_round(acc[2]), h_round(acc[3])};
+            const uint32_t rows = MM == 8 ? nb * S.CPT : nb;
+            if (lane < rows) {
+                const float* row = s_stage + lane * ST::SW;
                 float r = 0.0f;
 #pragma unroll
-                for (uint32_t j = 0; j < uint32_t(MM); ++j) {   // ascending j = 16 n + j16
-                    const uint32_t n = j >> 4, j16 = j & 15u;
-                    const uint32_t reg = 2u * (j16 >> 3) + (n & 1u);
-                    r = r + __shfl_sync(kFull, h[reg], 4 * (j16 & 7u) + (n >> 1));
+                for (uint32_t j = 0; j < (MM == 8 ? 8u : uint32_t(MM)); j += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + j);
+                    r = r + v.x; r = r + v.y; r = r + v.z; r = r + v.w;
                 }
                 r = r + 0.0f;
                 ovf |= !isfinite(r);
-                if (lane == 0) s_chunk[item] = r;
+                const uint32_t b = MM == 8 ? lane / S.CPT : lane;
+                const uint32_t item = warp + (it0 + b) * kGmWarps;
+                s_chunk[MM == 8 ? item * S.CPT + lane % S.CPT : item] = r;
+            }
+            __syncwarp();
+        };
+#pragma unroll 1
+        for (int f = 0; f < D - 1; ++f) issue();
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t ck = 0, it = 0, cslot = 0, nb = 0;
+        while (it < my_items) {
+            issue();
+            cp_wait<D - 1>();
+            __syncwarp();
+            uint32_t d0, d1, d2, d3;
+            ldsm4t(ring + cslot * 512u + ld_off, d0, d1, d2, d3);
+            __syncwarp();
+            cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
+            if (straddle) {
+                b0 = sel2(bsel(ck, 2 * c), bsel(ck, 2 * c + 1));
+                b1 = sel2(bsel(ck, 2 * c + 8), bsel(ck, 2 * c + 9));
+            }
+            mma_16816(acc, d0, d1, d2, d3, b0, b1);
+            if (++ck < S.K) continue;
+            ck = 0;
+            // ---- item complete: acc = (j16 = g, n = 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
+            if (MM == 8) {
+                // partial(chunk slot n, j8 = g) = D[g][n] + D[g+8][n]  -> staged row (nb CPT + n)
+                const uint32_t r0 = nb * S.CPT;
+                if (2 * c < S.CPT) s_stage[(r0 + 2 * c) * ST::SW + g] = h_round(acc[0] + acc[2]);
+                if (2 * c + 1 < S.CPT) s_stage[(r0 + 2 * c + 1) * ST::SW + g] = h_round(acc[1] + acc[3]);
+            } else {
+                // partial(j = 16 n + j16) = D[j16][n]
+                float* row = s_stage + nb * ST::SW;
+                if (2 * c < SG) {
+                    row[16 * (2 * c) + g] = h_round(acc[0]);
+                    row[16 * (2 * c) + g + 8] = h_round(acc[2]);
+                }
+                if (2 * c + 1 < SG) {
+                    row[16 * (2 * c + 1) + g] = h_round(acc[1]);
+                    row[16 * (2 * c + 1) + g + 8] = h_round(acc[3]);
+                }
             }
             acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-            k_in_item = 0;
             ++it;
+            if (++nb == batch_items) {
+                flush(it - nb, nb);
+                nb = 0;
+            }
+        }
+        if (nb) flush(it - nb, nb);
+        cp_wait<0>();
+        group_epilogue(p, gi, s_chunk, s_block);
+    }
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+    __threadfence();
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
+}
+
+// =============================================================== wide fragments, m >= 256
+// A chunk (R fragments of m x m) is streamed in column SLABS of 256 columns: for slab s, the R*m
+// rows of the chunk contribute one 256-element tile each (elements [256 s, 256 s + 256) of the
+// row, 512 contiguous bytes).  A tile's 16 segments are 16 different column groups, so two
+// HMMA.16816 per tile with identity selectors (B_lo[k][n] = [k == n], B_hi[k][n] = [k == n + 8])
+// accumulate the slab's 256 column sums over the chain of rows in D_lo / D_hi; at the end of a
+// slab the partials are rounded to binary16 (reduction.hpp:179-181) and added to the running
+// ascending-j finishing sum (:182, fragment.hpp:89-92), carried across the m / 256 slabs.
+__global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, const uint32_t m) {
+    constexpr int D = kGmTrDepth;
+    extern __shared__ __align__(128) unsigned char s_ring[];   // [kGmWarps][D][512] + tables
+    __shared__ float s_scratch[32];
+    __shared__ int s_last;
+    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
+    float* s_block = s_chunk + p.G * p.W;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned g = lane >> 2, c = lane & 3u;
+    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    const uint32_t Cg = p.G * p.W;
+    const uint32_t rows = p.R * m;                  // rows of a chunk (R fragments)
+    const uint32_t slabs = m / 256u;
+    const uint64_t chunk_el = uint64_t(rows) * m;
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint32_t blo0 = sel2(2 * c == g, 2 * c + 1 == g), blo1 = sel2(2 * c + 8 == g, 2 * c + 9 == g);
+    const uint32_t bhi0 = sel2(2 * c == g + 8, 2 * c + 1 == g + 8), bhi1 = sel2(2 * c + 8 == g + 8, 2 * c + 9 == g + 8);
+    auto swz = [](uint32_t k, uint32_t h) { return 32u * k + 16u * (h ^ ((k >> 2) & 1u)); };
+    const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_off = swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+    bool ovf = false;
+
+    // stream cursor: item (chunk of this warp), slab, row
+    struct Cur {
+        uint32_t it, s, i;
+    };
+    auto advance = [&](Cur& q) {
+        if (++q.i == rows) {
+            q.i = 0;
+            if (++q.s == slabs) {
+                q.s = 0;
+                ++q.it;
+            }
+        }
+    };
+    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+        const uint64_t gel0 = gi * uint64_t(Cg) * chunk_el;
+        const uint32_t my_items = Cg > warp ? (Cg - warp + kGmWarps - 1) / kGmWarps : 0;
+        Cur iq{0, 0, 0}, cq{0, 0, 0};
+        uint32_t slot_i = 0, slot_c = 0;
+        auto issue = [&]() {
+            if (iq.it < my_items) {
+                const uint64_t e = gel0 + uint64_t(warp + iq.it * kGmWarps) * chunk_el + uint64_t(iq.i) * m +
+                                   256u * iq.s + 8u * lane;
+                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                cp16(ring + slot_i * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+                advance(iq);
+            }
+            cp_commit();
+            slot_i = slot_i + 1 == D ? 0 : slot_i + 1;
+        };
+#pragma unroll 1
+        for (int f = 0; f < D - 1; ++f) issue();
+        float lo[4] = {0.f, 0.f, 0.f, 0.f}, hi[4] = {0.f, 0.f, 0.f, 0.f};
+        float r = 0.0f;
+        while (cq.it < my_items) {
+            issue();
+            cp_wait<D - 1>();
+            __syncwarp();
+            uint32_t d0, d1, d2, d3;
+            ldsm4t(ring + slot_c * 512u + ld_off, d0, d1, d2, d3);
+            __syncwarp();
+            slot_c = slot_c + 1 == D ? 0 : slot_c + 1;
+            mma_16816(lo, d0, d1, d2, d3, blo0, blo1);
+            mma_16816(hi, d0, d1, d2, d3, bhi0, bhi1);
+            const Cur done = cq;
+            advance(cq);
+            if (done.i + 1 < rows) continue;
+            // ---- slab complete: D[j16][n] = partial of column 256 s + 16 n + j16 (n < 8 in lo)
+            const float hl[4] = {h_round(lo[0]), h_round(lo[1]), h_round(lo[2]), h_round(lo[3])};
+            const float hh[4] = {h_round(hi[0]), h_round(hi[1]), h_round(hi[2]), h_round(hi[3])};
+#pragma unroll
+            for (uint32_t j = 0; j < 256u; ++j) {   // ascending j = 16 n + j16
+                const uint32_t n = (j >> 4) & 7u, j16 = j & 15u;
+                const uint32_t reg = 2u * (j16 >> 3) + (n & 1u);
+                const float v = j < 128u ? hl[reg] : hh[reg];
+                r = r + __shfl_sync(kFull, v, 4 * (j16 & 7u) + (n >> 1));
+            }
+            lo[0] = lo[1] = lo[2] = lo[3] = 0.f;
+            hi[0] = hi[1] = hi[2] = hi[3] = 0.f;
+            if (done.s + 1 < slabs) continue;
+            r = r + 0.0f;
+            ovf |= !isfinite(r);
+            if (lane == 0) s_chunk[warp + done.it * kGmWarps] = r;
+            r = 0.0f;
         }
         cp_wait<0>();
         group_epilogue(p, gi, s_chunk, s_block);
@@ -302,38 +499,40 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
 }
 
-bool nat_shape(uint32_t m, uint32_t R, uint32_t Cg, NatShape* S) {
-    const uint32_t ce = R * m * m;            // chunk elements
-    if (ce >= 16) {
-        if (ce % 16) return false;            // chunk must be whole 16-element rows
-        S->L = ce / 16;
-        if (S->L > 16) return false;          // unit = 16 chunks <= 8 KB per stage
-        S->CR = 1;
-        S->unit_rows = 16 * S->L;
-        S->chunks_per_unit = 16;
-    } else {
-        if (16 % ce) return false;            // whole chunks per row
-        S->L = 0;
-        S->CR = 16 / ce;
-        if (S->CR * m > 8) return false;      // N = 8 selector columns
-        S->unit_rows = 16;
-        S->chunks_per_unit = 16 * S->CR;
+uint32_t gcd32(uint32_t a, uint32_t b) {
+    while (b) {
+        const uint32_t t = a % b;
+        a = b;
+        b = t;
     }
-    if ((uint64_t(Cg) * ce) % 8) return false;  // 16-byte copies never straddle a group
+    return a;
+}
+
+bool nat_shape(uint32_t m, uint32_t R, uint32_t Cg, NatShape* S) {
+    const uint64_t ce = uint64_t(R) * m * m;             // chunk elements (m in {2, 4}: 4R or 16R)
+    if (ce > 0xFFFFFFFFull / 32) return false;
+    // period = lcm(16, ce) elements
+    const uint64_t g16 = gcd32(16, uint32_t(ce % 16));  // gcd(16, ce)
+    const uint64_t period = ce / g16 * 16;
+    S->PR = uint32_t(period / 16);
+    S->CP = uint32_t(period / ce);
+    if (S->CP * m > 8) return false;                     // N = 8 selector columns
+    uint32_t rb = 1;
+    while (rb * 2 <= S->PR && rb < 16) rb *= 2;
+    S->RB = rb;
+    S->chunks_per_unit = 16 * S->CP;
+    if (Cg % S->CP) return false;                        // groups start on a period
     return true;
 }
 
 bool tr_shape(uint32_t m, uint32_t R, uint32_t Cg, TrShape* S) {
     if (m == 8) {
-        if (R == 1 || R == 2 || R == 4) {
-            S->K = 1;
-            S->CPT = 4 / R;
-        } else if (R % 4 == 0) {
-            S->K = R / 4;
-            S->CPT = 1;
-        } else {
-            return false;
-        }
+        // chunk = 4R segments; item = lcm(16, 4R) segments = K tiles holding CPT (<= 4) chunks
+        const uint64_t cs = 4ull * R;
+        const uint64_t item = cs / gcd32(16, uint32_t(cs % 16)) * 16;
+        if (item / 16 > 0xFFFFFFFFull) return false;
+        S->K = uint32_t(item / 16);
+        S->CPT = uint32_t(item / cs);
     } else if (m == 32 || m == 64 || m == 128) {
         S->K = R * (m / 16) * (m / 16);
         S->CPT = 1;
@@ -345,8 +544,14 @@ bool tr_shape(uint32_t m, uint32_t R, uint32_t Cg, TrShape* S) {
 
 }  // namespace
 
+bool wide_ok(const SpGeometry& g) {
+    // m >= 256: rows = R m and the per-chunk cursor fit 32 bits
+    return g.m >= 256 && uint64_t(g.R) * g.m < (1ull << 31) && g.G * g.W <= uint32_t(kMaxChunksGenm);
+}
+
 bool genm_supported(const SpGeometry& g) {
     const uint32_t Cg = g.G * g.W;
+    if (g.m >= 256) return wide_ok(g);
     if (g.m == 2 || g.m == 4) {
         NatShape S;
         return nat_shape(g.m, g.R, Cg, &S);
@@ -355,22 +560,45 @@ bool genm_supported(const SpGeometry& g) {
     return tr_shape(g.m, g.R, Cg, &S);
 }
 
+namespace {
+template <typename K, typename S>
+cudaError_t launch_gm(K fn, uint32_t dyn, uint64_t groups, const SpParams& p, const S& shape, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGmThreads, dyn);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = int(groups < uint64_t(per_sm) * sm_count() ? groups : uint64_t(per_sm) * sm_count());
+    fn<<<grid, kGmThreads, dyn, s>>>(p, shape);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) {
     const uint32_t Cg = g.G * g.W;
     const uint64_t groups = p.group_end - p.group_begin;
-    int per_sm = 0;
+    const uint32_t tables = (Cg + g.G + 3u) / 4u * 16u;   // chunk results [Cg] + block results [G]
     if (g.m == 2 || g.m == 4) {
         NatShape S;
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
-        const uint32_t dyn = kGmWarps * 2u * S.unit_rows * 32u + 2u * kMaxChunksGenm * 4u;
-        auto fn = g.m == 2 ? gm_nat_kernel<2> : gm_nat_kernel<4>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
-        if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGmThreads, dyn);
-        if (per_sm < 1) per_sm = 1;
-        const int grid = int(groups < uint64_t(per_sm) * sm_count() ? groups : uint64_t(per_sm) * sm_count());
-        fn<<<grid, kGmThreads, dyn, s>>>(p, S);
-        return cudaGetLastError();
+        void (*fn)(SpParams, NatShape) = nullptr;
+        int nd = 2;
+        const bool fast = S.PR == S.RB;   // PR a power of two <= 16: one stage per unit
+#define TCR_NAT(MV, RBV) \
+    { fn = gm_nat_kernel<MV, RBV>; nd = nat_depth<RBV>(); }
+        if (g.m == 2) {
+            if (!fast) TCR_NAT(2, 0) else if (S.RB == 1) TCR_NAT(2, 1) else if (S.RB == 2) TCR_NAT(2, 2)
+            else if (S.RB == 4) TCR_NAT(2, 4) else if (S.RB == 8) TCR_NAT(2, 8) else TCR_NAT(2, 16)
+        } else {
+            if (!fast) TCR_NAT(4, 0) else if (S.RB == 1) TCR_NAT(4, 1) else if (S.RB == 2) TCR_NAT(4, 2)
+            else if (S.RB == 4) TCR_NAT(4, 4) else if (S.RB == 8) TCR_NAT(4, 8) else TCR_NAT(4, 16)
+        }
+#undef TCR_NAT
+        return launch_gm(fn, kGmWarps * uint32_t(nd) * (16u * S.RB * 32u) + tables, groups, p, S, s);
+    }
+    if (g.m >= 256) {
+        if (!wide_ok(g)) return cudaErrorInvalidValue;
+        return launch_gm(gm_wide_kernel, kGmWarps * kGmTrDepth * 512u + tables, groups, p, g.m, s);
     }
     TrShape S;
     if (!tr_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
@@ -382,14 +610,14 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) 
     case 128: fn = gm_tr_kernel<128>; break;
     default: return cudaErrorInvalidValue;
     }
-    const uint32_t dyn = kGmWarps * kGmTrDepth * 512u + 2u * kMaxChunksGenm * 4u;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
-    if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGmThreads, dyn);
-    if (per_sm < 1) per_sm = 1;
-    const int grid = int(groups < uint64_t(per_sm) * sm_count() ? groups : uint64_t(per_sm) * sm_count());
-    fn<<<grid, kGmThreads, dyn, s>>>(p, S);
-    return cudaGetLastError();
+    uint32_t stage = 0;
+    switch (g.m) {
+    case 8: stage = TrStage<8>::FLOATS; break;
+    case 32: stage = TrStage<32>::FLOATS; break;
+    case 64: stage = TrStage<64>::FLOATS; break;
+    default: stage = TrStage<128>::FLOATS; break;
+    }
+    return launch_gm(fn, kGmWarps * (kGmTrDepth * 512u + stage * 4u) + tables, groups, p, S, s);
 }
 
 }  // namespace tcr

@@ -321,7 +321,12 @@ def test_full_size_against_golden(dist, seed, lgn, engine):
 # --------------------------------------------------------------------------- fragment sides m != 16
 
 GENM = [(2, 1, 128), (2, 2, 64), (2, 4, 32), (4, 1, 128), (4, 4, 128), (4, 3, 96), (4, 1, 1024), (8, 1, 128),
-        (8, 2, 256), (8, 4, 32), (8, 8, 64), (32, 1, 128), (32, 3, 32), (64, 1, 64), (128, 1, 32)]
+        (8, 2, 256), (8, 4, 32), (8, 8, 64), (32, 1, 128), (32, 3, 32), (64, 1, 64), (128, 1, 32),
+        # chunks straddling rows / tiles (m = 2, 8 with R odd or R = 2 mod 4), long chains (m = 4,
+        # R > 16: several row-block stages per period), wide fragments (m >= 256: column slabs)
+        (2, 3, 128), (2, 5, 32), (2, 6, 96), (2, 7, 64), (2, 20, 32), (2, 68, 64), (4, 17, 32), (4, 33, 64),
+        (8, 3, 128), (8, 5, 32), (8, 6, 64), (8, 7, 256), (8, 10, 32), (256, 1, 32), (256, 3, 64),
+        (512, 1, 32), (1024, 1, 32)]
 
 
 @pytest.mark.parametrize("m,R,B", GENM)
@@ -329,9 +334,15 @@ def test_genm_integers_exact_and_blocks(oracle, m, R, B):
     x = oracle.generate("integers", 3, (1 << 20) + 333)
     xd = torch.from_numpy(x).to(DEV).half()
     cfg = T.ReductionConfig(m=m, R=R, B=B)
+    ref = oracle.single_pass(x, threads=8, m=m, R=R, B=B)
+    # column sums of R*m values in 0..9 stay exact in binary16 up to 2048; beyond, the reference
+    # itself rounds them (reduction.hpp:179-181) and its value is the bar (block results are
+    # integers < 2^24, so every finalize order reproduces it exactly)
+    if 9 * R * m <= 2048:
+        assert ref.value == oracle.oracle64(x)
     for fin in (T.Finalize.tree, T.Finalize.ordered, T.Finalize.atomic):
         o = T.reduce(xd, T.ReductionConfig(m=m, R=R, B=B, finalize=fin))
-        assert o.value == oracle.oracle64(x) and not o.overflow, (m, R, B, fin)
+        assert o.value == ref.value and not o.overflow, (m, R, B, fin)
     _, ref_blocks = oracle.single_pass(x, threads=8, want_blocks=True, m=m, R=R, B=B)
     got = T.block_results(xd, cfg).cpu().numpy()
     assert np.array_equal(got.view(np.uint32), ref_blocks.view(np.uint32))
@@ -345,15 +356,26 @@ def test_genm_float_vs_reference(oracle, m, R, B, dist, seed):
     _, ref_blocks = oracle.single_pass(h, threads=8, want_blocks=True, m=m, R=R, B=B)
     got = T.block_results(xd, T.ReductionConfig(m=m, R=R, B=B)).cpu().numpy()
     same = (got.view(np.uint32) == ref_blocks.view(np.uint32)).mean()
-    diff = np.abs(got.astype(np.float64) - ref_blocks).max()
+    d = np.abs(got.astype(np.float64) - ref_blocks)
+    diff = d.max()
     print(f"\nm={m} R={R} B={B} {dist}: bit-identical blocks {same:.6f} max abs diff {diff:.3e}")
-    assert same >= 0.99 and diff <= 2.0 ** -4
+    if got.size >= 100:
+        assert same >= 0.99 and diff <= 2.0 ** -4
+    else:
+        # m >= 256: a handful of blocks, each a sum of m binary16-rounded column sums of R*m
+        # values; a column sum the tensor core rounds to the other side of a binary16 midpoint
+        # moves the block by one binary16 ulp of that column sum (<= 2^-10 of its abs sum)
+        hf = np.abs(h.view(np.float16).astype(np.float64))
+        be = (B // 32) * R * m * m
+        babs = np.add.reduceat(hf, np.arange(0, hf.size, be))
+        assert np.all(d <= 2.0 ** -10 * babs), (d, babs)
     ref = oracle.single_pass(h, threads=8, m=m, R=R, B=B)
     o = T.reduce(xd, T.ReductionConfig(m=m, R=R, B=B, finalize=T.Finalize.ordered))
     if same == 1.0:
         assert o.value == ref.value
     exact, absum = oracle.exact_sum_f16(h)
-    assert abs(o.value - ref.value) <= 2e-5 * max(abs(exact), 1e-3 * absum)
+    # uniform: |gpu - ref| <= 2e-5 |exact|; normal (sum ~ sqrt(n), cancellation): <= 1e-6 sum|x|
+    assert abs(o.value - ref.value) <= max(2e-5 * abs(exact), 1e-6 * absum)
     assert o.atomic_count == ref.atomic_count and o.mma_count == ref.mma_count
 
 
@@ -378,12 +400,25 @@ def test_reference_default_config_goldens():
         assert got.atomic_count == exp["atomic_count"] and got.mma_count == exp["mma_count"]
 
 
-def test_genm_unsupported_is_loud():
+def test_genm_every_side_and_chain_runs_on_device(oracle):
+    """Every power-of-two m the reference accepts (fragment.hpp:22-25) with R = 1..9 runs on the
+    device: integers exact, counters equal to the reference formulas."""
+    x = oracle.generate("integers", 5, 50000)
+    xd = torch.from_numpy(x).to(DEV).half()
+    for m in (2, 4, 8, 16, 32, 64, 128, 256, 512):
+        for R in range(1, 10):
+            cfg = T.ReductionConfig(m=m, R=R, B=64)
+            ref = oracle.single_pass(x, threads=4, m=m, R=R, B=64)
+            o = T.reduce(xd, cfg)
+            assert o.value == ref.value and not o.overflow, (m, R)
+            c = T.counters(x.size, cfg)
+            assert (o.atomic_count, o.mma_count, o.sim_steps) == (c.atomic_count, c.mma_count, c.sim_steps)
+
+
+def test_genm_limits_are_loud():
     x = torch.ones(4096, device=DEV, dtype=torch.float16)
     with pytest.raises(NotImplementedError):
-        T.reduce(x, T.ReductionConfig(m=8, R=3, B=128))
-    with pytest.raises(NotImplementedError):
-        T.reduce(x, T.ReductionConfig(m=256, R=1, B=128))
+        T.reduce(x, T.ReductionConfig(m=1 << 16, R=1 << 16, B=32))
 
 
 # --------------------------------------------------------------------------- the other Variants (:344-358)
