@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
         return (e / ce) * M + (e % M) == g;
     };
     uint32_t b0 = sel2(bsel(0, 2 * c), bsel(0, 2 * c + 1)), b1 = sel2(bsel(0, 2 * c + 8), bsel(0, 2 * c + 9));
+    const uint32_t bfin = sel2((2 * c) / M == g, (2 * c + 1) / M == g);   // finishing B2, rows k < 8
     // ldmatrix (non-transposed) row supplied by this lane: A row (period) rho8, column half.
     // Stage layout: 16-byte unit u = 2 (period * rb + row) + half, stored at u ^ (period & 7)
     // (a bijection for rb a power of two; the 8 periods of one ldmatrix phase hit 8 bank groups).
@@ -203,33 +204,24 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
             cblk = 0;
             ++cu;
             // unit complete. acc: (period g, col 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
-            const uint32_t cu0 = (warp + u * kGmWarps) * S.chunks_per_unit;
-            if (M == 4) {
-                // one chunk per period; partial j in column j: lanes c = 0 (j 0,1) and c = 1 (j 2,3)
-                const float h0 = h_round(acc[0]), h1 = h_round(acc[1]), h2 = h_round(acc[2]), h3 = h_round(acc[3]);
-                const float n0 = __shfl_down_sync(kFull, h0, 1), n1 = __shfl_down_sync(kFull, h1, 1);
-                const float n2 = __shfl_down_sync(kFull, h2, 1), n3 = __shfl_down_sync(kFull, h3, 1);
-                if (c == 0) {
-                    // ascending-j fp32 sum from 0.0f, then + 0 (fragment.hpp:89-92)
-                    float ra = 0.0f, rb2 = 0.0f;
-                    ra = ra + h0; ra = ra + h1; ra = ra + n0; ra = ra + n1;
-                    rb2 = rb2 + h2; rb2 = rb2 + h3; rb2 = rb2 + n2; rb2 = rb2 + n3;
-                    ra = ra + 0.0f;
-                    rb2 = rb2 + 0.0f;
-                    ovf |= !isfinite(ra) || !isfinite(rb2);
-                    if (cu0 + g < Cg) s_chunk[cu0 + g] = ra;
-                    if (cu0 + g + 8 < Cg) s_chunk[cu0 + g + 8] = rb2;
+            // Finishing MMA on the tensor core (reduction.hpp:182): A2 = binary16(C_R) in the
+            // accumulator layout (= the A-operand layout of columns k < 8), B2[k][q] = [k / m == q]
+            // -> D2[period][q] = sum_j binary16(C_R[q m + j]) for chunk slot q, all in registers.
+            {
+                float d2[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_16816(d2, pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), 0u, 0u, bfin, 0u);
+                const uint32_t cu0 = (warp + u * kGmWarps) * S.chunks_per_unit;
+                if (2 * c < S.CP) {
+                    ovf |= !isfinite(d2[0]) || !isfinite(d2[2]);
+                    const uint32_t ca = cu0 + g * S.CP + 2 * c, cb = cu0 + (g + 8) * S.CP + 2 * c;
+                    if (ca < Cg) s_chunk[ca] = d2[0];
+                    if (cb < Cg) s_chunk[cb] = d2[2];
                 }
-            } else {
-                // M == 2: lane (g, q) owns chunk slot q of periods g and g+8 (columns 2q, 2q+1)
-                if (c < S.CP) {
-                    float ra = 0.0f, rb2 = 0.0f;
-                    ra = ra + h_round(acc[0]); ra = ra + h_round(acc[1]); ra = ra + 0.0f;
-                    rb2 = rb2 + h_round(acc[2]); rb2 = rb2 + h_round(acc[3]); rb2 = rb2 + 0.0f;
-                    ovf |= !isfinite(ra) || !isfinite(rb2);
-                    const uint32_t ca = cu0 + g * S.CP + c, cb = cu0 + (g + 8) * S.CP + c;
-                    if (ca < Cg) s_chunk[ca] = ra;
-                    if (cb < Cg) s_chunk[cb] = rb2;
+                if (2 * c + 1 < S.CP) {
+                    ovf |= !isfinite(d2[1]) || !isfinite(d2[3]);
+                    const uint32_t ca = cu0 + g * S.CP + 2 * c + 1, cb = cu0 + (g + 8) * S.CP + 2 * c + 1;
+                    if (ca < Cg) s_chunk[ca] = d2[1];
+                    if (cb < Cg) s_chunk[cb] = d2[3];
                 }
             }
             acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
