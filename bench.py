@@ -10,9 +10,10 @@ rank reduces its own contiguous shard (elements [r*n, (r+1)*n) of the same globa
 scaling) and the N fp32 partials are combined with one NCCL all_reduce.  The input (2 GiB) is
 16x the 126 MB L2, so no flush is needed between steps.
 
-`e2e` repeats the measurement through the reference-facing drop-in call
-tcr_reduce_f32_host (reduce(std::span<const float>) in the reference): fp32 host data in pinned
-memory, host->device copies inside the timed region, 8-byte result read back every step.
+`e2e` repeats the measurement through the C ABI with host buffers: binary16 host data in pinned
+memory (tcr_reduce_f16_host), host->device copies inside the timed region, 8-byte result read
+back every step; `e2e.f32_dropin` does the same through the reference-facing drop-in call
+tcr_reduce_f32_host (reduce(std::span<const float>) in the reference, fp32 host data).
 
 `--impl reference` times the reference's own CPU implementation of the path (the reference
 headers compiled as-is into oracle/_ref, parallelised over blocks exactly as
@@ -40,7 +41,7 @@ N_DEFAULT = 1 << 30
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_DEFAULT, help="elements per GPU")
@@ -64,12 +65,14 @@ def peaks():
 
 class Clocks:
     """SM clock and clock-event reasons sampled DURING the timed region (the B200_PROFILING.md
-    clocks line) through NVML in-process every ~2 ms (a timed region of 20 x 0.34 ms is shorter
-    than one nvidia-smi invocation); falls back to polling nvidia-smi if NVML is unavailable."""
+    clocks line) through NVML in-process (back to back, ~0.1-1 ms apart); falls back to polling
+    nvidia-smi if NVML is unavailable.  The sampler starts before the warm-up (NVML init takes
+    tens of ms) and only the samples taken between mark_start() and mark_end() are reported."""
 
     def __init__(self, index: int):
         self.index = index
-        self.sm, self.mx, self.reasons = [], [], set()
+        self.samples = []          # (t, sm_mhz, max_mhz, reasons)
+        self.window = [None, None]
         self.stop = threading.Event()
 
     def _loop(self):
@@ -82,31 +85,28 @@ class Clocks:
                      N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
                      N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
                      N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake_slowdown"}
+            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
             while not self.stop.is_set():
-                self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
-                self.mx.append(float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)))
+                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
                 r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for bit, nm in names.items():
-                    if r & bit:
-                        self.reasons.add(nm)
-                self.stop.wait(0.002)
+                self.samples.append((time.perf_counter(), sm, mx, {nm for bit, nm in names.items() if r & bit}))
+                self.stop.wait(0.0002)
             N.nvmlShutdown()
         except Exception:
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
             while not self.stop.is_set():
                 try:
+                    t = time.perf_counter()
                     r = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
                     f = [x.strip() for x in r.stdout.strip().split(",")]
-                    self.sm.append(float(f[0]))
-                    self.mx.append(float(f[1]))
-                    for nm, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], f[2:6]):
-                        if v.lower() == "active":
-                            self.reasons.add(nm)
+                    rs = {nm for nm, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                               "sw_power_cap"], f[2:6]) if v.lower() == "active"}
+                    self.samples.append((t, float(f[0]), float(f[1]), rs))
                 except Exception:
                     pass
-                self.stop.wait(0.2)
+                self.stop.wait(0.05)
 
     def __enter__(self):
         self.t = threading.Thread(target=self._loop, daemon=True)
@@ -117,10 +117,28 @@ class Clocks:
         self.stop.set()
         self.t.join(timeout=15)
 
+    def wait_ready(self, timeout: float = 5.0):
+        t = time.perf_counter()
+        while not self.samples and time.perf_counter() - t < timeout:
+            time.sleep(0.005)
+
+    def mark_start(self):
+        self.window[0] = time.perf_counter()
+
+    def mark_end(self):
+        self.window[1] = time.perf_counter()
+
     def summary(self):
-        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
-                "sm_max_mhz": max(self.mx) if self.mx else None,
-                "reasons": sorted(self.reasons), "samples": len(self.sm)}
+        t0, t1 = self.window
+        inside = [x for x in self.samples if t0 is not None and t1 is not None and t0 <= x[0] <= t1]
+        sel = inside or self.samples[-3:]
+        reasons = set()
+        for x in sel:
+            reasons |= x[3]
+        return {"sm_mhz": statistics.median(x[1] for x in sel) if sel else None,
+                "sm_max_mhz": max(x[2] for x in sel) if sel else None,
+                "reasons": sorted(reasons), "samples": len(inside),
+                "timed_region_ms": (t1 - t0) * 1e3 if t0 is not None and t1 is not None else None}
 
 
 def cpu_reference_rate(n_sample: int, reps: int = 1):
@@ -229,18 +247,21 @@ def main():
             dist.barrier()
             torch.cuda.synchronize(dev)
 
-    for _ in range(max(args.warmup, 3)):
-        step(False)
-    launches_per_step = lib.tcr_last_launch_count()
-    engine_used = T.Engine(lib.tcr_last_engine()).name
-    barrier()
     with Clocks(local) as clk:
+        for _ in range(max(args.warmup, 3)):
+            step(False)
+        launches_per_step = lib.tcr_last_launch_count()
+        engine_used = T.Engine(lib.tcr_last_engine()).name
+        barrier()
+        clk.wait_ready()
+        clk.mark_start()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
             step(True)
         t1.record(stream)
         barrier()
+        clk.mark_end()
     ms = t0.elapsed_time(t1) / args.steps
     kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
     t = torch.tensor([ms, kms], device=dev, dtype=torch.float64)
@@ -301,41 +322,55 @@ def main():
       except Exception as exc:  # optional section: never lose the contract line
         comparators = {"error": repr(exc)}
 
-    # end-to-end through the reference-facing drop-in (host fp32 in pinned memory)
+    # end-to-end through the C ABI with HOST buffers (pinned): the binary16 host entry
+    # (tcr_reduce_f16_host: the metric's fp16 data, 2 B/element over PCIe) is the headline; the
+    # fp32 drop-in (tcr_reduce_f32_host = reduce(std::span<const float>), 4 B/element) beside it
     e2e = None
     if not args.no_e2e:
       try:
-        xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
-        xh.copy_(T.generate("uniform", 0, n, device=dev, dtype="float32", first=rank * n).cpu())
-        torch.cuda.empty_cache()
-        hp = C.c_void_p(xh.data_ptr())
-        out = _capi.tcr_outcome()
-        e2e_steps = max(3, min(args.steps, 10))
+        def time_host(fn, hp):
+            out = _capi.tcr_outcome()
+            steps = max(3, min(args.steps, 10))
 
-        def e2e_step():
-            _capi.check(lib.tcr_reduce_f32_host(hp, n, C.byref(c_cfg), C.byref(out)))
+            def step():
+                _capi.check(fn(hp, n, C.byref(c_cfg), C.byref(out)))
+                if world > 1:
+                    r = torch.tensor([out.value], device=dev)
+                    dist.all_reduce(r)
+                    r.item()
+
+            for _ in range(2):
+                step()
+            barrier()
+            s0 = time.perf_counter()
+            for _ in range(steps):
+                step()
+            barrier()
+            e_dt = (time.perf_counter() - s0) / steps
+            et = torch.tensor([e_dt], device=dev, dtype=torch.float64)
             if world > 1:
-                r = torch.tensor([out.value], device=dev)
-                dist.all_reduce(r)
-                r.item()
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            return et.item(), out.value
 
-        for _ in range(2):
-            e2e_step()
-        barrier()
-        s0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            e2e_step()
-        barrier()
-        e_dt = (time.perf_counter() - s0) / e2e_steps
-        et = torch.tensor([e_dt], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_dt = et.item()
-        e2e = {"value": world * n / e_dt / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": 4 * n,
-               "d2h_bytes_per_step": 8, "ms_per_step": e_dt * 1e3,
-               "path": "tcr_reduce_f32_host (pinned fp32 host input, pipelined H2D + fused convert/reduce)",
-               "clock": "host wall clock around synchronous calls, max over ranks"}
+        xh = torch.empty(n, dtype=torch.float16, pin_memory=True)
+        xh.copy_(x.cpu())
+        torch.cuda.empty_cache()
+        e16, v16 = time_host(lib.tcr_reduce_f16_host, C.c_void_p(xh.data_ptr()))
         del xh
+        xf = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        xf.copy_(T.generate("uniform", 0, n, device=dev, dtype="float32", first=rank * n).cpu())
+        torch.cuda.empty_cache()
+        e32, v32 = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xf.data_ptr()))
+        del xf
+        e2e = {"value": world * n / e16 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": 2 * n,
+               "d2h_bytes_per_step": 8, "ms_per_step": e16 * 1e3,
+               "path": "tcr_reduce_f16_host (pinned binary16 host input, pipelined H2D + reduce)",
+               "clock": "host wall clock around synchronous calls, max over ranks",
+               "f32_dropin": {"value": world * n / e32 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": 4 * n,
+                              "d2h_bytes_per_step": 8, "ms_per_step": e32 * 1e3,
+                              "path": "tcr_reduce_f32_host = reduce(std::span<const float>) drop-in (pinned fp32 "
+                                      "host input, pipelined H2D + fused convert/reduce)",
+                              "same_value_as_f16_host": v32 == v16}}
       except Exception as exc:
         e2e = {"error": repr(exc)}
 

@@ -107,6 +107,11 @@ int tcr_validate(const tcr_config* cfg);
  * Host->device copies are pipelined with the fused convert(RNE->binary16)+reduce kernel. */
 int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* cfg, tcr_outcome* out);
 
+/* reduce() over a HOST array of binary16 bit patterns (values already rounded to binary16, as
+ * the reference's load_fragment would produce them, fragment.hpp:62-70): same pipeline, half the
+ * host->device bytes.  Equal to tcr_reduce_f32_host on the widened values. */
+int tcr_reduce_f16_host(const uint16_t* x, size_t n, const tcr_config* cfg, tcr_outcome* out);
+
 /* Same over device-resident data (fp32 converted on load, or binary16 bits).
  * Synchronous: returns after the result (8 bytes) is back on the host. */
 int tcr_reduce_f32_device(const float* d_x, size_t n, const tcr_config* cfg, tcr_outcome* out,

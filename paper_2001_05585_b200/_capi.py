@@ -42,6 +42,7 @@ SIGNATURES = {
     "tcr_config_init": (None, [_CFG]),
     "tcr_validate": (C.c_int, [_CFG]),
     "tcr_reduce_f32_host": (C.c_int, [_P, _SZ, _CFG, _OUT]),
+    "tcr_reduce_f16_host": (C.c_int, [_P, _SZ, _CFG, _OUT]),
     "tcr_reduce_f32_device": (C.c_int, [_P, _SZ, _CFG, _OUT, _P]),
     "tcr_reduce_f16_device": (C.c_int, [_P, _SZ, _CFG, _OUT, _P]),
     "tcr_single_pass_f16_async": (C.c_int, [_P, _SZ, _CFG, _P, _P, _P]),

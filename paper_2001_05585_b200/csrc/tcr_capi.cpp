@@ -802,15 +802,19 @@ int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config
     return enqueue_sp(d_x, 0, n, &cc, false, w->result(), w->overflow(), d_blocks, w, s, 0, g.n_groups, true);
 }
 
-int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outcome* out) {
-    // Drop-in for reduce(std::span<const float>, cfg): pipelined H2D in group-aligned chunks on
-    // a copy stream, fused convert+reduce per chunk on the compute stream, one finaliser.
+namespace {
+// Host-input reduce(): pipelined H2D of group-aligned chunks on a copy stream (2-slot ring,
+// pinned or pageable source), reduce kernel per chunk on the compute stream, one finaliser.
+// f32: fp32 values converted to binary16 on the device (fused into the m = 16 kernel);
+// otherwise binary16 bit patterns (half the bytes over PCIe).
+int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outcome* out) {
     g_launches = 0;
     if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
     std::memset(out, 0, sizeof *out);
     if (!c) return fail(TCR_INVALID_ARGUMENT, "null config");
+    const size_t esz = f32 ? sizeof(float) : sizeof(uint16_t);
     if (c->variant != TCR_SINGLE_PASS) {
-        // the other variants take the whole fp32 input on the device, then the same dispatcher
+        // the other variants take the whole input on the device, then the same dispatcher
         if (c->variant < TCR_ORACLE64 || c->variant > TCR_SPLIT) return fail(TCR_INVALID_ARGUMENT, "unknown variant");
         cudaStream_t s0 = nullptr;
         Workspace* w0 = nullptr;
@@ -821,10 +825,10 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
             return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
         }
         if (!x) return fail(TCR_INVALID_ARGUMENT, "null input");
-        rc0 = ensure(&w0->stage, &w0->stage_cap, n, s0);
+        rc0 = ensure(&w0->stage, &w0->stage_cap, f32 ? n : (n + 1) / 2, s0);
         if (rc0) return rc0;
-        TCR_CUDA(cudaMemcpyAsync(w0->stage, x, n * sizeof(float), cudaMemcpyHostToDevice, s0));
-        return run_variant(w0->stage, true, n, c, out, w0, s0);
+        TCR_CUDA(cudaMemcpyAsync(w0->stage, x, n * esz, cudaMemcpyHostToDevice, s0));
+        return run_variant(w0->stage, f32, n, c, out, w0, s0);
     }
     if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
     if (!x) return fail(TCR_INVALID_ARGUMENT, "null input");
@@ -837,7 +841,7 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
     rc = get_ws(s, &w);
     if (rc) return rc;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
-    // chunk: whole groups, ~32 Mi elements (128 MiB of fp32)
+    // chunk: whole groups, ~32 Mi elements (128 MiB of fp32 / 64 MiB of binary16)
     const uint64_t groups_per_chunk = std::max<uint64_t>(1, (32ull << 20) / g.group_elems);
     const uint64_t chunk_elems = groups_per_chunk * g.group_elems;
     const uint64_t n_chunks = (g.n_groups + groups_per_chunk - 1) / groups_per_chunk;
@@ -861,21 +865,22 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
     }
     tcr_config cc = *c;
     TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+    const char* xb = static_cast<const char*>(x);
     for (uint64_t k = 0; k < n_chunks; ++k) {
         const int slot = int(k & 1);
         const uint64_t e0 = k * chunk_elems;
         const uint64_t e1 = std::min<uint64_t>(n, e0 + chunk_elems);
         const uint64_t g0 = k * groups_per_chunk;
         const uint64_t g1 = std::min<uint64_t>(g.n_groups, g0 + groups_per_chunk);
+        void* dst = f32 ? static_cast<void*>(w->ring[slot]) : static_cast<void*>(w->ring16[slot]);
         if (k >= 2) TCR_CUDA(cudaStreamWaitEvent(w->copy_stream, w->consumed[slot], 0));
-        TCR_CUDA(cudaMemcpyAsync(w->ring[slot], x + e0, (e1 - e0) * sizeof(float), cudaMemcpyHostToDevice,
-                                 w->copy_stream));
+        TCR_CUDA(cudaMemcpyAsync(dst, xb + e0 * esz, (e1 - e0) * esz, cudaMemcpyHostToDevice, w->copy_stream));
         TCR_CUDA(cudaEventRecord(w->copied[slot], w->copy_stream));
         TCR_CUDA(cudaStreamWaitEvent(s, w->copied[slot], 0));
         const bool last = (k + 1 == n_chunks);
         // single chunk: finalise in the same launch; otherwise one finaliser at the end
-        if (cc.m == 16) {
-            rc = enqueue_sp(w->ring[slot], e0, n, &cc, true, w->result(), w->overflow(), nullptr, w, s, g0, g1,
+        if (!f32 || cc.m == 16) {
+            rc = enqueue_sp(dst, e0, n, &cc, f32, w->result(), w->overflow(), nullptr, w, s, g0, g1,
                             last && n_chunks == 1);
         } else {
             TCR_CUDA(tcr::launch_convert_f32_f16(w->ring[slot], w->ring16[slot], e1 - e0, s));
@@ -898,6 +903,16 @@ int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outco
     out->overflow = o ? 1 : 0;
     counters(n, c, out);
     return TCR_OK;
+}
+}  // namespace
+
+int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outcome* out) {
+    // Drop-in for reduce(std::span<const float>, cfg)
+    return reduce_host(x, true, n, c, out);
+}
+
+int tcr_reduce_f16_host(const uint16_t* x, size_t n, const tcr_config* c, tcr_outcome* out) {
+    return reduce_host(x, false, n, c, out);
 }
 
 int tcr_generate_f16_device(uint16_t* d_x, size_t n, int32_t dist, uint64_t seed, int64_t lo, int64_t hi,

@@ -109,18 +109,25 @@ def reduce(x, cfg: ReductionConfig) -> ReductionOutcome:
     """reduce() (reduction.hpp:344-358).
 
     x may be a host float32 array (the reference's std::span<const float>: copied to the
-    device, converted to binary16 with round-to-nearest-even inside the kernel) or a CUDA
-    tensor of dtype float16 / float32 (device resident, no copy)."""
+    device, converted to binary16 with round-to-nearest-even inside the kernel), a host float16
+    array (binary16 values, half the copy bytes; same result as its float32 widening), a CPU
+    tensor of either dtype, or a CUDA tensor of dtype float16 / float32 (device resident, no copy)."""
     lib = _capi.load()
     c = cfg.to_c()
     out = _capi.tcr_outcome()
-    if isinstance(x, np.ndarray) or isinstance(x, (list, tuple)):
-        a = np.ascontiguousarray(x, dtype=np.float32)
-        _capi.check(lib.tcr_reduce_f32_host(a.ctypes.data_as(C.c_void_p), a.size, C.byref(c), C.byref(out)))
-        return ReductionOutcome.from_c(out)
     import torch
-    if not isinstance(x, torch.Tensor) or not x.is_cuda:
-        raise TypeError("x must be a host float32 array or a CUDA tensor")
+    if isinstance(x, torch.Tensor) and not x.is_cuda:
+        x = x.contiguous().numpy()
+    if isinstance(x, np.ndarray) or isinstance(x, (list, tuple)):
+        if isinstance(x, np.ndarray) and x.dtype == np.float16:
+            a = np.ascontiguousarray(x)
+            _capi.check(lib.tcr_reduce_f16_host(a.ctypes.data_as(C.c_void_p), a.size, C.byref(c), C.byref(out)))
+        else:
+            a = np.ascontiguousarray(x, dtype=np.float32)
+            _capi.check(lib.tcr_reduce_f32_host(a.ctypes.data_as(C.c_void_p), a.size, C.byref(c), C.byref(out)))
+        return ReductionOutcome.from_c(out)
+    if not isinstance(x, torch.Tensor):
+        raise TypeError("x must be a host float16/float32 array or a tensor")
     x = x.contiguous()
     if x.dtype == torch.float16:
         fn = lib.tcr_reduce_f16_device

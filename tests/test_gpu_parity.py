@@ -231,8 +231,9 @@ def test_fp32_device_and_host_paths(oracle):
         a = T.reduce(to_dev_f16(h), cfg16(R=2, B=512))
         b = T.reduce(torch.from_numpy(x).to(DEV), cfg16(R=2, B=512))
         c = T.reduce(x, cfg16(R=2, B=512))  # host fp32 drop-in path
-        assert a.value == b.value == c.value
-        assert a.atomic_count == c.atomic_count
+        d = T.reduce(h.view(np.float16), cfg16(R=2, B=512))  # host binary16 path
+        assert a.value == b.value == c.value == d.value
+        assert a.atomic_count == c.atomic_count == d.atomic_count
 
 
 def test_host_path_multi_chunk(oracle):
@@ -240,10 +241,23 @@ def test_host_path_multi_chunk(oracle):
     h = np.array(x.astype(np.float16).view(np.uint16))
     a = T.reduce(x, cfg16())
     b = T.reduce(to_dev_f16(h), cfg16())
-    assert a.value == b.value
+    c = T.reduce(h.view(np.float16), cfg16())
+    assert a.value == b.value == c.value
     a = T.reduce(x, cfg16(finalize=T.Finalize.ordered))
     ref = oracle.single_pass(h, threads=8, m=16, R=1, B=1024)
     assert abs(a.value - ref.value) / abs(ref.value) < 1e-6
+
+
+@pytest.mark.parametrize("m,R,B", [(4, 1, 128), (2, 3, 64), (8, 5, 32), (32, 2, 96), (256, 1, 32)])
+@pytest.mark.parametrize("variant", ["single_pass", "recurrence", "split", "shuffle32"])
+def test_host_f16_path_equals_device(oracle, m, R, B, variant):
+    """tcr_reduce_f16_host (binary16 host input) == the device path on the same values, every m
+    and variant (multi-chunk pipeline at 2^25 + 7 elements)."""
+    h = oracle.generate_f16("normal", 2, (1 << 25) + 7)
+    cfg = T.ReductionConfig(variant=T.Variant[variant], m=m, R=R, B=B)
+    a = T.reduce(h.view(np.float16), cfg)
+    b = T.reduce(to_dev_f16(h), cfg)
+    assert a.value == b.value and a.overflow == b.overflow and a.mma_count == b.mma_count
 
 
 def test_errors():
