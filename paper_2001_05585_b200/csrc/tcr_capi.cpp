@@ -383,11 +383,11 @@ uint64_t levels_of(uint64_t n) {  // pairwise_tree levels of a pow2-padded lengt
 // shuffle32 (:113-122) / half_tree (:126-151): bit-exact strided pairwise tree.
 int run_tree(const void* d_x, bool f32, uint64_t n, bool half, tcr_outcome* out, Workspace* w, cudaStream_t s) {
     if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
-    int rc = ensure(&w->tree_cols, &w->tree_cap, tcr::tree_cols_needed(), s);
+    int rc = ensure(&w->tree_cols, &w->tree_cap, tcr::tree_cols_needed(n), s);
     if (rc) return rc;
     TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
     TCR_CUDA(tcr::launch_pairwise_tree(d_x, f32, n, half, w->tree_cols, w->var_result(), w->overflow(), s));
-    g_launches += 2;
+    g_launches += tcr::tree_launches(n);
     float v;
     uint32_t o;
     rc = sync_read(&v, w->var_result(), 4, w, s);
@@ -449,13 +449,14 @@ int run_recurrence(const void* d_x, bool f32, uint64_t n0, const tcr_config* c, 
     bool cur_f32 = f32;
     uint64_t n = n0;
     int nb = 0;
+    // the overflow flag accumulates (OR) over the levels on the device: one read at the end
+    TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
     while (n >= group) {
         const uint64_t count = (n + chunk - 1) / chunk;
         int rc = ensure(&w->lvl_f32, &w->lvl_f32_cap, count, s);
         if (rc) return rc;
         rc = ensure(&w->lvl16[nb], &w->lvl16_cap[nb], count, s);
         if (rc) return rc;
-        TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
         const tcr::SpGeometry g = tcr::make_geometry(n, cb.m, cb.R, cb.B);
         if (cur_f32 && cb.m != 16) {
             rc = ensure(&w->conv, &w->conv_cap, n, s);
@@ -468,10 +469,6 @@ int run_recurrence(const void* d_x, bool f32, uint64_t n0, const tcr_config* c, 
         if (rc) return rc;
         TCR_CUDA(tcr::launch_round_level(w->lvl_f32, w->lvl16[nb], count, w->overflow(), s));
         ++g_launches;
-        uint32_t o;
-        rc = sync_read(&o, w->overflow(), 4, w, s);
-        if (rc) return rc;
-        ovf_any |= o;
         cur = w->lvl16[nb];
         cur_f32 = false;
         nb ^= 1;
@@ -479,6 +476,12 @@ int run_recurrence(const void* d_x, bool f32, uint64_t n0, const tcr_config* c, 
         ++out->level_count;
         out->sim_steps += 2ull * c->R + 3;
         out->mma_count += count * (c->R + 1ull);
+    }
+    {
+        uint32_t o;
+        int rc = sync_read(&o, w->overflow(), 4, w, s);
+        if (rc) return rc;
+        ovf_any |= o;
     }
     if (n == 1) {
         if (cur_f32) {

@@ -101,7 +101,8 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s);
 
 // Variants (tcr_variants.cu): bit-exact strided pairwise trees (shuffle32 / half_tree), binary64
 // sum (oracle64), and the recurrence level rounding.
-uint64_t tree_cols_needed();
+uint64_t tree_cols_needed(uint64_t n);
+int tree_launches(uint64_t n);
 cudaError_t launch_pairwise_tree(const void* x, bool f32, uint64_t n, bool half, float* cols, float* out,
                                  uint32_t* ovf, cudaStream_t s);
 cudaError_t launch_dsum(const void* x, bool f32, uint64_t n, double* partials, uint32_t* ticket, double* out,

@@ -29,11 +29,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--precision", action="store_true")
+    ap.add_argument("--variants", action="store_true")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     args = ap.parse_args()
-    if not (args.sweep or args.precision):
-        args.sweep = args.precision = True
+    if not (args.sweep or args.precision or args.variants):
+        args.sweep = args.precision = args.variants = True
 
     import torch
 
@@ -113,6 +114,32 @@ def main():
         best = min(pts, key=lambda p: p["ms"])
         out["sweep"]["best"] = best
         out["sweep"]["speedup_best_vs_warp_shuffle"] = comps["warp_shuffle_fp32"] / best["ms"]
+        del x
+        torch.cuda.empty_cache()
+
+    if args.variants:
+        # every reduce() variant (reduction.hpp:344-358) through the synchronous device call
+        # (kernels + the 8-byte result read), n = 2^30 uniform s0, value checked against the exact sum
+        n = 1 << 30
+        x = T.generate("uniform", 0, n, device=dev)
+        exact, _ = T.exact_sum(x)
+        xp = C.c_void_p(x.data_ptr())
+        vpts = []
+        for name, kw in (("single_pass", dict(m=16, R=1, B=1024)), ("single_pass", dict(m=4, R=1, B=128)),
+                         ("recurrence", dict(m=16, R=5, B=32)), ("recurrence", dict(m=4, R=1, B=32)),
+                         ("split", dict(m=16, R=1, B=128, f=0.5)), ("split", dict(m=16, R=1, B=1024, f=0.9)),
+                         ("shuffle32", dict()), ("half_tree", dict()), ("oracle64", dict())):
+            cfg = T.ReductionConfig(variant=T.Variant[name], **kw)
+            c = cfg.to_c()
+            o = _capi.tcr_outcome()
+            fn = lambda: _capi.check(lib.tcr_reduce_f16_device(xp, n, C.byref(c), C.byref(o), sp))  # noqa: E731
+            med, best = time_fn(fn, max(3, args.reps // 2))
+            vpts.append({"variant": name, **kw, "ms": med, "gelem_s": n / med / 1e6, "gb_s": 2 * n / med / 1e6,
+                         "frac_hbm": 2 * n / med / 1e6 / peak, "value": o.value, "overflow": bool(o.overflow),
+                         "rel_err_exact": abs(o.value - exact) / abs(exact), "launches": lib.tcr_last_launch_count()})
+            print(json.dumps(vpts[-1]), flush=True)
+        out["variants"] = {"n": n, "dist": "uniform s0", "exact": exact, "points": vpts,
+                           "timing": "CUDA events around 5 back-to-back synchronous tcr_reduce_f16_device calls"}
         del x
         torch.cuda.empty_cache()
 
