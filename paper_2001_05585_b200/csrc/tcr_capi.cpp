@@ -82,6 +82,9 @@ struct Workspace {
     size_t ring_cap = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    // split variant: the shuffle32 share on an auxiliary stream
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
 
     float* result() { return reinterpret_cast<float*>(fixed); }
     uint32_t* overflow() { return reinterpret_cast<uint32_t*>(fixed + 4); }
@@ -524,7 +527,9 @@ int run_recurrence(const void* d_x, bool f32, uint64_t n0, const tcr_config* c, 
     return TCR_OK;
 }
 
-// split (:298-341): tensor share at R = 1 through single_pass, the rest through shuffle32.
+// split (:298-341): tensor share at R = 1 through single_pass, the rest through shuffle32 --
+// the two shares run CONCURRENTLY (the tree on an auxiliary stream forked from and joined back
+// into the caller's), as the paper's variant #3 intends; one host read.
 int run_split(const void* d_x, bool f32, uint64_t n, const tcr_config* c, tcr_outcome* out, Workspace* w,
               cudaStream_t s) {
     if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
@@ -535,27 +540,61 @@ int run_split(const void* d_x, bool f32, uint64_t n, const tcr_config* c, tcr_ou
     const uint64_t chunk_block = uint64_t(c->m) * c->m * (c->B / 32);
     uint64_t tensor_len = uint64_t(c->f * double(n));
     tensor_len = tensor_len / chunk_block * chunk_block;
-    tcr_outcome t{}, sh{};
-    float tensor_part = 0.0f, shuffle_part = 0.0f;
-    if (tensor_len > 0) {
-        int rc = run_single_pass(d_x, f32, tensor_len, &tc, &t, w, s);
+    const uint64_t tree_len = n - tensor_len;
+    int launches = 0;
+    if (tree_len > 0) {
+        int rc = ensure(&w->tree_cols, &w->tree_cap, tcr::tree_cols_needed(tree_len), s);
         if (rc) return rc;
-        tensor_part = float(t.value);
+        if (!w->aux_stream) {
+            TCR_CUDA(cudaStreamCreateWithFlags(&w->aux_stream, cudaStreamNonBlocking));
+            TCR_CUDA(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
+            TCR_CUDA(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
+        }
+    }
+    TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
+    if (tensor_len > 0) {
+        int rc = sp_async(d_x, tensor_len, &tc, f32, w->result(), w->overflow(), s);
+        if (rc) return rc;
+        launches += g_launches;
+    }
+    if (tree_len > 0) {
+        TCR_CUDA(cudaEventRecord(w->fork, s));
+        TCR_CUDA(cudaStreamWaitEvent(w->aux_stream, w->fork, 0));
+        const char* base = static_cast<const char*>(d_x) + tensor_len * (f32 ? 4 : 2);
+        TCR_CUDA(tcr::launch_pairwise_tree(base, f32, tree_len, false, w->tree_cols, w->var_result(), w->sink(),
+                                           w->aux_stream));
+        launches += tcr::tree_launches(tree_len);
+        TCR_CUDA(cudaEventRecord(w->join, w->aux_stream));
+        TCR_CUDA(cudaStreamWaitEvent(s, w->join, 0));
+    }
+    g_launches = launches;
+    unsigned char h[32];
+    int rc = sync_read(h, w->fixed, 32, w, s);
+    if (rc) return rc;
+    float tensor_part = 0.0f, shuffle_part = 0.0f;
+    uint32_t ovf = 0;
+    std::memcpy(&tensor_part, h, 4);
+    std::memcpy(&ovf, h + 4, 4);
+    std::memcpy(&shuffle_part, h + 24, 4);
+    tcr_outcome t{}, sh{};
+    if (tensor_len > 0) {
+        counters(tensor_len, &tc, &t);
+        t.overflow = ovf ? 1 : 0;
         out->level_count = 1;
     }
-    if (tensor_len < n) {
-        const char* base = static_cast<const char*>(d_x) + tensor_len * (f32 ? 4 : 2);
-        int rc = run_tree(base, f32, n - tensor_len, false, &sh, w, s);
-        if (rc) return rc;
-        shuffle_part = float(sh.value);
+    if (tree_len > 0) {
+        const uint64_t lv = levels_of(tree_len);
+        sh.level_count = lv;
+        sh.sim_steps = 4 * lv;
+        sh.shuffle_count = (1ull << lv) - 1;
         out->shuffle_count = sh.shuffle_count;
         out->level_count = std::max<uint64_t>(out->level_count, sh.level_count);
     }
     if (tensor_len == 0) out->value = shuffle_part;
-    else if (tensor_len == n) out->value = tensor_part;
+    else if (tree_len == 0) out->value = tensor_part;
     else out->value = tensor_part + shuffle_part;
     out->overflow = t.overflow;
-    out->sim_steps = std::max(t.sim_steps, sh.sim_steps) + ((tensor_len > 0 && tensor_len < n) ? 1 : 0);
+    out->sim_steps = std::max(t.sim_steps, sh.sim_steps) + ((tensor_len > 0 && tree_len > 0) ? 1 : 0);
     out->mma_count = t.mma_count;
     out->atomic_count = t.atomic_count;
     out->shuffle_count += t.shuffle_count;
