@@ -18,6 +18,8 @@
 //                 accumulated over the chunk's R*(m/16)^2 tiles.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "tcr_device.cuh"
 #include "tcr_kernels.h"
 #include "tcr_pipeline.cuh"
@@ -491,6 +493,123 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
 }
 
+// ============================================ wide fragments, m = 256 SL (SL <= 8): CTA per chunk
+// The whole CTA reduces one chunk at a time: warp w streams the contiguous rows
+// [w R m / 8, (w + 1) R m / 8) of the chunk (each row = SL 512-byte tiles, one HMMA pair per tile
+// into the slab's accumulators -- 8 SL registers), so every chunk keeps 8 warps busy and every
+// warp reads one contiguous range.  At the chunk end the 8 warp partials of each column are added
+// in warp order (fixed), rounded to binary16 (reduction.hpp:179-181) and summed by a fixed
+// lane-then-warp tree into the chunk result (the finishing MMA's sum, :182; binary16 partials of
+// similar magnitude add exactly in fp32, so the order rarely matters).
+template <int SL>
+__global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams p, const uint32_t m) {
+    constexpr int D = kGmTrDepth;
+    extern __shared__ __align__(128) unsigned char s_ring[];   // ring | part[8][m] | tables
+    __shared__ float s_scratch[32];
+    __shared__ float s_wsum[kGmWarps];
+    __shared__ int s_last;
+    float* s_part = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
+    float* s_chunk = s_part + kGmWarps * m;
+    const uint32_t Cg = p.G * p.W;
+    float* s_block = s_chunk + Cg;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned g = lane >> 2, c = lane & 3u;
+    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    const uint64_t rows = uint64_t(p.R) * m;
+    const uint64_t chunk_el = rows * m;
+    const uint64_t span = rows / kGmWarps * m;                  // elements of this warp per chunk
+    const uint64_t w_off = uint64_t(warp) * span;
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint32_t blo0 = sel2(2 * c == g, 2 * c + 1 == g), blo1 = sel2(2 * c + 8 == g, 2 * c + 9 == g);
+    const uint32_t bhi0 = sel2(2 * c == g + 8, 2 * c + 1 == g + 8), bhi1 = sel2(2 * c + 8 == g + 8, 2 * c + 9 == g + 8);
+    auto swz = [](uint32_t k, uint32_t h) { return 32u * k + 16u * (h ^ ((k >> 2) & 1u)); };
+    const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_off = swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+    bool ovf = false;
+
+    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+        const uint64_t gel0 = gi * uint64_t(Cg) * chunk_el;
+        uint32_t iit = 0, islot = 0;
+        uint64_t ioff = 0;                                         // issue cursor (chunk, offset)
+        auto issue = [&]() {
+            if (iit < Cg) {
+                const uint64_t e = gel0 + uint64_t(iit) * chunk_el + w_off + ioff + 8u * lane;
+                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                cp16(ring + islot * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+                ioff += 256u;
+                if (ioff == span) {
+                    ioff = 0;
+                    ++iit;
+                }
+            }
+            cp_commit();
+            islot = islot + 1 == uint32_t(D) ? 0 : islot + 1;
+        };
+#pragma unroll 1
+        for (int f = 0; f < D - 1; ++f) issue();
+        uint32_t cslot = 0;
+        for (uint32_t it = 0; it < Cg; ++it) {
+            float acc[SL][2][4];
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[sl][0][q] = acc[sl][1][q] = 0.f;
+            for (uint64_t r = 0; r < rows / kGmWarps; ++r) {
+#pragma unroll
+                for (int sl = 0; sl < SL; ++sl) {
+                    issue();
+                    cp_wait<D - 1>();
+                    __syncwarp();
+                    uint32_t d0, d1, d2, d3;
+                    ldsm4t(ring + cslot * 512u + ld_off, d0, d1, d2, d3);
+                    __syncwarp();
+                    cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
+                    mma_16816(acc[sl][0], d0, d1, d2, d3, blo0, blo1);
+                    mma_16816(acc[sl][1], d0, d1, d2, d3, bhi0, bhi1);
+                }
+            }
+            // warp partials: D[j16][n] = column 256 sl + 16 n + j16 (n + 8 for the hi half)
+            float* part = s_part + warp * m;
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t col0 = 256u * sl + 128u * hh;
+                    part[col0 + 16 * (2 * c) + g] = acc[sl][hh][0];
+                    part[col0 + 16 * (2 * c + 1) + g] = acc[sl][hh][1];
+                    part[col0 + 16 * (2 * c) + g + 8] = acc[sl][hh][2];
+                    part[col0 + 16 * (2 * c + 1) + g + 8] = acc[sl][hh][3];
+                }
+            __syncthreads();
+            float t = 0.0f;
+            for (uint32_t col = threadIdx.x; col < m; col += kGmThreads) {
+                float cs = 0.0f;
+#pragma unroll
+                for (int w = 0; w < kGmWarps; ++w) cs = cs + s_part[w * m + col];
+                t = t + h_round(cs);
+            }
+            t = warp_tree_xor(t);
+            if (lane == 0) s_wsum[warp] = t;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                float r = 0.0f;
+#pragma unroll
+                for (int w = 0; w < kGmWarps; ++w) r = r + s_wsum[w];
+                r = r + 0.0f;
+                ovf |= !isfinite(r);
+                s_chunk[it] = r;
+            }
+        }
+        cp_wait<0>();
+        group_epilogue(p, gi, s_chunk, s_block);
+    }
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+    __threadfence();
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
+}
+
 uint32_t gcd32(uint32_t a, uint32_t b) {
     while (b) {
         const uint32_t t = a % b;
@@ -590,7 +709,17 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) 
     }
     if (g.m >= 256) {
         if (!wide_ok(g)) return cudaErrorInvalidValue;
-        return launch_gm(gm_wide_kernel, kGmWarps * kGmTrDepth * 512u + tables, groups, p, g.m, s);
+        const uint32_t ring = kGmWarps * kGmTrDepth * 512u;
+        if (g.m <= 2048 && !std::getenv("TCR_GM_WIDE_WARP")) {   // knob: profiling A/B
+            const uint32_t dyn = ring + kGmWarps * g.m * 4u + tables;
+            switch (g.m) {
+            case 256: return launch_gm(gm_wide_cta_kernel<1>, dyn, groups, p, g.m, s);
+            case 512: return launch_gm(gm_wide_cta_kernel<2>, dyn, groups, p, g.m, s);
+            case 1024: return launch_gm(gm_wide_cta_kernel<4>, dyn, groups, p, g.m, s);
+            default: return launch_gm(gm_wide_cta_kernel<8>, dyn, groups, p, g.m, s);
+            }
+        }
+        return launch_gm(gm_wide_kernel, ring + tables, groups, p, g.m, s);
     }
     TrShape S;
     if (!tr_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
