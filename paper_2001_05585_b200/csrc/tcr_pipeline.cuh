@@ -242,6 +242,49 @@ __device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t ti
     range_trees_blocks(p, tile * p.G, p.G, chunks, blocks, w, nwarps);
 }
 
+// Adjacent pairwise tree ((v0 + v1) + (v2 + v3)) ... over the `seg` (power of two) values
+// ld(base), ..., ld(base + seg - 1): compile-time register trees up to 128 values (no
+// local-memory stack), a binary-counter stack beyond.
+template <int SEG, typename LD>
+__device__ __forceinline__ float static_segment_tree(LD ld, uint32_t base) {
+    float v[SEG];
+#pragma unroll
+    for (int i = 0; i < SEG; ++i) v[i] = ld(base + i);
+#pragma unroll
+    for (int len = SEG; len > 1; len >>= 1)
+#pragma unroll
+        for (int i = 0; i < len / 2; ++i) v[i] = v[2 * i] + v[2 * i + 1];
+    return v[0];
+}
+
+template <typename LD>
+__device__ __forceinline__ float lane_segment_tree(LD ld, uint32_t base, uint32_t seg) {
+    switch (seg) {
+    case 1: return ld(base);
+    case 2: return static_segment_tree<2>(ld, base);
+    case 4: return static_segment_tree<4>(ld, base);
+    case 8: return static_segment_tree<8>(ld, base);
+    case 16: return static_segment_tree<16>(ld, base);
+    case 32: return static_segment_tree<32>(ld, base);
+    case 64: return static_segment_tree<32>(ld, base) + static_segment_tree<32>(ld, base + 32);
+    case 128: {
+        const float a = static_segment_tree<32>(ld, base) + static_segment_tree<32>(ld, base + 32);
+        const float b = static_segment_tree<32>(ld, base + 64) + static_segment_tree<32>(ld, base + 96);
+        return a + b;
+    }
+    default: {
+        float stk[24];
+        int top = 0;
+        for (uint32_t i = 0; i < seg; ++i) {
+            float v = ld(base + i);
+            for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
+            stk[top++] = v;
+        }
+        return stk[0];
+    }
+    }
+}
+
 // Group stage: adjacent tree over the G (power of two) block results of group `tile`, by one
 // warp: each lane a contiguous segment (streaming binary-counter stack), then the xor tree
 // across lanes.  GLOBAL: `blocks` lives in global memory written by other CTAs (L2 loads).
@@ -256,20 +299,7 @@ __device__ __forceinline__ void tile_tree_group(const SpParams& p, uint64_t tile
         else return blocks[i];
     };
     float x = 0.0f;
-    if (lane * seg < G) {
-        if (seg == 1) {
-            x = ld(lane);
-        } else {
-            float stk[16];
-            int top = 0;
-            for (uint32_t i = 0; i < seg; ++i) {
-                float v = ld(lane * seg + i);
-                for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
-                stk[top++] = v;
-            }
-            x = stk[0];
-        }
-    }
+    if (lane * seg < G) x = lane_segment_tree(ld, lane * seg, seg);
     x = warp_tree_xor(x);
     if (lane == 0) p.group_partials[tile] = x;
 }

@@ -67,16 +67,7 @@ __device__ __forceinline__ void group_tree_any(const SpParams& p, uint64_t gi, c
     if (!p.group_partials) return;
     const uint32_t seg = G >= 32 ? G / 32 : 1;
     float acc = 0.0f;
-    if (lane * seg < G) {
-        float stk[16];
-        int top = 0;
-        for (uint32_t i = 0; i < seg; ++i) {
-            float v = blocks[lane * seg + i];
-            for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
-            stk[top++] = v;
-        }
-        acc = stk[0];
-    }
+    if (lane * seg < G) acc = lane_segment_tree([&](uint32_t i) { return blocks[i]; }, lane * seg, seg);
     acc = warp_tree_xor(acc);
     if (lane == 0) p.group_partials[gi] = acc;
 }
