@@ -845,6 +845,19 @@ int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config
 }
 
 namespace {
+// Host-input calls run on a per-thread, per-device stream, so concurrent callers on different
+// host threads get separate workspaces (the reference's reduce() is reentrant,
+// reduction.hpp:19-21).
+int host_stream(cudaStream_t* out) {
+    thread_local std::map<int, cudaStream_t> streams;
+    int dev = 0;
+    TCR_CUDA(cudaGetDevice(&dev));
+    auto& st = streams[dev];
+    if (!st) TCR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    *out = st;
+    return TCR_OK;
+}
+
 // Host-input reduce(): pipelined H2D of group-aligned chunks on a copy stream (2-slot ring,
 // pinned or pageable source), reduce kernel per chunk on the compute stream, one finaliser.
 // f32: fp32 values converted to binary16 on the device (fused into the m = 16 kernel);
@@ -859,8 +872,10 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
         // the other variants take the whole input on the device, then the same dispatcher
         if (c->variant < TCR_ORACLE64 || c->variant > TCR_SPLIT) return fail(TCR_INVALID_ARGUMENT, "unknown variant");
         cudaStream_t s0 = nullptr;
+        int rc0 = host_stream(&s0);
+        if (rc0) return rc0;
         Workspace* w0 = nullptr;
-        int rc0 = get_ws(s0, &w0);
+        rc0 = get_ws(s0, &w0);
         if (rc0) return rc0;
         if (n == 0) {
             if (c->variant == TCR_ORACLE64) return TCR_OK;
@@ -878,7 +893,9 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
     if (rc) return rc;
     rc = check_supported(c);
     if (rc) return rc;
-    cudaStream_t s = nullptr;  // legacy default stream of the calling thread's device
+    cudaStream_t s = nullptr;
+    rc = host_stream(&s);
+    if (rc) return rc;
     Workspace* w = nullptr;
     rc = get_ws(s, &w);
     if (rc) return rc;
@@ -889,7 +906,8 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
     const uint64_t n_chunks = (g.n_groups + groups_per_chunk - 1) / groups_per_chunk;
     const uint64_t ring_elems = std::min<uint64_t>(chunk_elems, n);
     if (w->ring_cap < ring_elems) {
-        TCR_CUDA(cudaDeviceSynchronize());
+        TCR_CUDA(cudaStreamSynchronize(s));
+        if (w->copy_stream) TCR_CUDA(cudaStreamSynchronize(w->copy_stream));
         for (auto& r : w->ring)
             if (r) TCR_CUDA(cudaFree(r));
         for (auto& r : w->ring) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(float)));

@@ -601,3 +601,41 @@ def test_split_units_identical(oracle, R, B, monkeypatch):
     monkeypatch.setenv("TCR_SPLIT", "4")
     assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
     assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
+
+
+# --------------------------------------------------------------------------- reentrancy (reduction.hpp:19-21)
+
+def test_concurrent_host_threads(oracle):
+    """reduce() is reentrant: host threads calling the host-buffer and device paths at the same
+    time (own CUDA streams) get exactly the serial results."""
+    import threading
+    cases = []
+    for i, (m, R, B) in enumerate([(16, 1, 1024), (4, 1, 128), (16, 4, 128), (8, 3, 64)]):
+        h = oracle.generate_f16("normal", 10 + i, (1 << 22) + 17 * i)
+        cfg = T.ReductionConfig(m=m, R=R, B=B)
+        cases.append((h, cfg, T.reduce(h.view(np.float16), cfg).value))
+    errors = []
+
+    def worker(k):
+        try:
+            st = torch.cuda.Stream(device=DEV)
+            for rep in range(6):
+                h, cfg, want = cases[(k + rep) % len(cases)]
+                if rep % 3 == 0:
+                    got = T.reduce(h.view(np.float16), cfg).value
+                elif rep % 3 == 1:
+                    got = T.reduce(h.view(np.float16).astype(np.float32), cfg).value
+                else:
+                    with torch.cuda.stream(st):
+                        got = T.reduce(to_dev_f16(h), cfg).value
+                if got != want:
+                    errors.append((k, rep, got, want))
+        except Exception as exc:  # noqa: BLE001
+            errors.append((k, repr(exc)))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
