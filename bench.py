@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT, help="elements per GPU")
+    ap.add_argument("--n", "--elems", dest="n", type=int, default=N_DEFAULT,
+                    help="elements per GPU (spell it --elems under torchrun: --n is ambiguous there)")
     ap.add_argument("--m", type=int, default=16, help="fragment side (16 = the hardware fragment)")
     ap.add_argument("--R", type=int, default=1)
     ap.add_argument("--B", type=int, default=1024)
@@ -211,10 +212,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (tests/test_gpu_parity.py::test_bench_two_ranks_one_gpu): every rank on cuda:0
+    # with gloo, to exercise the N > 1 code path of this script on a 1-GPU box
+    one_dev = os.environ.get("TCR_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     lib = _capi.load()
     n = args.n
     cfg = T.ReductionConfig(m=args.m, R=args.R, B=args.B, engine=T.Engine(args.engine))
@@ -362,12 +371,12 @@ def main():
         torch.cuda.empty_cache()
         e32, v32 = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xf.data_ptr()))
         del xf
-        e2e = {"value": world * n / e16 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": 2 * n,
-               "d2h_bytes_per_step": 8, "ms_per_step": e16 * 1e3,
+        e2e = {"value": world * n / e16 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": world * 2 * n,
+               "d2h_bytes_per_step": world * 8, "ms_per_step": e16 * 1e3,
                "path": "tcr_reduce_f16_host (pinned binary16 host input, pipelined H2D + reduce)",
                "clock": "host wall clock around synchronous calls, max over ranks",
-               "f32_dropin": {"value": world * n / e32 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": 4 * n,
-                              "d2h_bytes_per_step": 8, "ms_per_step": e32 * 1e3,
+               "f32_dropin": {"value": world * n / e32 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": world * 4 * n,
+                              "d2h_bytes_per_step": world * 8, "ms_per_step": e32 * 1e3,
                               "path": "tcr_reduce_f32_host = reduce(std::span<const float>) drop-in (pinned fp32 "
                                       "host input, pipelined H2D + fused convert/reduce)",
                               "same_value_as_f16_host": v32 == v16}}

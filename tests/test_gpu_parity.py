@@ -639,3 +639,24 @@ def test_concurrent_host_threads(oracle):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_bench_two_ranks_one_gpu(tmp_path):
+    """bench.py's N > 1 path (torchrun, per-rank shards, all_reduce combine, max over ranks,
+    one JSON line from rank 0) on one GPU: both ranks on cuda:0 over gloo."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TCR_BENCH_ONE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533", "bench.py", "--gpus", "2", "--steps", "5",
+           "--warmup", "3", "--elems", str(1 << 26), "--no-cpu", "--no-comparators"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["n_total"] == 2 << 26 and d["value"] > 0
+    # both shards of the global uniform stream, combined: within the single-GPU tolerance
+    assert d["rel_err_vs_exact"] < 1e-5
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 2 * 2 * (1 << 26)
