@@ -85,7 +85,7 @@ __device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, f
 // chunk of R rows; m = 2: CP = 4 / gcd(4, R) chunks, which may straddle rows).  A row i of an
 // MMA = row rho of period i, so a unit = 16 periods and the chain over the PR rows of a period
 // accumulates in D with B[k][n] = [element 16 rho + k of the period is column j of chunk slot
-// q, n = q m + j].  Stages: row blocks of RB (a power of two <= 16) rows of all 16 periods.
+// q, n = q m + j].  Stages: row blocks of RB = min(PR, 16) rows of all 16 periods.
 struct NatShape {
     uint32_t PR, CP;           // rows and chunks per period
     uint32_t RB;               // rows per stage
@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
     // Stage layout: 16-byte unit u = 2 (period * rb + row) + half, stored at u ^ (period & 7)
     // (a bijection for rb a power of two; the 8 periods of one ldmatrix phase hit 8 bank groups).
     const uint32_t rho8 = (lane & 7u) + 8u * ((lane >> 3) & 1u), half = lane >> 4;
+    // generic path, full row blocks of RB rows: this lane's first piece and the per-row step
+    const uint32_t gper0 = lane / (2u * RB), grr0 = lane % (2u * RB), gdq = 32u / (2u * RB), gdr = 32u % (2u * RB);
     bool ovf = false;
 
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
@@ -146,17 +148,29 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
                 const uint32_t r0 = iblk * RB, rb = RBC ? uint32_t(RBC) : min(RB, PR - r0);
                 const uint64_t e_unit = gel0 + uint64_t(warp + iu * kGmWarps) * 16u * period_el + r0 * 16u;
                 const uint32_t dst = ring + islot * stage_bytes;
+                // piece = lane + 32 t = per * 2 rb + rr: compile-time shifts on the fast path,
+                // one division per stage then increments on the generic one (any rb <= 16)
+                const bool last = !RBC && rb != RB;
+                uint32_t per = RBC ? lane / (2u * RBC) : (last ? lane / (2u * rb) : gper0);
+                uint32_t rr = RBC ? lane % (2u * RBC) : (last ? lane % (2u * rb) : grr0);
+                const uint32_t dq = RBC ? 32u / (2u * RBC) : (last ? 32u / (2u * rb) : gdq);
+                const uint32_t dr = RBC ? 32u % (2u * RBC) : (last ? 32u % (2u * rb) : gdr);
 #pragma unroll
                 for (uint32_t t = 0; t < (RBC ? uint32_t(RBC) : 16u); ++t) {
                     if (!RBC && t >= rb) break;
                     const uint32_t piece = lane + 32u * t;
-                    const uint32_t per = piece / (2u * rb), rr = piece % (2u * rb);   // shifts: rb pow2
                     const uint64_t e = e_unit + per * period_el + rr * 8u;
                     if (full) {
                         cp16(dst + ((piece ^ (per & 7u)) * 16u), x + e, 16u);
                     } else {
                         const uint32_t bytes = e + 8 <= lim ? 16u : (e < lim ? uint32_t(lim - e) * 2u : 0u);
                         cp16(dst + ((piece ^ (per & 7u)) * 16u), x + (e < lim ? e : 0), bytes);
+                    }
+                    per += dq;
+                    rr += dr;
+                    if (rr >= 2u * rb) {
+                        rr -= 2u * rb;
+                        ++per;
                     }
                 }
                 if (++iblk == nblk) {
@@ -619,9 +633,7 @@ bool nat_shape(uint32_t m, uint32_t R, uint32_t Cg, NatShape* S) {
     S->PR = uint32_t(period / 16);
     S->CP = uint32_t(period / ce);
     if (S->CP * m > 8) return false;                     // N = 8 selector columns
-    uint32_t rb = 1;
-    while (rb * 2 <= S->PR && rb < 16) rb *= 2;
-    S->RB = rb;
+    S->RB = S->PR < 16 ? S->PR : 16;                    // rows per stage (any count <= 16)
     S->chunks_per_unit = 16 * S->CP;
     if (Cg % S->CP) return false;                        // groups start on a period
     return true;
@@ -685,7 +697,7 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) 
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
         void (*fn)(SpParams, NatShape) = nullptr;
         int nd = 2;
-        const bool fast = S.PR == S.RB;   // PR a power of two <= 16: one stage per unit
+        const bool fast = S.PR == S.RB && (S.RB & (S.RB - 1)) == 0;   // PR a power of two <= 16
 #define TCR_NAT(MV, RBV) \
     { fn = gm_nat_kernel<MV, RBV>; nd = nat_depth<RBV>(); }
         if (g.m == 2) {

@@ -125,9 +125,14 @@ def main():
         exact, _ = T.exact_sum(x)
         xp = C.c_void_p(x.data_ptr())
         vpts = []
+        # the north-star config, the reference's defaults (m = 4, reduction.hpp:41-44) and its
+        # best-known per-variant configs (curve_config, harness.hpp:178-196), the m = 16 analogues
         for name, kw in (("single_pass", dict(m=16, R=1, B=1024)), ("single_pass", dict(m=4, R=1, B=128)),
-                         ("recurrence", dict(m=16, R=5, B=32)), ("recurrence", dict(m=4, R=1, B=32)),
-                         ("split", dict(m=16, R=1, B=128, f=0.5)), ("split", dict(m=16, R=1, B=1024, f=0.9)),
+                         ("single_pass", dict(m=4, R=4, B=128)), ("single_pass", dict(m=16, R=4, B=128)),
+                         ("recurrence", dict(m=4, R=5, B=32)), ("recurrence", dict(m=16, R=5, B=32)),
+                         ("recurrence", dict(m=4, R=1, B=32)),
+                         ("split", dict(m=4, R=1, B=128, f=0.5)), ("split", dict(m=16, R=1, B=128, f=0.5)),
+                         ("split", dict(m=16, R=1, B=1024, f=0.9)),
                          ("shuffle32", dict()), ("half_tree", dict()), ("oracle64", dict())):
             cfg = T.ReductionConfig(variant=T.Variant[name], **kw)
             c = cfg.to_c()
