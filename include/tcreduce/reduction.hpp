@@ -13,8 +13,17 @@
 //   ReductionOutcome                 :59-67      -> tcr_outcome
 //   warp_offset                      :154-158    (pure index arithmetic, kept inline)
 //
+//   oracle64 / shuffle32_reduce /
+//   half_tree_reduce / recurrence_reduce /
+//   split_reduce                     :106-341    -> tcr_reduce_f32_host (variant set)
+//   chained_warp_reduce              :164-184    -> one warp chunk as a one-block single_pass
+//   detail::SimCounters, MmaStats    :71-82, fragment.hpp:16-20 (counter structs)
+//
 // Additions (B200-only): ReductionConfig::finalize / engine, and device-pointer overloads
 // reduce_device_f16 / reduce_device_f32 for data already resident in HBM.
+//
+// The reference's own unit tests (proj/tests/test_reduction.cpp, test_harness.cpp) compile
+// against this header unchanged (oracle/Makefile target ref_tests) and pass on the B200.
 #pragma once
 
 #include <cstddef>
@@ -24,6 +33,14 @@
 #include <string>
 
 #include "tcreduce_b200.h"
+
+// The reference's reduction.hpp includes its fragment/half emulator headers; when they are on
+// the include path (a caller that keeps the reference tree behind this directory), pull them in
+// the same way so code using Half / HalfFragment / MmaStats keeps compiling.
+#if __has_include("tcreduce/fragment.hpp")
+#include "tcreduce/fragment.hpp"
+#define TCREDUCE_B200_REFERENCE_FRAGMENT 1
+#endif
 
 namespace tcreduce {
 
@@ -97,6 +114,15 @@ struct ReductionConfig {
     }
 };
 
+#ifndef TCREDUCE_B200_REFERENCE_FRAGMENT
+// fragment.hpp:16-20 (the counter struct the reference's MMA emulation fills).
+struct MmaStats {
+    std::uint64_t mma_count = 0;
+    std::uint64_t loads = 0;
+    std::uint64_t stores = 0;
+};
+#endif
+
 struct ReductionOutcome {
     double value = 0.0;       // binary32 result (binary64 for the oracle)
     bool overflow = false;    // some Half produced during the run was non-finite
@@ -108,6 +134,15 @@ struct ReductionOutcome {
 };
 
 namespace detail {
+
+// reduction.hpp:71-82: running counters of one reduction.
+struct SimCounters {
+    MmaStats mma;
+    std::uint64_t atomic_count = 0;
+    std::uint64_t shuffle_count = 0;
+    std::uint64_t sim_steps = 0;
+    bool overflow = false;
+};
 
 inline ReductionOutcome from_c(const tcr_outcome& o) {
     ReductionOutcome r;
@@ -140,6 +175,58 @@ inline ReductionOutcome reduce(std::span<const float> x, const ReductionConfig& 
 inline ReductionOutcome single_pass_reduce(std::span<const float> x, ReductionConfig cfg) {
     cfg.variant = Variant::single_pass;
     return reduce(x, cfg);
+}
+
+// reduction.hpp:106-110: binary64 sum (0 for an empty span, as the reference).
+inline double oracle64(std::span<const float> x) {
+    ReductionConfig cfg;
+    cfg.variant = Variant::oracle64;
+    return reduce(x, cfg).value;
+}
+
+// reduction.hpp:113-122 / :126-151: bit-exact strided pairwise trees (fp32 / binary16 partials).
+inline ReductionOutcome shuffle32_reduce(std::span<const float> x) {
+    ReductionConfig cfg;
+    cfg.variant = Variant::shuffle32;
+    return reduce(x, cfg);
+}
+
+inline ReductionOutcome half_tree_reduce(std::span<const float> x) {
+    ReductionConfig cfg;
+    cfg.variant = Variant::half_tree;
+    return reduce(x, cfg);
+}
+
+// reduction.hpp:189-231 and :298-341 (cfg by value, variant forced).
+inline ReductionOutcome recurrence_reduce(std::span<const float> x, ReductionConfig cfg) {
+    cfg.variant = Variant::recurrence;
+    return reduce(x, cfg);
+}
+
+inline ReductionOutcome split_reduce(std::span<const float> x, ReductionConfig cfg) {
+    cfg.variant = Variant::split;
+    return reduce(x, cfg);
+}
+
+// reduction.hpp:164-184: the warp chunk x[base, base + R m^2) through the tensor-core chain and
+// the finishing MMA -- on the device, as a single_pass over that chunk with one warp per block
+// (its one block result IS the chunk result).  Same out_of_range contract and counter updates.
+inline float chained_warp_reduce(std::span<const float> x, std::size_t base, const ReductionConfig& cfg,
+                                 detail::SimCounters& sc) {
+    const std::size_t chunk = static_cast<std::size_t>(cfg.R) * cfg.m * cfg.m;
+    if (base + chunk > x.size()) throw std::out_of_range("chained_warp_reduce: chunk exceeds input");
+    if (cfg.R == 0) {   // no chain: the finishing MMA of a zero accumulator
+        ++sc.mma.mma_count;
+        return 0.0f;
+    }
+    ReductionConfig one = cfg;
+    one.variant = Variant::single_pass;
+    one.B = 32;
+    const ReductionOutcome o = reduce(x.subspan(base, chunk), one);
+    sc.mma.mma_count += cfg.R + 1ull;
+    sc.mma.loads += cfg.R;
+    sc.overflow = sc.overflow || o.overflow;
+    return static_cast<float>(o.value);
 }
 
 // Device-resident input (binary16 bits or fp32), result synchronously on the host.

@@ -55,6 +55,34 @@ __device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t& d0, uint32_t& d1
 
 __device__ __forceinline__ float h_round(float v) { return h_to_f32(f32_to_h(v)); }
 
+// The reference chunk (chained_warp_reduce, reduction.hpp:164-184, with the emulated mma of
+// fragment.hpp:82-97: ascending-k fp32 sums from 0, C added last) evaluated exactly on one CUDA
+// core.  Slow path for a chunk whose tensor-core result is NaN: the selector engines multiply
+// every binary16 by 0/1 entries, and a non-finite input times 0 is NaN where the reference's
+// all-ones products keep +-inf -- recomputing keeps the reference's non-finite value.
+__device__ __noinline__ float chunk_exact(const uint16_t* x, uint64_t n, uint64_t e0, uint32_t m, uint32_t R) {
+    float fin = 0.0f;
+    for (uint32_t j = 0; j < m; ++j) {
+        float c = 0.0f;
+        for (uint32_t r = 0; r < R; ++r) {
+            float col = 0.0f;
+            for (uint32_t k = 0; k < m; ++k) {
+                const uint64_t e = e0 + uint64_t(r) * m * m + uint64_t(k) * m + j;
+                col = col + (e < n ? h_to_f32(x[e]) : 0.0f);   // zero padding (reduction.hpp:244-245)
+            }
+            c = col + c;
+        }
+        fin = fin + h_round(c);
+    }
+    return fin + 0.0f;
+}
+
+__device__ __forceinline__ float repair_nan(float v, const SpParams& p, uint64_t chunk, uint32_t m) {
+    if (!isnan(v)) return v;
+    const uint64_t ce = uint64_t(p.R) * m * m;
+    return chunk_exact(static_cast<const uint16_t*>(p.x), p.n, chunk * ce, m, p.R);
+}
+
 // binary16 0/1 pair
 __device__ __forceinline__ uint32_t sel2(bool lo, bool hi) {
     return (lo ? 0x3C00u : 0u) | (hi ? 0x3C000000u : 0u);
@@ -221,14 +249,14 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
                 if (2 * c < S.CP) {
                     ovf |= !isfinite(d2[0]) || !isfinite(d2[2]);
                     const uint32_t ca = cu0 + g * S.CP + 2 * c, cb = cu0 + (g + 8) * S.CP + 2 * c;
-                    if (ca < Cg) s_chunk[ca] = d2[0];
-                    if (cb < Cg) s_chunk[cb] = d2[2];
+                    if (ca < Cg) s_chunk[ca] = repair_nan(d2[0], p, gi * Cg + ca, M);
+                    if (cb < Cg) s_chunk[cb] = repair_nan(d2[2], p, gi * Cg + cb, M);
                 }
                 if (2 * c + 1 < S.CP) {
                     ovf |= !isfinite(d2[1]) || !isfinite(d2[3]);
                     const uint32_t ca = cu0 + g * S.CP + 2 * c + 1, cb = cu0 + (g + 8) * S.CP + 2 * c + 1;
-                    if (ca < Cg) s_chunk[ca] = d2[1];
-                    if (cb < Cg) s_chunk[cb] = d2[3];
+                    if (ca < Cg) s_chunk[ca] = repair_nan(d2[1], p, gi * Cg + ca, M);
+                    if (cb < Cg) s_chunk[cb] = repair_nan(d2[3], p, gi * Cg + cb, M);
                 }
             }
             acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
@@ -336,7 +364,8 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
                 ovf |= !isfinite(r);
                 const uint32_t b = MM == 8 ? lane / S.CPT : lane;
                 const uint32_t item = warp + (it0 + b) * kGmWarps;
-                s_chunk[MM == 8 ? item * S.CPT + lane % S.CPT : item] = r;
+                const uint32_t ch = MM == 8 ? item * S.CPT + lane % S.CPT : item;
+                s_chunk[ch] = repair_nan(r, p, gi * Cg + ch, MM);
             }
             __syncwarp();
         };
@@ -486,7 +515,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
             if (done.s + 1 < slabs) continue;
             r = r + 0.0f;
             ovf |= !isfinite(r);
-            if (lane == 0) s_chunk[warp + done.it * kGmWarps] = r;
+            if (lane == 0) s_chunk[warp + done.it * kGmWarps] = repair_nan(r, p, gi * Cg + warp + done.it * kGmWarps, m);
             r = 0.0f;
         }
         cp_wait<0>();
@@ -603,7 +632,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
                 for (int w = 0; w < kGmWarps; ++w) r = r + s_wsum[w];
                 r = r + 0.0f;
                 ovf |= !isfinite(r);
-                s_chunk[it] = r;
+                s_chunk[it] = repair_nan(r, p, gi * Cg + it, m);
             }
         }
         cp_wait<0>();

@@ -660,3 +660,31 @@ def test_bench_two_ranks_one_gpu(tmp_path):
     # both shards of the global uniform stream, combined: within the single-GPU tolerance
     assert d["rel_err_vs_exact"] < 1e-5
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 2 * 2 * (1 << 26)
+
+
+@pytest.mark.parametrize("m,R,B", [(2, 1, 128), (2, 3, 64), (4, 1, 128), (4, 5, 32), (8, 1, 128), (8, 3, 32),
+                                   (16, 1, 1024), (16, 3, 96), (32, 1, 128), (128, 2, 64), (256, 1, 32),
+                                   (512, 1, 64), (4096, 1, 32)])
+def test_non_finite_values_match_reference(oracle, m, R, B):
+    """+inf / -inf / NaN inputs and column-sum overflow give the reference's value class and sign
+    (reduction.hpp:78-81, :179-182): the selector engines' 0 x inf = NaN is repaired per chunk."""
+    import math
+    base = oracle.generate_f16("uniform", 4, 300_000)
+    inf, ninf, nan, big = np.uint16(0x7C00), np.uint16(0xFC00), np.uint16(0x7E00), np.uint16(0x7800)  # 32768
+    cases = {}
+    h = base.copy(); h[1234] = inf; cases["+inf"] = h
+    h = base.copy(); h[99_999] = ninf; cases["-inf"] = h
+    h = base.copy(); h[7] = inf; h[250_001] = ninf; cases["+inf,-inf"] = h
+    h = base.copy(); h[4321] = nan; cases["nan"] = h
+    h = base.copy(); h[:64] = big; cases["column overflow"] = h
+    for name, h in cases.items():
+        for fin in (T.Finalize.tree, T.Finalize.ordered):
+            o = T.reduce(to_dev_f16(h), T.ReductionConfig(m=m, R=R, B=B, finalize=fin))
+            ref = oracle.single_pass(h, threads=8, m=m, R=R, B=B)
+            assert o.overflow == ref.overflow, (name, fin)
+            if math.isnan(ref.value):
+                assert math.isnan(o.value), (name, fin, o.value)
+            elif math.isinf(ref.value):
+                assert o.value == ref.value, (name, fin, o.value, ref.value)
+            else:
+                assert math.isfinite(o.value), (name, fin, o.value, ref.value)
