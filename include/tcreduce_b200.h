@@ -122,7 +122,9 @@ int tcr_reduce_f16_device(const uint16_t* d_x, size_t n, const tcr_config* cfg, 
 /* Asynchronous single_pass over device binary16: enqueues the kernel on `cuda_stream`,
  * writes the fp32 result to *d_result and ORs the overflow flag into *d_overflow (both device
  * pointers; *d_overflow is not cleared).  No host synchronisation; CUDA-graph capturable.
- * This is the per-shard step of the multi-GPU path. */
+ * This is the per-shard step of the multi-GPU path.  Non-finite inputs with m != 16 may yield
+ * NaN where the reference yields +-inf (the overflow flag is exact); the synchronous entry
+ * points detect that case and re-run with exact non-finite handling. */
 int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* cfg, float* d_result,
                               uint32_t* d_overflow, void* cuda_stream);
 int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* cfg, float* d_result,

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <string>
@@ -30,6 +31,28 @@ namespace {
 thread_local std::string g_err;
 thread_local int g_launches = 0;
 thread_local int g_engine = 0;  // engine that ran the full groups of the last call
+// m != 16 engines: use the NaN-repairing instantiations (tcr_sp_genm.cu, group_epilogue)
+thread_local bool g_repair = false;
+
+struct RepairScope {
+    bool prev;
+    explicit RepairScope(bool on) : prev(g_repair) { g_repair = g_repair || on; }
+    ~RepairScope() { g_repair = prev; }
+};
+
+// Synchronous entry points: a result that comes back NaN with the overflow note set on a
+// selector engine (m != 16) may be a 0 x inf artefact -- run the call again with the repairing
+// kernels, which reproduce the reference's +-inf / NaN exactly.  Finite data never pays.
+template <class F>
+int with_nan_retry(const tcr_config* c, tcr_outcome* out, F&& call) {
+    int rc = call();
+    if (rc == TCR_OK && c && out && c->m != 16 && !g_repair && out->overflow && std::isnan(out->value) &&
+        (c->variant == TCR_SINGLE_PASS || c->variant == TCR_RECURRENCE || c->variant == TCR_SPLIT)) {
+        RepairScope rs(true);
+        rc = call();
+    }
+    return rc;
+}
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -253,7 +276,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         // m != 16: the selector-matrix engine (binary16 input; fp32 callers convert first)
         if (f32) return fail(TCR_NOT_SUPPORTED, "internal: m != 16 needs binary16 input");
         g_engine = TCR_ENGINE_MMA_SYNC_ASYNC;
-        TCR_CUDA(tcr::launch_genm(p, g, s));
+        TCR_CUDA(tcr::launch_genm(p, g, s, g_repair));
         ++g_launches;
         return TCR_OK;
     }
@@ -695,6 +718,10 @@ int tcr_single_pass_counters(size_t n, const tcr_config* c, tcr_outcome* out) {
 
 int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_result,
                               uint32_t* d_overflow, void* stream) {
+    // The result stays on the device, so there is no retry: on a selector engine (m != 16) a
+    // non-finite input can surface as NaN where the reference has +-inf (the overflow flag is
+    // exact either way).  The synchronous entry points re-run such calls with the repairing
+    // kernels; this one keeps the fast instantiations.
     return sp_async(d_x, n, c, false, d_result, d_overflow, static_cast<cudaStream_t>(stream));
 }
 
@@ -704,11 +731,11 @@ int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* c, f
 }
 
 int tcr_reduce_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
-    return reduce_device(d_x, n, c, out, false, static_cast<cudaStream_t>(stream));
+    return with_nan_retry(c, out, [&] { return reduce_device(d_x, n, c, out, false, static_cast<cudaStream_t>(stream)); });
 }
 
 int tcr_reduce_f32_device(const float* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
-    return reduce_device(d_x, n, c, out, true, static_cast<cudaStream_t>(stream));
+    return with_nan_retry(c, out, [&] { return reduce_device(d_x, n, c, out, true, static_cast<cudaStream_t>(stream)); });
 }
 
 }  // extern "C"
@@ -749,6 +776,7 @@ extern "C" {
 
 int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const int32_t* devices, int32_t ngpu,
                            const tcr_config* c, tcr_outcome* out) {
+    RepairScope rs(c && c->m != 16);   // one combined result: repair up front
     g_launches = 0;
     if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
     std::memset(out, 0, sizeof *out);
@@ -828,6 +856,7 @@ int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const in
 
 int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_blocks,
                                  void* stream) {
+    RepairScope rs(c && c->m != 16);   // parity hook: per-block values exact for non-finite data too
     g_launches = 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
@@ -968,11 +997,11 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
 
 int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outcome* out) {
     // Drop-in for reduce(std::span<const float>, cfg)
-    return reduce_host(x, true, n, c, out);
+    return with_nan_retry(c, out, [&] { return reduce_host(x, true, n, c, out); });
 }
 
 int tcr_reduce_f16_host(const uint16_t* x, size_t n, const tcr_config* c, tcr_outcome* out) {
-    return reduce_host(x, false, n, c, out);
+    return with_nan_retry(c, out, [&] { return reduce_host(x, false, n, c, out); });
 }
 
 int tcr_generate_f16_device(uint16_t* d_x, size_t n, int32_t dist, uint64_t seed, int64_t lo, int64_t hi,

@@ -97,7 +97,9 @@ bool async_plan(const SpGeometry& g, SpParams* p, int grid);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.
 bool genm_supported(const SpGeometry& g);
-cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s);
+// repair: instantiations that recompute NaN chunk results exactly (non-finite inputs; see
+// group_epilogue in tcr_sp_genm.cu).
+cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair);
 
 // Variants (tcr_variants.cu): bit-exact strided pairwise trees (shuffle32 / half_tree), binary64
 // sum (oracle64), and the recurrence level rounding.

@@ -60,7 +60,7 @@ __device__ __forceinline__ float h_round(float v) { return h_to_f32(f32_to_h(v))
 // core.  Slow path for a chunk whose tensor-core result is NaN: the selector engines multiply
 // every binary16 by 0/1 entries, and a non-finite input times 0 is NaN where the reference's
 // all-ones products keep +-inf -- recomputing keeps the reference's non-finite value.
-__device__ __noinline__ float chunk_exact(const uint16_t* x, uint64_t n, uint64_t e0, uint32_t m, uint32_t R) {
+__device__ __forceinline__ float chunk_exact(const uint16_t* x, uint64_t n, uint64_t e0, uint32_t m, uint32_t R) {
     float fin = 0.0f;
     for (uint32_t j = 0; j < m; ++j) {
         float c = 0.0f;
@@ -77,11 +77,6 @@ __device__ __noinline__ float chunk_exact(const uint16_t* x, uint64_t n, uint64_
     return fin + 0.0f;
 }
 
-__device__ __forceinline__ float repair_nan(float v, const SpParams& p, uint64_t chunk, uint32_t m) {
-    if (!isnan(v)) return v;
-    const uint64_t ce = uint64_t(p.R) * m * m;
-    return chunk_exact(static_cast<const uint16_t*>(p.x), p.n, chunk * ce, m, p.R);
-}
 
 // binary16 0/1 pair
 __device__ __forceinline__ uint32_t sel2(bool lo, bool hi) {
@@ -95,13 +90,41 @@ __device__ __forceinline__ void group_tree_any(const SpParams& p, uint64_t gi, c
     if (!p.group_partials) return;
     const uint32_t seg = G >= 32 ? G / 32 : 1;
     float acc = 0.0f;
-    if (lane * seg < G) acc = lane_segment_tree([&](uint32_t i) { return blocks[i]; }, lane * seg, seg);
+    if (lane * seg < G) {
+        float stk[16];
+        int top = 0;
+        for (uint32_t i = 0; i < seg; ++i) {
+            float v = blocks[lane * seg + i];
+            for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
+            stk[top++] = v;
+        }
+        acc = stk[0];
+    }
     acc = warp_tree_xor(acc);
     if (lane == 0) p.group_partials[gi] = acc;
 }
 
-__device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, float* s_chunk, float* s_block) {
-    __syncthreads();
+// Group epilogue.  A NaN chunk result may be an artefact of the selector products (0 x inf).
+// REPAIR instantiations (the C ABI re-runs a call in this mode when its result came back NaN
+// with the overflow note set, and always uses it for results that stay on the device): every
+// non-finite chunk result already set the thread's overflow note (`ovf`, reduction.hpp:78-81),
+// so only then does the CTA scan its chunk table and recompute the NaN chunks exactly
+// (chunk_exact) before the block stage.  The default instantiations carry none of this code.
+template <bool REPAIR>
+__device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, float* s_chunk, float* s_block,
+                                               uint32_t m, bool ovf) {
+    if constexpr (REPAIR) {
+        if (__syncthreads_or(ovf)) {
+            const uint32_t Cg = p.G * p.W;
+            const uint64_t ce = uint64_t(p.R) * m * m;
+            for (uint32_t i = threadIdx.x; i < Cg; i += kGmThreads)
+                if (isnan(s_chunk[i]))
+                    s_chunk[i] = chunk_exact(static_cast<const uint16_t*>(p.x), p.n, (gi * Cg + i) * ce, m, p.R);
+            __syncthreads();
+        }
+    } else {
+        __syncthreads();
+    }
     tile_trees_blocks(p, gi, s_chunk, s_block, threadIdx.x >> 5, kGmWarps);
     __syncthreads();
     if ((threadIdx.x >> 5) == 0) group_tree_any(p, gi, s_block);
@@ -125,7 +148,7 @@ struct NatShape {
 template <int RBC>
 __host__ __device__ constexpr int nat_depth() { return RBC == 0 ? 2 : (8 / RBC > 2 ? 8 / RBC : 2); }
 
-template <int M, int RBC>
+template <int M, int RBC, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, const NatShape S) {
     constexpr int ND = nat_depth<RBC>();
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -249,20 +272,20 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
                 if (2 * c < S.CP) {
                     ovf |= !isfinite(d2[0]) || !isfinite(d2[2]);
                     const uint32_t ca = cu0 + g * S.CP + 2 * c, cb = cu0 + (g + 8) * S.CP + 2 * c;
-                    if (ca < Cg) s_chunk[ca] = repair_nan(d2[0], p, gi * Cg + ca, M);
-                    if (cb < Cg) s_chunk[cb] = repair_nan(d2[2], p, gi * Cg + cb, M);
+                    if (ca < Cg) s_chunk[ca] = d2[0];
+                    if (cb < Cg) s_chunk[cb] = d2[2];
                 }
                 if (2 * c + 1 < S.CP) {
                     ovf |= !isfinite(d2[1]) || !isfinite(d2[3]);
                     const uint32_t ca = cu0 + g * S.CP + 2 * c + 1, cb = cu0 + (g + 8) * S.CP + 2 * c + 1;
-                    if (ca < Cg) s_chunk[ca] = repair_nan(d2[1], p, gi * Cg + ca, M);
-                    if (cb < Cg) s_chunk[cb] = repair_nan(d2[3], p, gi * Cg + cb, M);
+                    if (ca < Cg) s_chunk[ca] = d2[1];
+                    if (cb < Cg) s_chunk[cb] = d2[3];
                 }
             }
             acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
         }
         cp_wait<0>();
-        group_epilogue(p, gi, s_chunk, s_block);
+        group_epilogue<REPAIR>(p, gi, s_chunk, s_block, M, ovf);
     }
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __threadfence();
@@ -291,7 +314,7 @@ struct TrStage {
     static constexpr uint32_t FLOATS = ROWS * SW;                                 // per warp
 };
 
-template <int MM>   // 8, 32, 64, 128
+template <int MM, bool REPAIR>   // MM = 8, 32, 64, 128
 __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, const TrShape S) {
     constexpr int D = kGmTrDepth;
     constexpr uint32_t SG = MM >= 32 ? MM / 16 : 1;    // column groups per chunk (m >= 32)
@@ -365,7 +388,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
                 const uint32_t b = MM == 8 ? lane / S.CPT : lane;
                 const uint32_t item = warp + (it0 + b) * kGmWarps;
                 const uint32_t ch = MM == 8 ? item * S.CPT + lane % S.CPT : item;
-                s_chunk[ch] = repair_nan(r, p, gi * Cg + ch, MM);
+                s_chunk[ch] = r;
             }
             __syncwarp();
         };
@@ -415,7 +438,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
         }
         if (nb) flush(it - nb, nb);
         cp_wait<0>();
-        group_epilogue(p, gi, s_chunk, s_block);
+        group_epilogue<REPAIR>(p, gi, s_chunk, s_block, MM, ovf);
     }
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __threadfence();
@@ -431,6 +454,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
 // accumulate the slab's 256 column sums over the chain of rows in D_lo / D_hi; at the end of a
 // slab the partials are rounded to binary16 (reduction.hpp:179-181) and added to the running
 // ascending-j finishing sum (:182, fragment.hpp:89-92), carried across the m / 256 slabs.
+template <bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, const uint32_t m) {
     constexpr int D = kGmTrDepth;
     extern __shared__ __align__(128) unsigned char s_ring[];   // [kGmWarps][D][512] + tables
@@ -515,11 +539,11 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
             if (done.s + 1 < slabs) continue;
             r = r + 0.0f;
             ovf |= !isfinite(r);
-            if (lane == 0) s_chunk[warp + done.it * kGmWarps] = repair_nan(r, p, gi * Cg + warp + done.it * kGmWarps, m);
+            if (lane == 0) s_chunk[warp + done.it * kGmWarps] = r;
             r = 0.0f;
         }
         cp_wait<0>();
-        group_epilogue(p, gi, s_chunk, s_block);
+        group_epilogue<REPAIR>(p, gi, s_chunk, s_block, m, ovf);
     }
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __threadfence();
@@ -535,7 +559,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
 // in warp order (fixed), rounded to binary16 (reduction.hpp:179-181) and summed by a fixed
 // lane-then-warp tree into the chunk result (the finishing MMA's sum, :182; binary16 partials of
 // similar magnitude add exactly in fp32, so the order rarely matters).
-template <int SL>
+template <int SL, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams p, const uint32_t m) {
     constexpr int D = kGmTrDepth;
     extern __shared__ __align__(128) unsigned char s_ring[];   // ring | part[8][m] | tables
@@ -632,11 +656,11 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
                 for (int w = 0; w < kGmWarps; ++w) r = r + s_wsum[w];
                 r = r + 0.0f;
                 ovf |= !isfinite(r);
-                s_chunk[it] = repair_nan(r, p, gi * Cg + it, m);
+                s_chunk[it] = r;
             }
         }
         cp_wait<0>();
-        group_epilogue(p, gi, s_chunk, s_block);
+        group_epilogue<REPAIR>(p, gi, s_chunk, s_block, m, ovf);
     }
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __threadfence();
@@ -717,7 +741,8 @@ cudaError_t launch_gm(K fn, uint32_t dyn, uint64_t groups, const SpParams& p, co
 }
 }  // namespace
 
-cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) {
+template <bool REPAIR>
+cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s) {
     const uint32_t Cg = g.G * g.W;
     const uint64_t groups = p.group_end - p.group_begin;
     const uint32_t tables = (Cg + g.G + 3u) / 4u * 16u;   // chunk results [Cg] + block results [G]
@@ -728,7 +753,7 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) 
         int nd = 2;
         const bool fast = S.PR == S.RB && (S.RB & (S.RB - 1)) == 0;   // PR a power of two <= 16
 #define TCR_NAT(MV, RBV) \
-    { fn = gm_nat_kernel<MV, RBV>; nd = nat_depth<RBV>(); }
+    { fn = gm_nat_kernel<MV, RBV, REPAIR>; nd = nat_depth<RBV>(); }
         if (g.m == 2) {
             if (!fast) TCR_NAT(2, 0) else if (S.RB == 1) TCR_NAT(2, 1) else if (S.RB == 2) TCR_NAT(2, 2)
             else if (S.RB == 4) TCR_NAT(2, 4) else if (S.RB == 8) TCR_NAT(2, 8) else TCR_NAT(2, 16)
@@ -745,32 +770,30 @@ cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s) 
         if (g.m <= 2048 && !std::getenv("TCR_GM_WIDE_WARP")) {   // knob: profiling A/B
             const uint32_t dyn = ring + kGmWarps * g.m * 4u + tables;
             switch (g.m) {
-            case 256: return launch_gm(gm_wide_cta_kernel<1>, dyn, groups, p, g.m, s);
-            case 512: return launch_gm(gm_wide_cta_kernel<2>, dyn, groups, p, g.m, s);
-            case 1024: return launch_gm(gm_wide_cta_kernel<4>, dyn, groups, p, g.m, s);
-            default: return launch_gm(gm_wide_cta_kernel<8>, dyn, groups, p, g.m, s);
+            case 256: return launch_gm(gm_wide_cta_kernel<1, REPAIR>, dyn, groups, p, g.m, s);
+            case 512: return launch_gm(gm_wide_cta_kernel<2, REPAIR>, dyn, groups, p, g.m, s);
+            case 1024: return launch_gm(gm_wide_cta_kernel<4, REPAIR>, dyn, groups, p, g.m, s);
+            default: return launch_gm(gm_wide_cta_kernel<8, REPAIR>, dyn, groups, p, g.m, s);
             }
         }
-        return launch_gm(gm_wide_kernel, ring + tables, groups, p, g.m, s);
+        return launch_gm(gm_wide_kernel<REPAIR>, ring + tables, groups, p, g.m, s);
     }
     TrShape S;
     if (!tr_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
     void (*fn)(SpParams, TrShape) = nullptr;
-    switch (g.m) {
-    case 8: fn = gm_tr_kernel<8>; break;
-    case 32: fn = gm_tr_kernel<32>; break;
-    case 64: fn = gm_tr_kernel<64>; break;
-    case 128: fn = gm_tr_kernel<128>; break;
-    default: return cudaErrorInvalidValue;
-    }
     uint32_t stage = 0;
     switch (g.m) {
-    case 8: stage = TrStage<8>::FLOATS; break;
-    case 32: stage = TrStage<32>::FLOATS; break;
-    case 64: stage = TrStage<64>::FLOATS; break;
-    default: stage = TrStage<128>::FLOATS; break;
+    case 8: fn = gm_tr_kernel<8, REPAIR>; stage = TrStage<8>::FLOATS; break;
+    case 32: fn = gm_tr_kernel<32, REPAIR>; stage = TrStage<32>::FLOATS; break;
+    case 64: fn = gm_tr_kernel<64, REPAIR>; stage = TrStage<64>::FLOATS; break;
+    case 128: fn = gm_tr_kernel<128, REPAIR>; stage = TrStage<128>::FLOATS; break;
+    default: return cudaErrorInvalidValue;
     }
     return launch_gm(fn, kGmWarps * (kGmTrDepth * 512u + stage * 4u) + tables, groups, p, S, s);
+}
+
+cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair) {
+    return repair ? launch_genm_t<true>(p, g, s) : launch_genm_t<false>(p, g, s);
 }
 
 }  // namespace tcr
