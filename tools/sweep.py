@@ -124,6 +124,11 @@ def main():
         x = T.generate("uniform", 0, n, device=dev)
         exact, _ = T.exact_sum(x)
         xp = C.c_void_p(x.data_ptr())
+        # recurrence overflows binary16 on uniform input (its level partials grow past 65504, as
+        # the paper reports): time it on normal(0,1) input too, where it does not
+        xn = T.generate("normal", 1, n, device=dev)
+        exact_n, _ = T.exact_sum(xn)
+        xnp = C.c_void_p(xn.data_ptr())
         vpts = []
         # the north-star config, the reference's defaults (m = 4, reduction.hpp:41-44) and its
         # best-known per-variant configs (curve_config, harness.hpp:178-196), the m = 16 analogues
@@ -131,21 +136,28 @@ def main():
                          ("single_pass", dict(m=4, R=4, B=128)), ("single_pass", dict(m=16, R=4, B=128)),
                          ("recurrence", dict(m=4, R=5, B=32)), ("recurrence", dict(m=16, R=5, B=32)),
                          ("recurrence", dict(m=4, R=1, B=32)),
+                         ("recurrence", dict(m=4, R=5, B=32, dist="normal")),
+                         ("recurrence", dict(m=16, R=5, B=32, dist="normal")),
                          ("split", dict(m=4, R=1, B=128, f=0.5)), ("split", dict(m=16, R=1, B=128, f=0.5)),
                          ("split", dict(m=16, R=1, B=1024, f=0.9)),
                          ("shuffle32", dict()), ("half_tree", dict()), ("oracle64", dict())):
+            kw = dict(kw)
+            dist = kw.pop("dist", "uniform")
+            ptr, ex = (xnp, exact_n) if dist == "normal" else (xp, exact)
             cfg = T.ReductionConfig(variant=T.Variant[name], **kw)
             c = cfg.to_c()
             o = _capi.tcr_outcome()
-            fn = lambda: _capi.check(lib.tcr_reduce_f16_device(xp, n, C.byref(c), C.byref(o), sp))  # noqa: E731
+            fn = lambda: _capi.check(lib.tcr_reduce_f16_device(ptr, n, C.byref(c), C.byref(o), sp))  # noqa: E731
             med, best = time_fn(fn, max(3, args.reps // 2))
-            vpts.append({"variant": name, **kw, "ms": med, "gelem_s": n / med / 1e6, "gb_s": 2 * n / med / 1e6,
-                         "frac_hbm": 2 * n / med / 1e6 / peak, "value": o.value, "overflow": bool(o.overflow),
-                         "rel_err_exact": abs(o.value - exact) / abs(exact), "launches": lib.tcr_last_launch_count()})
+            vpts.append({"variant": name, **kw, "dist": dist, "ms": med, "gelem_s": n / med / 1e6,
+                         "gb_s": 2 * n / med / 1e6, "frac_hbm": 2 * n / med / 1e6 / peak, "value": o.value,
+                         "overflow": bool(o.overflow), "rel_err_exact": abs(o.value - ex) / abs(ex),
+                         "launches": lib.tcr_last_launch_count()})
             print(json.dumps(vpts[-1]), flush=True)
-        out["variants"] = {"n": n, "dist": "uniform s0", "exact": exact, "points": vpts,
+        out["variants"] = {"n": n, "dist": "uniform s0 (normal s1 where marked)", "exact": exact,
+                           "exact_normal": exact_n, "points": vpts,
                            "timing": "CUDA events around 5 back-to-back synchronous tcr_reduce_f16_device calls"}
-        del x
+        del x, xn
         torch.cuda.empty_cache()
 
     if args.precision:
