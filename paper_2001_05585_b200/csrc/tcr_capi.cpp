@@ -697,6 +697,9 @@ const char* tcr_last_error(void) { return g_err.c_str(); }
 const char* tcr_version(void) { return "tcreduce-b200 0.1 (sm_100a)"; }
 int tcr_last_launch_count(void) { return g_launches; }
 int tcr_last_engine(void) { return g_engine; }
+// Profiling hook (not in the public header): timestamps of the last TCR_DEBUG_MODE=20 launch of
+// the cp.async engine, 4 per CTA (start, streaming done, after finalise, is-last).
+int tcr_debug_timestamps(unsigned long long* host, size_t count) { return tcr::debug_timestamps(host, count); }
 
 size_t tcr_block_count(size_t n, const tcr_config* c) {
     if (!c || validate_cfg(c)) return 0;

@@ -89,6 +89,8 @@ bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
 // Per-warp cp.async pipeline engine (LDGSTS ring per warp, ldmatrix.trans + HMMA); handles any
 // group range including the ragged tail (zero-fill copies).  binary16 input.
 int async_max_grid(uint32_t R, int debug_mode = 0);
+// profiling: per-CTA %globaltimer stamps of the last debug_mode-20 launch
+int debug_timestamps(unsigned long long* host, size_t count);
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s);
 // Work-unit plan of the cp.async engine over groups [p.group_begin, p.group_end) on `grid`
 // CTAs: sets split, split_tail, tail_group; returns whether units are handed out dynamically.

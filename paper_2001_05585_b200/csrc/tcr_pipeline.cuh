@@ -84,8 +84,55 @@ __device__ __forceinline__ float warp_tree_xor(float v) {
     return v;
 }
 
+// Adjacent pairwise tree ((v0 + v1) + (v2 + v3)) ... over the `seg` (power of two) values
+// ld(base), ..., ld(base + seg - 1): compile-time register trees up to 128 values (no
+// local-memory stack), a binary-counter stack beyond.
+template <int SEG, typename LD>
+__device__ __forceinline__ float static_segment_tree(LD ld, uint32_t base) {
+    float v[SEG];
+#pragma unroll
+    for (int i = 0; i < SEG; ++i) v[i] = ld(base + i);
+#pragma unroll
+    for (int len = SEG; len > 1; len >>= 1)
+#pragma unroll
+        for (int i = 0; i < len / 2; ++i) v[i] = v[2 * i] + v[2 * i + 1];
+    return v[0];
+}
+
+template <typename LD>
+__device__ __forceinline__ float lane_segment_tree(LD ld, uint32_t base, uint32_t seg) {
+    switch (seg) {
+    case 1: return ld(base);
+    case 2: return static_segment_tree<2>(ld, base);
+    case 4: return static_segment_tree<4>(ld, base);
+    case 8: return static_segment_tree<8>(ld, base);
+    case 16: return static_segment_tree<16>(ld, base);
+    case 32: return static_segment_tree<32>(ld, base);
+    case 64: return static_segment_tree<32>(ld, base) + static_segment_tree<32>(ld, base + 32);
+    case 128: {
+        const float a = static_segment_tree<32>(ld, base) + static_segment_tree<32>(ld, base + 32);
+        const float b = static_segment_tree<32>(ld, base + 64) + static_segment_tree<32>(ld, base + 96);
+        return a + b;
+    }
+    default: {
+        float stk[24];
+        int top = 0;
+        for (uint32_t i = 0; i < seg; ++i) {
+            float v = ld(base + i);
+            for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
+            stk[top++] = v;
+        }
+        return stk[0];
+    }
+    }
+}
+
 // Canonical adjacent tree over vals[0,count) (zero padded to a power of two) by the first
 // `nthr` threads (power of two, multiple of 32); every thread of the CTA must call it.
+// REG: per-thread segments of <= 128 values as compile-time register trees with all loads in
+// flight at once (the last CTA's finalise of the cp.async engine: ~1 L2 round trip instead of a
+// local-memory stack walk); same tree, same result.
+template <bool REG = false>
 __device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, float* s_scratch, unsigned nthr) {
     uint64_t P = 1;
     while (P < count) P <<= 1;
@@ -93,7 +140,11 @@ __device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, flo
     if (seg == 0) seg = 1;
     float acc = 0.0f;
     const uint64_t lo = uint64_t(threadIdx.x) * seg;
-    if (threadIdx.x < nthr && lo < P) {
+    if (REG && seg <= 128) {
+        if (threadIdx.x < nthr && lo < P)
+            acc = lane_segment_tree([&](uint32_t i) { return i < count ? __ldcg(vals + i) : 0.0f; }, uint32_t(lo),
+                                    uint32_t(seg));
+    } else if (threadIdx.x < nthr && lo < P) {
         float stk[40];
         int top = 0;
         // batches of 8 independent L2 loads in flight, then the same streaming stack order
@@ -132,6 +183,7 @@ __device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, flo
 
 // Last-CTA-done finaliser shared by the persistent engines: every thread of the CTA calls it
 // after publishing its partials (__threadfence + __syncthreads done by the caller).
+template <bool REG = false>
 __device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_scratch, int* s_last, unsigned nthr) {
     if (!(p.finalize == kFinTree || p.finalize == kFinOrdered)) return;
     if (threadIdx.x == 0) {
@@ -142,7 +194,7 @@ __device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_sc
     if (!*s_last) return;
     __threadfence();
     if (p.finalize == kFinTree) {
-        const float r = cta_tree(p.group_partials, p.n_groups, s_scratch, nthr);
+        const float r = cta_tree<REG>(p.group_partials, p.n_groups, s_scratch, nthr);
         if (threadIdx.x == 0) *p.result = r;
     } else if (threadIdx.x == 0) {
         // reduction.hpp:257-268: serial binary32 accumulation, ascending or seeded permutation
@@ -240,49 +292,6 @@ __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t b
 __device__ __forceinline__ void tile_trees_blocks(const SpParams& p, uint64_t tile, const float* chunks,
                                                   float* blocks, uint32_t w, uint32_t nwarps) {
     range_trees_blocks(p, tile * p.G, p.G, chunks, blocks, w, nwarps);
-}
-
-// Adjacent pairwise tree ((v0 + v1) + (v2 + v3)) ... over the `seg` (power of two) values
-// ld(base), ..., ld(base + seg - 1): compile-time register trees up to 128 values (no
-// local-memory stack), a binary-counter stack beyond.
-template <int SEG, typename LD>
-__device__ __forceinline__ float static_segment_tree(LD ld, uint32_t base) {
-    float v[SEG];
-#pragma unroll
-    for (int i = 0; i < SEG; ++i) v[i] = ld(base + i);
-#pragma unroll
-    for (int len = SEG; len > 1; len >>= 1)
-#pragma unroll
-        for (int i = 0; i < len / 2; ++i) v[i] = v[2 * i] + v[2 * i + 1];
-    return v[0];
-}
-
-template <typename LD>
-__device__ __forceinline__ float lane_segment_tree(LD ld, uint32_t base, uint32_t seg) {
-    switch (seg) {
-    case 1: return ld(base);
-    case 2: return static_segment_tree<2>(ld, base);
-    case 4: return static_segment_tree<4>(ld, base);
-    case 8: return static_segment_tree<8>(ld, base);
-    case 16: return static_segment_tree<16>(ld, base);
-    case 32: return static_segment_tree<32>(ld, base);
-    case 64: return static_segment_tree<32>(ld, base) + static_segment_tree<32>(ld, base + 32);
-    case 128: {
-        const float a = static_segment_tree<32>(ld, base) + static_segment_tree<32>(ld, base + 32);
-        const float b = static_segment_tree<32>(ld, base + 64) + static_segment_tree<32>(ld, base + 96);
-        return a + b;
-    }
-    default: {
-        float stk[24];
-        int top = 0;
-        for (uint32_t i = 0; i < seg; ++i) {
-            float v = ld(base + i);
-            for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
-            stk[top++] = v;
-        }
-        return stk[0];
-    }
-    }
 }
 
 // Group stage: adjacent tree over the G (power of two) block results of group `tile`, by one

@@ -260,6 +260,15 @@ constexpr uint32_t as_smem_bytes() {
 // concurrent CTAs read neighbouring units).  Per unit: stream -> chunk results -> block trees
 // (reduction.hpp:253) -> group tree, either in place (S = 1) or by the CTA that completes the
 // group (S > 1).
+// Profiling (debug_mode 20, never set in production): %globaltimer stamps per CTA (start,
+// streaming done) and of the last CTA's finalise, read back by tcr_debug_timestamps.
+__device__ unsigned long long g_dbg_ts[4 * 1024 + 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
     extern __shared__ __align__(128) unsigned char s_ring[];
@@ -272,6 +281,8 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     const uint32_t ring = smem_u32(s_ring) + warp * D * kAsStageBytes;
     bool ovf = false;
     const uint32_t G = p.G, Cg = G * p.W;
+    const bool stamp = p.debug_mode == 20 && threadIdx.x == 0 && blockIdx.x < 1024;
+    if (stamp) g_dbg_ts[4 * blockIdx.x] = gtimer();
     // unit space: groups [group_begin, tail_group) in `split` pieces, then the tail groups
     // [tail_group, group_end) in `split_tail` smaller pieces
     const uint64_t u_main = (p.tail_group - p.group_begin) * p.split;
@@ -336,9 +347,14 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
         u = dyn ? s_next : nxt;
     }
     if (__any_sync(kFull, ovf) && lane_id() == 0) atomicOr(p.overflow, 1u);
+    if (stamp) g_dbg_ts[4 * blockIdx.x + 1] = gtimer();
     __threadfence();
     __syncthreads();
-    finalize_last_cta(p, s_scratch, &s_last, kAsThreads);
+    finalize_last_cta<true>(p, s_scratch, &s_last, kAsThreads);
+    if (stamp) {
+        g_dbg_ts[4 * blockIdx.x + 2] = gtimer();
+        g_dbg_ts[4 * blockIdx.x + 3] = s_last;
+    }
 }
 
 using AsKernel = void (*)(SpParams);
@@ -479,6 +495,11 @@ AsLaunch as_launch(const AsPick& k, int cps) {
 }
 
 }  // namespace
+
+int debug_timestamps(unsigned long long* host, size_t count) {
+    if (count > 4 * 1024 + 4) count = 4 * 1024 + 4;
+    return cudaMemcpyFromSymbol(host, g_dbg_ts, count * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
 
 int async_max_grid(uint32_t R, int mode) {
     as_attr_once();
