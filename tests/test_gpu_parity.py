@@ -688,3 +688,28 @@ def test_non_finite_values_match_reference(oracle, m, R, B):
                 assert o.value == ref.value, (name, fin, o.value, ref.value)
             else:
                 assert math.isfinite(o.value), (name, fin, o.value, ref.value)
+
+
+@pytest.mark.parametrize("m,R,B", [(16, 1, 1024), (16, 4, 128), (4, 1, 128), (8, 3, 64), (256, 1, 32)])
+def test_async_single_pass_is_graph_capturable(oracle, m, R, B):
+    """tcr_single_pass_f16_async (the per-shard step) captured into a CUDA graph after one warm-up
+    call replays to the eager result: no host synchronisation or allocation inside."""
+    h = oracle.generate_f16("normal", 6, (1 << 22) + 99)
+    x = to_dev_f16(h)
+    cfg = T.ReductionConfig(m=m, R=R, B=B)
+    res = torch.zeros(1, dtype=torch.float32, device=DEV)
+    ovf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    s = torch.cuda.Stream(device=DEV)
+    with torch.cuda.stream(s):
+        T.single_pass_async(x, cfg, res, ovf)          # warm-up: workspaces allocated here
+    torch.cuda.synchronize()
+    eager = res.item()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        T.single_pass_async(x, cfg, res, ovf)
+    for _ in range(3):
+        res.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert res.item() == eager
+    assert eager == T.reduce(x, cfg).value
