@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
-"""fp32 device-input single_pass throughput (convert on load), cp.async fp32 engine vs the
-register engine (TCR_F32_REGS=1) and m = 4 (convert pass + selector engine).  Profiling tool."""
+"""fp32 device-input single_pass throughput (convert on load): m = 16 (register engine with
+from_single fused into the load) and m = 4 (convert pass + selector engine).  Profiling tool."""
 import ctypes as C
 import os
 import statistics
@@ -20,7 +20,7 @@ for n in (1 << 28, 1 << 30):
     xf = T.generate('uniform', 0, n, device=dev, dtype='float32')
     res = torch.zeros(2, dtype=torch.float32, device=dev)
     ovf = torch.zeros(1, dtype=torch.int32, device=dev)
-    for m, env in ((16, None), (16, "TCR_F32_REGS"), (4, None)):
+    for m, env in ((16, None), (4, None)):
         if env:
             os.environ[env] = "1"
         cfg = T.ReductionConfig(m=m, R=1, B=1024 if m == 16 else 128).to_c()
