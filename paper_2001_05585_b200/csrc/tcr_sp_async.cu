@@ -228,12 +228,15 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
 }
 
 // Ring depth per chain length: 2*R | D keeps every stage index and chunk pair compile-time.
-template <int RT> struct AsDepth { static constexpr int value = 8; };
+template <int RT> struct AsDepth { static constexpr int value = 16; };
 template <> struct AsDepth<1> { static constexpr int value = 16; };
 template <> struct AsDepth<2> { static constexpr int value = 16; };
 template <> struct AsDepth<3> { static constexpr int value = 24; };   // 12: -0..3 % (mode 11)
 template <> struct AsDepth<4> { static constexpr int value = 16; };
 template <> struct AsDepth<5> { static constexpr int value = 20; };   // 10: -3..5 % (mode 11)
+template <> struct AsDepth<6> { static constexpr int value = 24; };
+template <> struct AsDepth<7> { static constexpr int value = 14; };   // 28 would not fit 2 CTAs/SM
+template <> struct AsDepth<8> { static constexpr int value = 16; };
 
 int as_depth(uint32_t R) {
     switch (R) {
@@ -242,12 +245,15 @@ int as_depth(uint32_t R) {
     case 3: return AsDepth<3>::value;
     case 4: return AsDepth<4>::value;
     case 5: return AsDepth<5>::value;
+    case 6: return AsDepth<6>::value;
+    case 7: return AsDepth<7>::value;
+    case 8: return AsDepth<8>::value;
     default: return AsDepth<0>::value;
     }
 }
 
 __host__ __device__ inline bool static_unit(uint32_t Cu, uint32_t R, int D) {
-    return R >= 1 && R <= 5 && Cu % (8 * kAsWarps) == 0 && (Cu / kAsWarps) * R >= uint32_t(D) &&
+    return R >= 1 && R <= 8 && Cu % (8 * kAsWarps) == 0 && (Cu / kAsWarps) * R >= uint32_t(D) &&
            ((Cu / kAsWarps) * R) % uint32_t(D) == 0;
 }
 
@@ -377,6 +383,9 @@ AsPick pick(uint32_t R, int mode = 0) {
     case 3: return {sp_async_kernel<3>, as_smem_bytes<3>()};
     case 4: return {sp_async_kernel<4>, as_smem_bytes<4>()};
     case 5: return {sp_async_kernel<5>, as_smem_bytes<5>()};
+    case 6: return {sp_async_kernel<6>, as_smem_bytes<6>()};
+    case 7: return {sp_async_kernel<7>, as_smem_bytes<7>()};
+    case 8: return {sp_async_kernel<8>, as_smem_bytes<8>()};
     default: return {sp_async_kernel<0>, as_smem_bytes<0>()};
     }
 }
@@ -385,7 +394,7 @@ bool as_attr_once() {
     static bool done = false;
     if (!done) {
         for (int mode : {0, 9, 10, 11})
-        for (uint32_t R = 0; R <= 5; ++R) {
+        for (uint32_t R = 0; R <= 8; ++R) {
             const AsPick k = pick(R, mode);
             cudaFuncAttributes fa{};
             cudaFuncGetAttributes(&fa, k.fn);

@@ -113,7 +113,7 @@ def _block_parity(oracle, h, R, B, engine=T.Engine.auto):
 
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1)])
-@pytest.mark.parametrize("R,B", [(1, 1024), (4, 128), (2, 32), (5, 96)])
+@pytest.mark.parametrize("R,B", [(1, 1024), (4, 128), (2, 32), (5, 96), (6, 128), (7, 64), (8, 1024), (9, 32)])
 def test_block_results_vs_oracle(oracle, dist, seed, R, B, engine):
     """Blocks may differ from the reference only where the tensor core's internal fp32 sum of a
     column lands on the other side of a binary16 rounding boundary of C_R: one binary16 ulp
@@ -123,10 +123,15 @@ def test_block_results_vs_oracle(oracle, dist, seed, R, B, engine):
     print(f"\n{engine.name} {dist} R={R} B={B}: bit-identical blocks {frac:.6f}, max rel diff {rel:.3e}, "
           f"max abs diff {diff:.3e}")
     if dist == "uniform":
-        assert rel <= 2.0 ** -20
+        # a flipped binary16 rounding of one column sum moves a block by one binary16 ulp of that
+        # sum (column sums of uniform[0,1) data are < 16 R); below R = 6 none was ever measured
+        ulp16 = 2.0 ** (math.floor(math.log2(16 * R)) - 10)
+        assert rel <= 2.0 ** -20 or (R > 5 and diff <= ulp16)
     else:
         assert diff <= 2.0 ** -4
-    assert frac >= 0.99
+    # longer chains (R > 5) sum more values per column before the binary16 rounding, so a block
+    # (32 x 16 rounded partials at B = 1024) flips more often: >= 90 % bit-identical there
+    assert frac >= (0.99 if R <= 5 else 0.9)
 
 
 @pytest.mark.parametrize("R,B", [(1, 1024), (4, 128), (3, 96), (5, 32), (2, 256)])
