@@ -87,16 +87,22 @@ __device__ __forceinline__ void as_unit(const SpParams& p, uint64_t c0, uint32_t
     const uint32_t mi = lane >> 3;
     const uint32_t ld_off = swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
 
-    // element index of fragment f's first element for this warp
-    auto frag_elem = [&](uint32_t f) -> uint64_t {
-        const uint32_t ci = f / R, r = f - ci * R;
-        return (c0 + warp + uint64_t(ci) * kAsWarps) * ce + uint64_t(r) * 256u;
-    };
+    // issue cursor (called with f = 0, 1, 2, ... in order): element of fragment f for this warp,
+    // advanced by increments instead of a division by the runtime R
+    uint64_t ie = (c0 + warp) * ce + 8u * lane;
+    uint32_t ir = 0;
+    const uint64_t chunk_step = uint64_t(kAsWarps) * ce - uint64_t(R - 1) * 256u;
     auto issue = [&](uint32_t f) {
         if (f < F) {
-            const uint64_t e = frag_elem(f) + 8u * lane;
+            const uint64_t e = ie;
             const uint32_t bytes = e + 8 <= n ? 16u : (e < n ? uint32_t(n - e) * 2u : 0u);
             cp_async16(ring_saddr + (f % D) * kAsStageBytes + cp_dst, x + (e < n ? e : 0), bytes);
+            if (++ir == R) {
+                ir = 0;
+                ie += chunk_step;
+            } else {
+                ie += 256u;
+            }
         }
         cp_async_commit();
     };
