@@ -313,5 +313,30 @@ __device__ __forceinline__ void tile_tree_group(const SpParams& p, uint64_t tile
     if (lane == 0) p.group_partials[tile] = x;
 }
 
+// The same group tree by a whole 8-warp CTA (every thread calls): thread t reduces blocks
+// [t seg, (t+1) seg) with the register segment tree, the warps' xor trees pair adjacent lanes,
+// thread 0 pairs the 8 warp results.  One eighth of the serial work per thread of the one-warp
+// version, which matters when G is large (B = 32: G = 1024 blocks per group).
+template <bool GLOBAL = false>
+__device__ __forceinline__ void tile_tree_group_cta(const SpParams& p, uint64_t tile, const float* blocks) {
+    __shared__ float s_w[8];
+    const uint32_t G = p.G;
+    const uint32_t seg = G >= 256u ? G / 256u : 1u;
+    const uint32_t lo = threadIdx.x * seg;
+    auto ld = [&](uint32_t i) -> float {
+        if constexpr (GLOBAL) return __ldcg(blocks + i);
+        else return blocks[i];
+    };
+    float x = lo < G ? lane_segment_tree(ld, lo, seg) : 0.0f;
+    x = warp_tree_xor(x);
+    if (lane_id() == 0) s_w[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0 && p.group_partials) {
+        const float a = (s_w[0] + s_w[1]) + (s_w[2] + s_w[3]);
+        const float b = (s_w[4] + s_w[5]) + (s_w[6] + s_w[7]);
+        p.group_partials[tile] = a + b;
+    }
+}
+
 }  // namespace pipe
 }  // namespace tcr

@@ -342,17 +342,23 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
         range_trees_blocks(p, b0, Gu, s_chunk, s_block, warp, kAsWarps);
         __syncthreads();
         if (S == 1) {
-            if (warp == 0) tile_tree_group(p, gi, s_block);
+            // large groups (B = 32: G = 1024) by the whole CTA, small ones by one warp (no barrier)
+            if (G >= 256) tile_tree_group_cta(p, gi, s_block);
+            else if (warp == 0) tile_tree_group(p, gi, s_block);
         } else {
             for (uint32_t b = threadIdx.x; b < Gu; b += kAsThreads) p.block_scratch[b0 + b] = s_block[b];
             __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) s_glast = atomicAdd(p.group_count + gi, 1u) == S - 1;
             __syncthreads();
-            if (s_glast && warp == 0) {
+            if (s_glast) {
                 __threadfence();
-                tile_tree_group<true>(p, gi, p.block_scratch + gi * G);
-                if (lane_id() == 0) p.group_count[gi] = 0u;
+                if (G >= 256) {
+                    tile_tree_group_cta<true>(p, gi, p.block_scratch + gi * G);
+                } else if (warp == 0) {
+                    tile_tree_group<true>(p, gi, p.block_scratch + gi * G);
+                }
+                if (threadIdx.x == 0) p.group_count[gi] = 0u;
             }
         }
         __syncthreads();
