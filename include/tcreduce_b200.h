@@ -173,6 +173,13 @@ int tcr_cub_sum_f16_async(const uint16_t* d_x, size_t n, int half_accumulator, v
 /* Streaming-read probe over `bytes` of device memory (bandwidth ceiling). */
 int tcr_read_probe_async(const void* d_x, size_t bytes, void* cuda_stream);
 
+/* Workspaces (partials, pipeline rings, pinned readback) are created per (device, stream) on
+ * first use and reused.  tcr_release_stream frees the one bound to `cuda_stream` on the current
+ * device; tcr_release_all frees every one (no call may be in flight).  A host thread's private
+ * workspaces (the host-buffer entry points) are freed when the thread exits. */
+int tcr_release_stream(void* cuda_stream);
+int tcr_release_all(void);
+
 /* Number of kernels the last single_pass call on this thread launched (launch accounting). */
 int tcr_last_launch_count(void);
 /* Engine (tcr_engine) that reduced the full groups in the last single_pass call on this thread. */

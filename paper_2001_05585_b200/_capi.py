@@ -62,6 +62,8 @@ SIGNATURES = {
     "tcr_cub_sum_f16_async": (C.c_int, [_P, _SZ, C.c_int, _P, _P]),
     "tcr_read_probe_async": (C.c_int, [_P, _SZ, _P]),
     "tcr_last_launch_count": (C.c_int, []),
+    "tcr_release_stream": (C.c_int, [_P]),
+    "tcr_release_all": (C.c_int, []),
     "tcr_last_engine": (C.c_int, []),
     "tcr_last_error": (C.c_char_p, []),
     "tcr_version": (C.c_char_p, []),

@@ -109,6 +109,23 @@ struct Workspace {
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 
+    // Free every device / pinned buffer, stream and event (the owner guarantees no work in flight).
+    void release() {
+        auto f = [](auto*& ptr) {
+            if (ptr) cudaFree(ptr);
+            ptr = nullptr;
+        };
+        f(group_partials); f(block_partials); f(order); f(fixed); f(exact_ws); f(shuffle_partials); f(cub_temp);
+        f(conv); f(tree_cols); f(dpart); f(lvl_f32); f(lvl16[0]); f(lvl16[1]); f(block_scratch); f(group_count);
+        f(work_counter); f(stage); f(ring[0]); f(ring[1]); f(ring16[0]); f(ring16[1]);
+        if (host_pinned) cudaFreeHost(host_pinned);
+        host_pinned = nullptr;
+        for (cudaEvent_t* e : {&copied[0], &copied[1], &consumed[0], &consumed[1], &fork, &join})
+            if (*e) cudaEventDestroy(*e), *e = nullptr;
+        for (cudaStream_t* st : {&copy_stream, &aux_stream})
+            if (*st) cudaStreamDestroy(*st), *st = nullptr;
+    }
+
     float* result() { return reinterpret_cast<float*>(fixed); }
     uint32_t* overflow() { return reinterpret_cast<uint32_t*>(fixed + 4); }
     uint32_t* ticket() { return reinterpret_cast<uint32_t*>(fixed + 8); }
@@ -122,8 +139,50 @@ struct Workspace {
 
 std::mutex g_mu;
 std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+std::vector<std::pair<int, cudaStream_t>> g_reap;   // host streams of exited threads
+
+// Release the workspace bound to (device, stream), if any (no work may be in flight on it).
+void release_ws(int dev, cudaStream_t s) {
+    Workspace* w = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_ws.find({dev, s});
+        if (it == g_ws.end()) return;
+        w = it->second;
+        g_ws.erase(it);
+    }
+    if (w) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        cudaStreamSynchronize(s);
+        w->release();
+        delete w;
+        cudaSetDevice(cur);
+    }
+}
+
+void reap_exited_threads() {
+    std::vector<std::pair<int, cudaStream_t>> todo;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (g_reap.empty()) return;
+        todo.swap(g_reap);
+    }
+    for (auto& [dev, st] : todo) {
+        release_ws(dev, st);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        cudaStreamDestroy(st);
+        cudaSetDevice(cur);
+    }
+}
+
+void reap_exited_threads();
 
 int get_ws(cudaStream_t s, Workspace** out) {
+    reap_exited_threads();
     int dev = 0;
     TCR_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
@@ -696,6 +755,24 @@ int tcr_validate(const tcr_config* c) { return validate_cfg(c); }
 const char* tcr_last_error(void) { return g_err.c_str(); }
 const char* tcr_version(void) { return "tcreduce-b200 0.1 (sm_100a)"; }
 int tcr_last_launch_count(void) { return g_launches; }
+
+int tcr_release_stream(void* stream) {
+    int dev = 0;
+    TCR_CUDA(cudaGetDevice(&dev));
+    release_ws(dev, static_cast<cudaStream_t>(stream));
+    return TCR_OK;
+}
+
+int tcr_release_all(void) {
+    reap_exited_threads();
+    std::vector<std::pair<int, cudaStream_t>> keys;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        for (auto& kv : g_ws) keys.push_back(kv.first);
+    }
+    for (auto& k : keys) release_ws(k.first, k.second);
+    return TCR_OK;
+}
 int tcr_last_engine(void) { return g_engine; }
 // Profiling hook (not in the public header): timestamps of the last TCR_DEBUG_MODE=20 launch of
 // the cp.async engine, 4 per CTA (start, streaming done, after finalise, is-last).
@@ -880,8 +957,20 @@ namespace {
 // Host-input calls run on a per-thread, per-device stream, so concurrent callers on different
 // host threads get separate workspaces (the reference's reduce() is reentrant,
 // reduction.hpp:19-21).
+struct HostStreams {
+    std::map<int, cudaStream_t> m;
+    // A host thread's streams and their workspaces (ring buffers of ~384 MiB) go with the
+    // thread: at thread exit they are queued (no CUDA call from a thread-exit handler, where the
+    // runtime's own per-thread state may already be gone) and the next API call frees them.
+    ~HostStreams() {
+        std::lock_guard<std::mutex> lk(g_mu);
+        for (auto& kv : m) g_reap.push_back(kv);
+    }
+};
+
 int host_stream(cudaStream_t* out) {
-    thread_local std::map<int, cudaStream_t> streams;
+    thread_local HostStreams hs;
+    auto& streams = hs.m;
     int dev = 0;
     TCR_CUDA(cudaGetDevice(&dev));
     auto& st = streams[dev];

@@ -9,6 +9,7 @@ Tolerances:
   * uniform: |gpu - exact| / |exact| <= 1e-5 and |gpu - ref_single_pass| / |exact| <= 2e-5;
   * normal: |gpu - exact| / sum|x| <= 1e-6.
 """
+import ctypes as C
 import json
 import math
 import os
@@ -718,3 +719,31 @@ def test_async_single_pass_is_graph_capturable(oracle, m, R, B):
         torch.cuda.synchronize()
         assert res.item() == eager
     assert eager == T.reduce(x, cfg).value
+
+
+def test_workspaces_are_released(oracle):
+    """A host thread's private workspace (pipeline rings) is freed when the thread exits, and
+    tcr_release_all / tcr_release_stream free the rest; calls afterwards recreate what they need."""
+    import threading
+    from paper_2001_05585_b200 import _capi
+    h = oracle.generate_f16("uniform", 8, (1 << 25) + 3)   # > one 32 Mi pipeline chunk
+    cfg = T.ReductionConfig(m=16, R=1, B=1024)
+    want = T.reduce(h.view(np.float16), cfg).value
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    out = []
+    t = threading.Thread(target=lambda: out.append(T.reduce(h.view(np.float16), cfg).value))
+    t.start()
+    t.join()
+    T.reduce(to_dev_f16(h[:4096]), cfg)                     # the next call frees the exited thread's
+    torch.cuda.synchronize()                                # workspace (~384 MiB of pipeline rings)
+    free1, _ = torch.cuda.mem_get_info()
+    assert out == [want]
+    assert free0 - free1 < (64 << 20), (free0, free1)
+    lib = _capi.load()
+    st = torch.cuda.Stream(device=DEV)
+    with torch.cuda.stream(st):
+        v = T.reduce(to_dev_f16(h), cfg).value
+    _capi.check(lib.tcr_release_stream(C.c_void_p(st.cuda_stream)))
+    _capi.check(lib.tcr_release_all())
+    assert T.reduce(h.view(np.float16), cfg).value == want == v
