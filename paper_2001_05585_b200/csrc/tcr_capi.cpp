@@ -99,6 +99,8 @@ struct Workspace {
     size_t wc_cap = 0;
     float* stage = nullptr;  // host path of the non-single_pass variants
     size_t stage_cap = 0;
+    float* unaligned = nullptr;  // aligned copy of a device input that is not 16-byte aligned
+    size_t unaligned_cap = 0;
     // pipelined host path
     float* ring[2] = {nullptr, nullptr};
     uint16_t* ring16[2] = {nullptr, nullptr};
@@ -117,7 +119,7 @@ struct Workspace {
         };
         f(group_partials); f(block_partials); f(order); f(fixed); f(exact_ws); f(shuffle_partials); f(cub_temp);
         f(conv); f(tree_cols); f(dpart); f(lvl_f32); f(lvl16[0]); f(lvl16[1]); f(block_scratch); f(group_count);
-        f(work_counter); f(stage); f(ring[0]); f(ring[1]); f(ring16[0]); f(ring16[1]);
+        f(work_counter); f(stage); f(unaligned); f(ring[0]); f(ring[1]); f(ring16[0]); f(ring16[1]);
         if (host_pinned) cudaFreeHost(host_pinned);
         host_pinned = nullptr;
         for (cudaEvent_t* e : {&copied[0], &copied[1], &consumed[0], &consumed[1], &fork, &join})
@@ -412,6 +414,18 @@ int enqueue_finalize(uint64_t n, const tcr_config* c, float* d_result, Workspace
     return TCR_OK;
 }
 
+// The kernels stream 16-byte lines: an input that does not start on a 16-byte boundary (e.g. a
+// tensor slice; the reference takes any span) is first copied into an aligned workspace buffer.
+int aligned_input(const void** d_x, size_t n, bool f32, Workspace* w, cudaStream_t s) {
+    if (reinterpret_cast<uintptr_t>(*d_x) % 16 == 0) return TCR_OK;
+    const size_t bytes = n * (f32 ? 4 : 2);
+    int rc = ensure(&w->unaligned, &w->unaligned_cap, (bytes + 3) / 4, s);
+    if (rc) return rc;
+    TCR_CUDA(cudaMemcpyAsync(w->unaligned, *d_x, bytes, cudaMemcpyDeviceToDevice, s));
+    *d_x = w->unaligned;
+    return TCR_OK;
+}
+
 int sp_async(const void* d_x, size_t n, const tcr_config* c, bool f32, float* d_result, uint32_t* d_overflow,
              cudaStream_t s) {
     g_launches = 0;
@@ -421,10 +435,10 @@ int sp_async(const void* d_x, size_t n, const tcr_config* c, bool f32, float* d_
     rc = check_supported(c);
     if (rc) return rc;
     if (!d_x || !d_result || !d_overflow) return fail(TCR_INVALID_ARGUMENT, "null device pointer");
-    if (reinterpret_cast<uintptr_t>(d_x) % (f32 ? 32 : 16) != 0)
-        return fail(TCR_INVALID_ARGUMENT, "device input must be 16-byte (binary16) / 32-byte (fp32) aligned");
     Workspace* w = nullptr;
     rc = get_ws(s, &w);
+    if (rc) return rc;
+    rc = aligned_input(&d_x, n, f32, w, s);
     if (rc) return rc;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
     if (f32 && c->m != 16) {
@@ -717,6 +731,10 @@ int reduce_device(const void* d_x, size_t n, const tcr_config* c, tcr_outcome* o
     if (rc) return rc;
     if (c->variant != TCR_SINGLE_PASS) {
         g_launches = 0;
+        if (n > 0 && d_x) {
+            rc = aligned_input(&d_x, n, f32, w, s);
+            if (rc) return rc;
+        }
         return run_variant(d_x, f32, n, c, out, w, s);
     }
     TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));

@@ -747,3 +747,18 @@ def test_workspaces_are_released(oracle):
     _capi.check(lib.tcr_release_stream(C.c_void_p(st.cuda_stream)))
     _capi.check(lib.tcr_release_all())
     assert T.reduce(h.view(np.float16), cfg).value == want == v
+
+
+@pytest.mark.parametrize("variant", ["single_pass", "recurrence", "split", "shuffle32", "half_tree", "oracle64"])
+@pytest.mark.parametrize("dtype", ["float16", "float32"])
+def test_unaligned_device_input(oracle, variant, dtype):
+    """A device input that does not start on a 16-byte boundary (a tensor slice; the reference
+    takes any span) gives the same result as the same values aligned."""
+    h = oracle.generate_f16("normal", 9, (1 << 21) + 5)
+    base = to_dev_f16(h) if dtype == "float16" else to_dev_f16(h).float()
+    sl = base[3:]                                   # 6 / 12 bytes off a 16-byte boundary
+    assert sl.data_ptr() % 16 != 0
+    cfg = T.ReductionConfig(variant=T.Variant[variant], m=4, R=2, B=128)
+    a = T.reduce(sl, cfg)
+    b = T.reduce(sl.clone(), cfg)
+    assert a.value == b.value and a.overflow == b.overflow
