@@ -208,7 +208,9 @@ int ensure(T** p, size_t* cap, size_t count, cudaStream_t s) {
     if (*p) TCR_CUDA(cudaFree(*p));
     *p = nullptr;
     const size_t want = std::max<size_t>(count, 1024);
-    TCR_CUDA(cudaMalloc(reinterpret_cast<void**>(p), want * sizeof(T)));
+    // +16 bytes: a ragged tail's last 16-byte copy line (partial, zero-filled past n) stays
+    // inside the allocation even when it starts at the last element
+    TCR_CUDA(cudaMalloc(reinterpret_cast<void**>(p), want * sizeof(T) + 16));
     *cap = want;
     return TCR_OK;
 }
@@ -1049,10 +1051,10 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
         if (w->copy_stream) TCR_CUDA(cudaStreamSynchronize(w->copy_stream));
         for (auto& r : w->ring)
             if (r) TCR_CUDA(cudaFree(r));
-        for (auto& r : w->ring) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(float)));
+        for (auto& r : w->ring) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(float) + 16));
         for (auto& r : w->ring16)
             if (r) TCR_CUDA(cudaFree(r));
-        for (auto& r : w->ring16) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(uint16_t)));
+        for (auto& r : w->ring16) TCR_CUDA(cudaMalloc(&r, ring_elems * sizeof(uint16_t) + 16));
         w->ring_cap = ring_elems;
     }
     if (!w->copy_stream) {
