@@ -16,6 +16,7 @@
 //                 partial(j) = D[j][n] + D[j+8][n];
 //   m in {32,64,128}  transposed tiles, B[t][n] = [t mod (m/16) == n], partial(16n + j) = D[j][n],
 //                 accumulated over the chunk's R*(m/16)^2 tiles.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -25,6 +26,8 @@
 #include "tcr_pipeline.cuh"
 
 namespace tcr {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -678,6 +681,139 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
 }
 
+// ======================================= wide fragments, m >= 1024: a CLUSTER of CS CTAs per chunk
+// As gm_wide_cta_kernel, but the chunk's rows are split over the CS CTAs of a thread-block
+// cluster (CS x 8 warps, each a contiguous row range): every CTA adds its 8 warp partials per
+// column, and the cluster's rank 0 adds the CS CTA column sums in rank order through distributed
+// shared memory (cluster.map_shared_rank), then rounds and sums as before.  2^28 elements are
+// only 256 chunks at m = 1024: one CTA per chunk left most SMs idle.
+template <int SL, bool REPAIR>
+__global__ void __launch_bounds__(kGmThreads) gm_wide_cluster_kernel(const SpParams p, const uint32_t m) {
+    constexpr int D = kGmTrDepth;
+    extern __shared__ __align__(128) unsigned char s_ring[];   // ring | part[8][m] | cta[m] | tables
+    __shared__ float s_scratch[32];
+    __shared__ float s_wsum[kGmWarps];
+    __shared__ int s_last;
+    cg::cluster_group cluster = cg::this_cluster();
+    const uint32_t CS = cluster.num_blocks();
+    const uint32_t rank = cluster.block_rank();
+    const uint64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    float* s_part = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
+    float* s_cta = s_part + kGmWarps * m;                       // this CTA's column sums
+    float* s_chunk = s_cta + m;
+    const uint32_t Cg = p.G * p.W;
+    float* s_block = s_chunk + Cg;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned g = lane >> 2, c = lane & 3u;
+    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    const uint64_t rows = uint64_t(p.R) * m;
+    const uint64_t chunk_el = rows * m;
+    const uint64_t rpw = rows / (uint64_t(kGmWarps) * CS);     // rows of this warp per chunk
+    const uint64_t span = rpw * m;
+    const uint64_t w_off = (uint64_t(rank) * kGmWarps + warp) * span;
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint32_t blo0 = sel2(2 * c == g, 2 * c + 1 == g), blo1 = sel2(2 * c + 8 == g, 2 * c + 9 == g);
+    const uint32_t bhi0 = sel2(2 * c == g + 8, 2 * c + 1 == g + 8), bhi1 = sel2(2 * c + 8 == g + 8, 2 * c + 9 == g + 8);
+    auto swz = [](uint32_t k, uint32_t h) { return 32u * k + 16u * (h ^ ((k >> 2) & 1u)); };
+    const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
+    const uint32_t mi = lane >> 3;
+    const uint32_t ld_off = swz((lane & 7u) + 8u * (mi >> 1), mi & 1u);
+    bool ovf = false;
+
+    for (uint64_t gi = p.group_begin + cid; gi < p.group_end; gi += ncl) {
+        const uint64_t gel0 = gi * uint64_t(Cg) * chunk_el;
+        uint32_t iit = 0, islot = 0;
+        uint64_t ioff = 0;                                         // issue cursor (chunk, offset)
+        auto issue = [&]() {
+            if (iit < Cg) {
+                const uint64_t e = gel0 + uint64_t(iit) * chunk_el + w_off + ioff + 8u * lane;
+                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                cp16(ring + islot * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+                ioff += 256u;
+                if (ioff == span) {
+                    ioff = 0;
+                    ++iit;
+                }
+            }
+            cp_commit();
+            islot = islot + 1 == uint32_t(D) ? 0 : islot + 1;
+        };
+#pragma unroll 1
+        for (int f = 0; f < D - 1; ++f) issue();
+        uint32_t cslot = 0;
+        for (uint32_t it = 0; it < Cg; ++it) {
+            float acc[SL][2][4];
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[sl][0][q] = acc[sl][1][q] = 0.f;
+            for (uint64_t r = 0; r < rpw; ++r) {
+#pragma unroll
+                for (int sl = 0; sl < SL; ++sl) {
+                    issue();
+                    cp_wait<D - 1>();
+                    __syncwarp();
+                    uint32_t d0, d1, d2, d3;
+                    ldsm4t(ring + cslot * 512u + ld_off, d0, d1, d2, d3);
+                    __syncwarp();
+                    cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
+                    mma_16816(acc[sl][0], d0, d1, d2, d3, blo0, blo1);
+                    mma_16816(acc[sl][1], d0, d1, d2, d3, bhi0, bhi1);
+                }
+            }
+            // warp partials: D[j16][n] = column 256 sl + 16 n + j16 (n + 8 for the hi half)
+            float* part = s_part + warp * m;
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t col0 = 256u * sl + 128u * hh;
+                    part[col0 + 16 * (2 * c) + g] = acc[sl][hh][0];
+                    part[col0 + 16 * (2 * c + 1) + g] = acc[sl][hh][1];
+                    part[col0 + 16 * (2 * c) + g + 8] = acc[sl][hh][2];
+                    part[col0 + 16 * (2 * c + 1) + g + 8] = acc[sl][hh][3];
+                }
+            __syncthreads();
+            // this CTA's column sums (8 warp partials in warp order) -> s_cta, visible cluster-wide
+            for (uint32_t col = threadIdx.x; col < m; col += kGmThreads) {
+                float cs = 0.0f;
+#pragma unroll
+                for (int w = 0; w < kGmWarps; ++w) cs = cs + s_part[w * m + col];
+                s_cta[col] = cs;
+            }
+            cluster.sync();
+            if (rank == 0) {
+                // the cluster's CTAs in rank order through distributed shared memory
+                float t = 0.0f;
+                for (uint32_t col = threadIdx.x; col < m; col += kGmThreads) {
+                    float cs = 0.0f;
+                    for (uint32_t q = 0; q < CS; ++q) cs = cs + cluster.map_shared_rank(s_cta, q)[col];
+                    t = t + h_round(cs);
+                }
+                t = warp_tree_xor(t);
+                if (lane == 0) s_wsum[warp] = t;
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    float r = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < kGmWarps; ++w) r = r + s_wsum[w];
+                    r = r + 0.0f;
+                    ovf |= !isfinite(r);
+                    s_chunk[it] = r;
+                }
+            }
+            cluster.sync();                     // s_cta is reused by the next chunk
+        }
+        cp_wait<0>();
+        if (rank == 0) group_epilogue<REPAIR>(p, gi, s_chunk, s_block, m, ovf);
+    }
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+    __threadfence();
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
+}
+
+
 uint32_t gcd32(uint32_t a, uint32_t b) {
     while (b) {
         const uint32_t t = a % b;
@@ -749,6 +885,35 @@ cudaError_t launch_gm(K fn, uint32_t dyn, uint64_t groups, const SpParams& p, co
     fn<<<grid, kGmThreads, dyn, s>>>(p, shape);
     return cudaGetLastError();
 }
+
+// Thread-block-cluster launch (CS CTAs per cluster, one group of chunks per cluster at a time).
+template <typename K>
+cudaError_t launch_cluster(K fn, uint32_t dyn, uint64_t groups, uint32_t CS, const SpParams& p, uint32_t m,
+                           cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kGmThreads, 1, 1);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(CS, 1, 1);
+    int max_clusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg);
+    if (e != cudaSuccess) return e;
+    if (max_clusters < 1) max_clusters = 1;
+    const uint64_t ncl = groups < uint64_t(max_clusters) ? groups : uint64_t(max_clusters);
+    cfg.gridDim = dim3(unsigned(ncl * CS), 1, 1);
+    e = cudaLaunchKernelEx(&cfg, fn, p, m);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
 }  // namespace
 
 template <bool REPAIR>
@@ -782,8 +947,14 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
             switch (g.m) {
             case 256: return launch_gm(gm_wide_cta_kernel<1, REPAIR>, dyn, groups, p, g.m, s);
             case 512: return launch_gm(gm_wide_cta_kernel<2, REPAIR>, dyn, groups, p, g.m, s);
-            case 1024: return launch_gm(gm_wide_cta_kernel<4, REPAIR>, dyn, groups, p, g.m, s);
-            default: return launch_gm(gm_wide_cta_kernel<8, REPAIR>, dyn, groups, p, g.m, s);
+            case 1024:
+                if (!std::getenv("TCR_GM_NO_CLUSTER"))   // knob: profiling A/B
+                    return launch_cluster(gm_wide_cluster_kernel<4, REPAIR>, dyn + g.m * 4u, groups, 4, p, g.m, s);
+                return launch_gm(gm_wide_cta_kernel<4, REPAIR>, dyn, groups, p, g.m, s);
+            default:
+                if (!std::getenv("TCR_GM_NO_CLUSTER"))
+                    return launch_cluster(gm_wide_cluster_kernel<8, REPAIR>, dyn + g.m * 4u, groups, 8, p, g.m, s);
+                return launch_gm(gm_wide_cta_kernel<8, REPAIR>, dyn, groups, p, g.m, s);
             }
         }
         return launch_gm(gm_wide_kernel<REPAIR>, ring + tables, groups, p, g.m, s);
