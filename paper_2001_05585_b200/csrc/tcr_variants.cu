@@ -15,6 +15,7 @@
 // phases repeat (K = 16: P -> P/16) until <= 64 Ki values remain, which one CTA finishes
 // (per-thread binary-counter stacks in bit-reversed row order, then the in-shared-memory
 // strided levels).  Zero padding is implicit (loads beyond n read 0).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "tcr_device.cuh"
@@ -142,6 +143,34 @@ __global__ void __launch_bounds__(kRowThreads) tree_rows_kernel(const T* x, uint
 #pragma unroll
         for (int k = 0; k < kRowK; ++k) r[k] = row[k * kRowThreads];
         float res[CW];
+        if constexpr (sizeof(T) == 2 && HALF) {
+            // half_tree on binary16 input: from_single(a + b) of two binary16 values equals the
+            // native round-to-nearest binary16 add (an fp32 intermediate has 24 >= 2*11 + 2
+            // significand bits, so the double rounding is innocuous), and inf / NaN propagate to
+            // the column result, so packed HADD2 trees reproduce the reference bit for bit and a
+            // non-finite column result is exactly "some partial overflowed" (:136-146).
+            __half2 hv[kRowK][4];
+#pragma unroll
+            for (int k = 0; k < kRowK; ++k) {
+                hv[k][0] = *reinterpret_cast<const __half2*>(&r[k].x);
+                hv[k][1] = *reinterpret_cast<const __half2*>(&r[k].y);
+                hv[k][2] = *reinterpret_cast<const __half2*>(&r[k].z);
+                hv[k][3] = *reinterpret_cast<const __half2*>(&r[k].w);
+            }
+#pragma unroll
+            for (int h = kRowK / 2; h >= 1; h >>= 1)
+#pragma unroll
+                for (int k = 0; k < h; ++k)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) hv[k][q] = __hadd2(hv[k][q], hv[k + h][q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __half22float2(hv[0][q]);
+                res[2 * q] = f.x;
+                res[2 * q + 1] = f.y;
+                ovf |= !isfinite(f.x) || !isfinite(f.y);
+            }
+        } else
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
             float v[kRowK];
