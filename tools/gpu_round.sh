@@ -25,4 +25,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc05_kernel -s 2 -c 1 \
      -o $OUT/tc05 python bench.py --steps 2 --warmup 2 --no-e2e --no-cpu --no-comparators --engine 2 > $OUT/ncu_tc05.log 2>&1
 fi
+timeout 600 python tools/f32_probe.py > $OUT/f32_probe.txt 2>&1
+timeout 300 python tools/timeline.py > $OUT/timeline.txt 2>&1
+timeout 300 python tools/size_scan.py > $OUT/size_scan.txt 2>&1
 echo done > $OUT/DONE
