@@ -8,6 +8,7 @@
 #include "tcreduce_b200.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -33,6 +34,13 @@ thread_local int g_launches = 0;
 thread_local int g_engine = 0;  // engine that ran the full groups of the last call
 // m != 16 engines: use the NaN-repairing instantiations (tcr_sp_genm.cu, group_epilogue)
 thread_local bool g_repair = false;
+
+// NVTX range around each public entry point (visible in nsys / ncu range filters; no cost when
+// no tool is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct RepairScope {
     bool prev;
@@ -818,6 +826,7 @@ int tcr_single_pass_counters(size_t n, const tcr_config* c, tcr_outcome* out) {
 
 int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_result,
                               uint32_t* d_overflow, void* stream) {
+    NvtxRange nvtx_("tcr_single_pass_f16_async");
     // The result stays on the device, so there is no retry: on a selector engine (m != 16) a
     // non-finite input can surface as NaN where the reference has +-inf (the overflow flag is
     // exact either way).  The synchronous entry points re-run such calls with the repairing
@@ -827,14 +836,17 @@ int tcr_single_pass_f16_async(const uint16_t* d_x, size_t n, const tcr_config* c
 
 int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* c, float* d_result,
                               uint32_t* d_overflow, void* stream) {
+    NvtxRange nvtx_("tcr_single_pass_f32_async");
     return sp_async(d_x, n, c, true, d_result, d_overflow, static_cast<cudaStream_t>(stream));
 }
 
 int tcr_reduce_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
+    NvtxRange nvtx_("tcr_reduce_f16_device");
     return with_nan_retry(c, out, [&] { return reduce_device(d_x, n, c, out, false, static_cast<cudaStream_t>(stream)); });
 }
 
 int tcr_reduce_f32_device(const float* d_x, size_t n, const tcr_config* c, tcr_outcome* out, void* stream) {
+    NvtxRange nvtx_("tcr_reduce_f32_device");
     return with_nan_retry(c, out, [&] { return reduce_device(d_x, n, c, out, true, static_cast<cudaStream_t>(stream)); });
 }
 
@@ -876,6 +888,7 @@ extern "C" {
 
 int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const int32_t* devices, int32_t ngpu,
                            const tcr_config* c, tcr_outcome* out) {
+    NvtxRange nvtx_("tcr_reduce_f16_sharded");
     RepairScope rs(c && c->m != 16);   // one combined result: repair up front
     g_launches = 0;
     if (!out) return fail(TCR_INVALID_ARGUMENT, "null outcome");
@@ -956,6 +969,7 @@ int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const in
 
 int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_blocks,
                                  void* stream) {
+    NvtxRange nvtx_("tcr_block_results_f16_device");
     RepairScope rs(c && c->m != 16);   // parity hook: per-block values exact for non-finite data too
     g_launches = 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1108,11 +1122,13 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
 }  // namespace
 
 int tcr_reduce_f32_host(const float* x, size_t n, const tcr_config* c, tcr_outcome* out) {
+    NvtxRange nvtx_("tcr_reduce_f32_host");
     // Drop-in for reduce(std::span<const float>, cfg)
     return with_nan_retry(c, out, [&] { return reduce_host(x, true, n, c, out); });
 }
 
 int tcr_reduce_f16_host(const uint16_t* x, size_t n, const tcr_config* c, tcr_outcome* out) {
+    NvtxRange nvtx_("tcr_reduce_f16_host");
     return with_nan_retry(c, out, [&] { return reduce_host(x, false, n, c, out); });
 }
 
