@@ -346,7 +346,7 @@ GENM = [(2, 1, 128), (2, 2, 64), (2, 4, 32), (4, 1, 128), (4, 4, 128), (4, 3, 96
         # R > 16: several row-block stages per period), wide fragments (m >= 256: column slabs)
         (2, 3, 128), (2, 5, 32), (2, 6, 96), (2, 7, 64), (2, 20, 32), (2, 68, 64), (4, 17, 32), (4, 33, 64),
         (8, 3, 128), (8, 5, 32), (8, 6, 64), (8, 7, 256), (8, 10, 32), (256, 1, 32), (256, 3, 64),
-        (512, 1, 32), (1024, 1, 32)]
+        (512, 1, 32), (1024, 1, 32), (1024, 2, 64), (2048, 1, 32)]
 
 
 @pytest.mark.parametrize("m,R,B", GENM)
@@ -762,3 +762,30 @@ def test_unaligned_device_input(oracle, variant, dtype):
     a = T.reduce(sl, cfg)
     b = T.reduce(sl.clone(), cfg)
     assert a.value == b.value and a.overflow == b.overflow
+
+
+@pytest.mark.parametrize("m,R,B", [(1024, 1, 32), (1024, 1, 128), (2048, 1, 32), (1024, 3, 64)])
+@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1), ("integers", 2)])
+def test_cluster_engine_many_chunks(oracle, m, R, B, dist, seed):
+    """The thread-block-cluster engine (m = 1024, 2048) over several groups and a ragged tail:
+    block results against the reference (integers exact; otherwise one binary16 ulp of a column
+    sum per differing block), value within the single-pass bars."""
+    n = 3 * (1 << 21) + 12345
+    h = oracle.generate("integers", seed, n).astype(np.float16).view(np.uint16) if dist == "integers" \
+        else oracle.generate_f16(dist, seed, n)
+    xd = to_dev_f16(h)
+    cfg = T.ReductionConfig(m=m, R=R, B=B)
+    _, ref_blocks = oracle.single_pass(h, threads=8, want_blocks=True, m=m, R=R, B=B)
+    got = T.block_results(xd, cfg).cpu().numpy()
+    d = np.abs(got.astype(np.float64) - ref_blocks)
+    hf = np.abs(h.view(np.float16).astype(np.float64))
+    be = (B // 32) * R * m * m
+    babs = np.add.reduceat(hf, np.arange(0, hf.size, be))
+    if dist == "integers" and 9 * R * m <= 2048:
+        assert np.array_equal(got.view(np.uint32), ref_blocks.view(np.uint32))
+    assert np.all(d <= 2.0 ** -10 * babs + 1e-30), (d, babs)
+    ref = oracle.single_pass(h, threads=8, m=m, R=R, B=B)
+    o = T.reduce(xd, cfg)
+    exact, absum = oracle.exact_sum_f16(h)
+    assert abs(o.value - ref.value) <= max(2e-5 * abs(exact), 1e-6 * absum)
+    assert o.atomic_count == ref.atomic_count and o.mma_count == ref.mma_count
