@@ -46,6 +46,12 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32
     else
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
 }
+// Same copy with an L2 eviction-priority policy (the streamed input is read exactly once).
+__device__ __forceinline__ void cp_async16_pol(uint32_t saddr, const void* g, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint.L2::256B [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g),
+                 "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -183,9 +189,11 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
     // global element offset of warp-local fragment f (chunk f/RT, fragment f%RT)
 #define TCR_FRAG_OFF(f) (uint64_t((f) / RT) * kAsWarps * CE + uint64_t((f) % RT) * 256u)
     constexpr uint64_t ITB = uint64_t(CPI) * kAsWarps * CE;     // elements per outer iteration
+    uint64_t pol = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
     for (int u = 0; u < D - 1; ++u) {
-        cp_async16(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), 16u);
+        cp_async16_pol(cp_dst + u * kAsStageBytes, gp + TCR_FRAG_OFF(u), pol);
         cp_async_commit();
     }
     float* out = s_chunk + warp;
@@ -197,7 +205,7 @@ __device__ __forceinline__ void as_unit_static(const SpParams& p, uint64_t c0, u
         for (int u = 0; u < D; ++u) {
             // refill the stage consumed one step ago with fragment it*D + u + D-1
             if (it + 1 < iters || u == 0)
-                cp_async16(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + TCR_FRAG_OFF(u + D - 1), 16u);
+                cp_async16_pol(cp_dst + ((u + D - 1) % D) * kAsStageBytes, gq + TCR_FRAG_OFF(u + D - 1), pol);
             cp_async_commit();
             cp_async_wait<D - 1>();
             __syncwarp();
