@@ -278,6 +278,32 @@ __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t b
     }
     uint32_t P = 1;
     while (P < W) P <<= 1;
+    if (P == 32) {
+        // 32 blocks per warp pass: lane l loads chunk l of each of the 32 blocks (conflict free),
+        // then a transpose-reduce: the step with offset o performs level len = 2o of the
+        // reference tree (v[i] += v[i + o]) for half of the blocks a lane still holds, the lane
+        // pair l, l^o exchanging the other half; lane l ends with block l.  31 shuffles per 32
+        // blocks instead of 5 per block, the same operand pairs.
+        for (uint32_t b0 = w * 32u; b0 < nblk; b0 += nwarps * 32u) {
+            float v[32];
+#pragma unroll
+            for (uint32_t r = 0; r < 32; ++r) v[r] = (b0 + r < nblk && lane < W) ? chunks[(b0 + r) * W + lane] : 0.0f;
+#pragma unroll
+            for (uint32_t o = 16; o >= 1; o >>= 1) {
+                const bool up = lane & o;
+#pragma unroll
+                for (uint32_t r = 0; r < o; ++r) {
+                    const float recv = __shfl_xor_sync(kFull, up ? v[r] : v[r + o], o);
+                    v[r] = up ? recv + v[r + o] : v[r] + recv;
+                }
+            }
+            if (b0 + lane < nblk) {
+                blocks[b0 + lane] = v[0];
+                publish_block(p, block0 + b0 + lane, v[0]);
+            }
+        }
+        return;
+    }
     for (uint32_t b = w; b < nblk; b += nwarps) {
         float x = lane < W ? chunks[b * W + lane] : 0.0f;
         for (uint32_t off = P >> 1; off >= 1; off >>= 1) x += __shfl_down_sync(kFull, x, off);

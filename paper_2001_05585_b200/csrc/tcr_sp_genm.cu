@@ -156,8 +156,14 @@ struct NatShape {
     uint32_t chunks_per_unit;  // 16 * CP
 };
 
-// RBC > 0: compile-time fast path for PR == RBC (one stage per unit, shifts instead of
-// divisions, a ring of ND = max(2, 8 / RBC) stages); RBC == 0: any PR (row blocks of S.RB).
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+// RBC == 0 (the instantiation launched): any PR, row blocks of S.RB rows.  Power-of-two periods
+// run gm_nat_fast_kernel below (RBC > 0 here is the earlier form of that fast path, kept
+// compilable for A/B builds).  A cross-group issue cursor and register-capped variants of this
+// generic kernel measured 1-10 % SLOWER on m = 4 R = 3, 5, 6 and m = 2 R = 3.
 template <int RBC>
 __host__ __device__ constexpr int nat_depth() { return RBC == 0 ? 2 : (8 / RBC > 2 ? 8 / RBC : 2); }
 
@@ -300,6 +306,151 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
         cp_wait<0>();
         group_epilogue<REPAIR>(p, gi, s_chunk, s_block, M, ovf);
     }
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+    __threadfence();
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
+}
+
+// Natural layout, PR = RBC a power of two (the common shapes: m = 4 with R in {1, 2, 4, 8, 16},
+// m = 2 with any R whose period is <= 16 rows).  A unit (16 periods) is then 256 RBC CONTIGUOUS
+// elements and lane l's 16-byte piece q of a stage is elements 8 (l + 32 q): the stage of a warp
+// is UPS consecutive units (one 2 KiB cp.async burst per stage for the one-row shapes instead of
+// a 512-byte one), every address and ring offset is a compile-time constant plus a per-lane
+// invariant, chunk results leave through precomputed shared addresses, and the overflow note is
+// a NaN-propagating accumulator (x * 0 is NaN exactly when x is not finite) instead of per-value
+// tests.  Same arithmetic, operand order and chunk -> shared-table mapping as gm_nat_kernel.
+template <int M, int RBC, int UPS, int ND, bool REPAIR>
+__global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams p, const NatShape S) {
+    constexpr uint32_t UNIT_EL = 256u * RBC;
+    constexpr uint32_t UNIT_B = 2u * UNIT_EL;
+    constexpr uint32_t STAGE_EL = UNIT_EL * UPS;
+    constexpr uint32_t STAGE_B = 2u * STAGE_EL;
+    constexpr uint32_t NQ = STAGE_B / 512u;                           // 16-byte pieces per lane per stage
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ float s_scratch[32];
+    __shared__ int s_last;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned g = lane >> 2, c = lane & 3u;
+    const uint32_t R = p.R;
+    float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * ND * STAGE_B);
+    float* s_block = s_chunk + p.G * p.W;
+    const uint32_t ring = smem_u32(dsm) + warp * ND * STAGE_B;
+    const uint32_t ce = R * M * M;
+    const uint32_t CP = S.CP, cpu = S.chunks_per_unit;
+    const uint32_t Cg = p.G * p.W;
+    const uint32_t sunits = ((Cg + cpu - 1) / cpu + UPS - 1) / UPS;  // stages per group
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    auto bsel = [&](uint32_t rho, uint32_t k) -> bool {
+        const uint32_t e = 16u * rho + k;
+        return (e / ce) * M + (e % M) == g;
+    };
+    const bool straddle = CP > 1 && RBC > 1;
+    uint32_t b0 = sel2(bsel(0, 2 * c), bsel(0, 2 * c + 1)), b1 = sel2(bsel(0, 2 * c + 8), bsel(0, 2 * c + 9));
+    const uint32_t bfin = sel2((2 * c) / M == g, (2 * c + 1) / M == g);
+    const uint32_t rho8 = (lane & 7u) + 8u * ((lane >> 3) & 1u), half = lane >> 4;
+    // chunk slots this lane owns after the finishing MMA: columns 2c, 2c+1 of rows g, g+8
+    const bool own0 = 2 * c < CP, own1 = 2 * c + 1 < CP;
+    const uint32_t sa = smem_u32(s_chunk) + 4u * (g * CP + 2 * c), srow8 = 4u * 8u * CP;
+    float nanacc = 0.0f;
+    bool ovf = false;
+    const uint32_t F = sunits > warp ? (sunits - warp + kGmWarps - 1) / kGmWarps : 0;   // stages per group
+    // The issue cursor runs ahead ACROSS groups: the next group's first stages are in flight
+    // while this group's epilogue (block and group trees) runs, so the per-group pipeline drain
+    // of a small group (<= 4096 chunks) is not paid.
+    uint64_t igi = p.group_begin + blockIdx.x;
+    uint64_t e_issue = 0, ilim = 0;
+    bool ifull = false;
+    uint32_t is = 0, islot = 0;
+    auto iset = [&]() {
+        const uint64_t gel0 = igi * uint64_t(Cg) * ce, gel1 = gel0 + uint64_t(Cg) * ce;
+        ilim = gel1 < p.n ? gel1 : p.n;
+        ifull = gel1 <= p.n && Cg % (cpu * UPS) == 0;
+        e_issue = gel0 + uint64_t(warp) * STAGE_EL + 8u * lane;          // this lane's piece 0
+        is = 0;
+    };
+    iset();
+    auto issue = [&]() {
+        if (F != 0 && is == F) {
+            igi += gridDim.x;
+            iset();
+        }
+        if (F != 0 && igi < p.group_end) {
+            const uint32_t dst = ring + islot * STAGE_B;
+            auto off = [&](uint32_t q) {
+                const uint32_t piece = lane + 32u * (q % RBC);
+                return (q / RBC) * UNIT_B + ((piece ^ ((piece / (2u * RBC)) & 7u)) * 16u);
+            };
+            if (ifull) {
+#pragma unroll
+                for (uint32_t q = 0; q < NQ; ++q) cp16(dst + off(q), x + e_issue + 256u * q, 16u);
+            } else {
+#pragma unroll
+                for (uint32_t q = 0; q < NQ; ++q) {
+                    const uint64_t e = e_issue + 256u * q;
+                    const uint32_t bytes = e + 8 <= ilim ? 16u : (e < ilim ? uint32_t(ilim - e) * 2u : 0u);
+                    cp16(dst + off(q), x + (e < ilim ? e : 0), bytes);
+                }
+            }
+            e_issue += uint64_t(kGmWarps) * STAGE_EL;
+            ++is;
+        }
+        cp_commit();
+        islot = islot + 1 == uint32_t(ND) ? 0 : islot + 1;
+    };
+#pragma unroll
+    for (int f = 0; f < ND - 1; ++f) issue();
+    uint32_t cslot = 0;
+
+    for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+        const uint64_t gel1 = (gi + 1) * uint64_t(Cg) * ce;
+        const bool full = gel1 <= p.n && Cg % (cpu * UPS) == 0;
+        uint32_t cu0 = warp * UPS * cpu;                                  // first chunk of the stage
+        for (uint32_t f = 0; f < F; ++f) {
+            issue();
+            cp_wait<ND - 1>();
+            __syncwarp();
+            const uint32_t base = ring + cslot * STAGE_B;
+            cslot = cslot + 1 == uint32_t(ND) ? 0 : cslot + 1;
+#pragma unroll
+            for (uint32_t j = 0; j < UPS; ++j) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (uint32_t i = 0; i < RBC; ++i) {
+                    if (straddle) {
+                        b0 = sel2(bsel(i, 2 * c), bsel(i, 2 * c + 1));
+                        b1 = sel2(bsel(i, 2 * c + 8), bsel(i, 2 * c + 9));
+                    }
+                    const uint32_t unit16 = 2u * (rho8 * RBC + i) + half;
+                    uint32_t d0, d1, d2, d3;
+                    ldsm4(base + j * UNIT_B + ((unit16 ^ (rho8 & 7u)) * 16u), d0, d1, d2, d3);
+                    mma_16816(acc, d0, d1, d2, d3, b0, b1);
+                }
+                float d2[4] = {0.f, 0.f, 0.f, 0.f};
+                mma_16816(d2, pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), 0u, 0u, bfin, 0u);
+                // non-owner columns are 0 unless an input is non-finite, which its owner sees too
+                nanacc = fmaf(d2[0], 0.0f, nanacc);
+                nanacc = fmaf(d2[1], 0.0f, nanacc);
+                nanacc = fmaf(d2[2], 0.0f, nanacc);
+                nanacc = fmaf(d2[3], 0.0f, nanacc);
+                const uint32_t cu = cu0 + j * cpu;
+                const uint32_t ca = cu + g * CP + 2 * c;
+                if (own0) {
+                    if (full || ca < Cg) sts_f32(sa + 4u * cu, d2[0]);
+                    if (full || ca + 8 * CP < Cg) sts_f32(sa + 4u * cu + srow8, d2[2]);
+                }
+                if (own1) {
+                    if (full || ca + 1 < Cg) sts_f32(sa + 4u * cu + 4u, d2[1]);
+                    if (full || ca + 1 + 8 * CP < Cg) sts_f32(sa + 4u * cu + 4u + srow8, d2[3]);
+                }
+            }
+            __syncwarp();
+            cu0 += kGmWarps * UPS * cpu;
+        }
+        ovf = nanacc != nanacc;
+        group_epilogue<REPAIR>(p, gi, s_chunk, s_block, M, ovf);
+    }
+    cp_wait<0>();
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __threadfence();
     __syncthreads();
@@ -924,20 +1075,39 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     if (g.m == 2 || g.m == 4) {
         NatShape S;
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
-        void (*fn)(SpParams, NatShape) = nullptr;
-        int nd = 2;
         const bool fast = S.PR == S.RB && (S.RB & (S.RB - 1)) == 0;   // PR a power of two <= 16
-#define TCR_NAT(MV, RBV) \
-    { fn = gm_nat_kernel<MV, RBV, REPAIR>; nd = nat_depth<RBV>(); }
-        if (g.m == 2) {
-            if (!fast) TCR_NAT(2, 0) else if (S.RB == 1) TCR_NAT(2, 1) else if (S.RB == 2) TCR_NAT(2, 2)
-            else if (S.RB == 4) TCR_NAT(2, 4) else if (S.RB == 8) TCR_NAT(2, 8) else TCR_NAT(2, 16)
-        } else {
-            if (!fast) TCR_NAT(4, 0) else if (S.RB == 1) TCR_NAT(4, 1) else if (S.RB == 2) TCR_NAT(4, 2)
-            else if (S.RB == 4) TCR_NAT(4, 4) else if (S.RB == 8) TCR_NAT(4, 8) else TCR_NAT(4, 16)
+        if (fast) {
+            const char* alt = std::getenv("TCR_GM_NAT_ALT");           // knob: ring shape A/B
+            const int a = alt ? std::atoi(alt) : 0;
+            void (*ff)(SpParams, NatShape) = nullptr;
+            uint32_t stage = 0, nd = 0;
+            // (units per stage, stages): 2 KiB stages; one-row periods 3 stages -> 3 CTAs per SM
+            // (+7..38 % over 4 stages / 2 CTAs, A/B on m = 2, 4)
+#define TCR_NATF(MV, RBV, UPSV, NDV) \
+    { ff = gm_nat_fast_kernel<MV, RBV, UPSV, NDV, REPAIR>; stage = 512u * RBV * UPSV; nd = NDV; }
+#define TCR_NATF_M(MV)                                                        \
+    switch (S.RB) {                                                           \
+    case 1:                                                                   \
+        if (a == 1) TCR_NATF(MV, 1, 4, 4) else if (a == 2) TCR_NATF(MV, 1, 2, 6) \
+        else TCR_NATF(MV, 1, 4, 3)                                            \
+        break;                                                                \
+    case 2: TCR_NATF(MV, 2, 2, 4) break;                                      \
+    case 4: TCR_NATF(MV, 4, 1, 4) break;                                      \
+    case 8: TCR_NATF(MV, 8, 1, 2) break;                                      \
+    default: TCR_NATF(MV, 16, 1, 2) break;                                    \
+    }
+            if (g.m == 2) {
+                TCR_NATF_M(2)
+            } else {
+                TCR_NATF_M(4)
+            }
+#undef TCR_NATF_M
+#undef TCR_NATF
+            return launch_gm(ff, kGmWarps * nd * stage + tables, groups, p, S, s);
         }
-#undef TCR_NAT
-        return launch_gm(fn, kGmWarps * uint32_t(nd) * (16u * S.RB * 32u) + tables, groups, p, S, s);
+        // any other period (rows not a power of two, or more than 16): row blocks of <= 16 rows
+        void (*fn)(SpParams, NatShape) = g.m == 2 ? gm_nat_kernel<2, 0, REPAIR> : gm_nat_kernel<4, 0, REPAIR>;
+        return launch_gm(fn, kGmWarps * uint32_t(nat_depth<0>()) * (16u * S.RB * 32u) + tables, groups, p, S, s);
     }
     if (g.m >= 256) {
         if (!wide_ok(g)) return cudaErrorInvalidValue;
