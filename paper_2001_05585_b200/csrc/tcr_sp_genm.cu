@@ -480,7 +480,10 @@ struct TrStage {
 
 template <int MM, bool REPAIR>   // MM = 8, 32, 64, 128
 __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, const TrShape S) {
-    constexpr int D = kGmTrDepth;
+    // stages of T tiles: m >= 32 items are K = R (m/16)^2 (a multiple of 4) contiguous tiles, so a
+    // 2 KiB stage of 4 tiles stays inside one item (one issue / wait / sync per 4 tiles)
+    constexpr uint32_t T = MM >= 32 ? 4u : 1u;
+    constexpr int D = kGmTrDepth / int(T);
     constexpr uint32_t SG = MM >= 32 ? MM / 16 : 1;    // column groups per chunk (m >= 32)
     using ST = TrStage<MM>;
     extern __shared__ __align__(128) unsigned char s_ring[];   // [kGmWarps][D][512], staging, tables
@@ -488,9 +491,9 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
     __shared__ int s_last;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
-    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
-    float* s_stage = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512) + warp * ST::FLOATS;
-    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512) + kGmWarps * ST::FLOATS;
+    const uint32_t ring = smem_u32(s_ring) + warp * kGmTrDepth * 512u;
+    float* s_stage = reinterpret_cast<float*>(s_ring + kGmWarps * kGmTrDepth * 512) + warp * ST::FLOATS;
+    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * kGmTrDepth * 512) + kGmWarps * ST::FLOATS;
     const uint32_t Cg = p.G * p.W;
     float* s_block = s_chunk + Cg;
     const uint32_t items = Cg / S.CPT;
@@ -520,14 +523,20 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
         uint32_t iit = 0, ik = 0, islot = 0;                          // issue cursor
         auto issue = [&]() {
             if (iit < my_items) {
-                const uint64_t e = (tile0 + uint64_t(warp + iit * kGmWarps) * S.K + ik) * 256u + 8u * lane;
+                const uint64_t e0 = (tile0 + uint64_t(warp + iit * kGmWarps) * S.K + ik) * 256u + 8u * lane;
+                const uint32_t dst = ring + islot * (512u * T) + cp_dst;
                 if (full) {
-                    cp16(ring + islot * 512u + cp_dst, x + e, 16u);
+#pragma unroll
+                    for (uint32_t t = 0; t < T; ++t) cp16(dst + 512u * t, x + e0 + 256u * t, 16u);
                 } else {
-                    const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
-                    cp16(ring + islot * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+#pragma unroll
+                    for (uint32_t t = 0; t < T; ++t) {
+                        const uint64_t e = e0 + 256u * t;
+                        const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                        cp16(dst + 512u * t, x + (e < p.n ? e : 0), bytes);
+                    }
                 }
-                if (++ik == S.K) {
+                if ((ik += T) == S.K) {
                     ik = 0;
                     ++iit;
                 }
@@ -564,16 +573,19 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
             issue();
             cp_wait<D - 1>();
             __syncwarp();
-            uint32_t d0, d1, d2, d3;
-            ldsm4t(ring + cslot * 512u + ld_off, d0, d1, d2, d3);
+#pragma unroll
+            for (uint32_t t = 0; t < T; ++t) {
+                uint32_t d0, d1, d2, d3;
+                ldsm4t(ring + cslot * (512u * T) + 512u * t + ld_off, d0, d1, d2, d3);
+                if (straddle) {
+                    b0 = sel2(bsel(ck + t, 2 * c), bsel(ck + t, 2 * c + 1));
+                    b1 = sel2(bsel(ck + t, 2 * c + 8), bsel(ck + t, 2 * c + 9));
+                }
+                mma_16816(acc, d0, d1, d2, d3, b0, b1);
+            }
             __syncwarp();
             cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
-            if (straddle) {
-                b0 = sel2(bsel(ck, 2 * c), bsel(ck, 2 * c + 1));
-                b1 = sel2(bsel(ck, 2 * c + 8), bsel(ck, 2 * c + 9));
-            }
-            mma_16816(acc, d0, d1, d2, d3, b0, b1);
-            if (++ck < S.K) continue;
+            if ((ck += T) < S.K) continue;
             ck = 0;
             // ---- item complete: acc = (j16 = g, n = 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
             if (MM == 8) {
