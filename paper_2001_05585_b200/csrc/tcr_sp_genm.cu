@@ -478,11 +478,14 @@ struct TrStage {
     static constexpr uint32_t FLOATS = ROWS * SW;                                 // per warp
 };
 
-template <int MM, bool REPAIR>   // MM = 8, 32, 64, 128
+template <int MM, int SI, bool REPAIR>   // MM = 8, 32, 64, 128
 __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, const TrShape S) {
     // stages of T tiles: m >= 32 items are K = R (m/16)^2 (a multiple of 4) contiguous tiles, so a
-    // 2 KiB stage of 4 tiles stays inside one item (one issue / wait / sync per 4 tiles)
-    constexpr uint32_t T = MM >= 32 ? 4u : 1u;
+    // 2 KiB stage of 4 tiles stays inside one item (one issue / wait / sync per 4 tiles); m = 8
+    // with one-tile items (K = 1: R = 1, 2, 4) is dealt to the warps in runs of SI = 4 adjacent
+    // items, a stage = one run (SI = 1: items dealt one by one, one tile per stage).
+    static_assert(SI == 1 || MM == 8, "item runs only for one-tile items");
+    constexpr uint32_t T = MM >= 32 ? 4u : uint32_t(SI);
     constexpr int D = kGmTrDepth / int(T);
     constexpr uint32_t SG = MM >= 32 ? MM / 16 : 1;    // column groups per chunk (m >= 32)
     using ST = TrStage<MM>;
@@ -518,12 +521,16 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
 
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
         const uint64_t tile0 = gi * uint64_t(items) * S.K;          // first tile of the group
-        const bool full = (tile0 + uint64_t(items) * S.K) * 256u <= p.n;
-        const uint32_t my_items = items > warp ? (items - warp + kGmWarps - 1) / kGmWarps : 0;
+        const uint64_t gend = (tile0 + uint64_t(items) * S.K) * 256u;
+        const uint64_t glim = gend < p.n ? gend : p.n;
+        const bool full = gend <= p.n && items % uint32_t(SI) == 0;
+        const uint32_t runs = (items + SI - 1) / SI;
+        const uint32_t my_runs = runs > warp ? (runs - warp + kGmWarps - 1) / kGmWarps : 0;
+        const uint32_t my_items = my_runs * SI;
         uint32_t iit = 0, ik = 0, islot = 0;                          // issue cursor
         auto issue = [&]() {
-            if (iit < my_items) {
-                const uint64_t e0 = (tile0 + uint64_t(warp + iit * kGmWarps) * S.K + ik) * 256u + 8u * lane;
+            if (iit < my_runs) {
+                const uint64_t e0 = (tile0 + uint64_t(warp + iit * kGmWarps) * SI * S.K + ik) * 256u + 8u * lane;
                 const uint32_t dst = ring + islot * (512u * T) + cp_dst;
                 if (full) {
 #pragma unroll
@@ -532,11 +539,11 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
 #pragma unroll
                     for (uint32_t t = 0; t < T; ++t) {
                         const uint64_t e = e0 + 256u * t;
-                        const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
-                        cp16(dst + 512u * t, x + (e < p.n ? e : 0), bytes);
+                        const uint32_t bytes = e + 8 <= glim ? 16u : (e < glim ? uint32_t(glim - e) * 2u : 0u);
+                        cp16(dst + 512u * t, x + (e < glim ? e : 0), bytes);
                     }
                 }
-                if ((ik += T) == S.K) {
+                if (SI > 1 || (ik += T) == S.K) {
                     ik = 0;
                     ++iit;
                 }
@@ -559,9 +566,10 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
                 r = r + 0.0f;
                 ovf |= !isfinite(r);
                 const uint32_t b = MM == 8 ? lane / S.CPT : lane;
-                const uint32_t item = warp + (it0 + b) * kGmWarps;
+                const uint32_t wi = it0 + b;                            // item of this warp
+                const uint32_t item = SI == 1 ? warp + wi * kGmWarps : (warp + wi / SI * kGmWarps) * SI + wi % SI;
                 const uint32_t ch = MM == 8 ? item * S.CPT + lane % S.CPT : item;
-                s_chunk[ch] = r;
+                if (SI == 1 || ch < Cg) s_chunk[ch] = r;
             }
             __syncwarp();
         };
@@ -573,43 +581,64 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
             issue();
             cp_wait<D - 1>();
             __syncwarp();
+            if constexpr (SI > 1) {
+                // a run of SI one-tile items: each tile completes an item
 #pragma unroll
-            for (uint32_t t = 0; t < T; ++t) {
-                uint32_t d0, d1, d2, d3;
-                ldsm4t(ring + cslot * (512u * T) + 512u * t + ld_off, d0, d1, d2, d3);
-                if (straddle) {
-                    b0 = sel2(bsel(ck + t, 2 * c), bsel(ck + t, 2 * c + 1));
-                    b1 = sel2(bsel(ck + t, 2 * c + 8), bsel(ck + t, 2 * c + 9));
+                for (uint32_t t = 0; t < T; ++t) {
+                    uint32_t d0, d1, d2, d3;
+                    ldsm4t(ring + cslot * (512u * T) + 512u * t + ld_off, d0, d1, d2, d3);
+                    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+                    mma_16816(a4, d0, d1, d2, d3, b0, b1);
+                    const uint32_t r0 = nb * S.CPT;
+                    if (2 * c < S.CPT) s_stage[(r0 + 2 * c) * ST::SW + g] = h_round(a4[0] + a4[2]);
+                    if (2 * c + 1 < S.CPT) s_stage[(r0 + 2 * c + 1) * ST::SW + g] = h_round(a4[1] + a4[3]);
+                    ++it;
+                    if (++nb == batch_items) {
+                        flush(it - nb, nb);
+                        nb = 0;
+                    }
                 }
-                mma_16816(acc, d0, d1, d2, d3, b0, b1);
-            }
-            __syncwarp();
-            cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
-            if ((ck += T) < S.K) continue;
-            ck = 0;
-            // ---- item complete: acc = (j16 = g, n = 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
-            if (MM == 8) {
-                // partial(chunk slot n, j8 = g) = D[g][n] + D[g+8][n]  -> staged row (nb CPT + n)
-                const uint32_t r0 = nb * S.CPT;
-                if (2 * c < S.CPT) s_stage[(r0 + 2 * c) * ST::SW + g] = h_round(acc[0] + acc[2]);
-                if (2 * c + 1 < S.CPT) s_stage[(r0 + 2 * c + 1) * ST::SW + g] = h_round(acc[1] + acc[3]);
+                __syncwarp();
+                cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
             } else {
-                // partial(j = 16 n + j16) = D[j16][n]
-                float* row = s_stage + nb * ST::SW;
-                if (2 * c < SG) {
-                    row[16 * (2 * c) + g] = h_round(acc[0]);
-                    row[16 * (2 * c) + g + 8] = h_round(acc[2]);
+#pragma unroll
+                for (uint32_t t = 0; t < T; ++t) {
+                    uint32_t d0, d1, d2, d3;
+                    ldsm4t(ring + cslot * (512u * T) + 512u * t + ld_off, d0, d1, d2, d3);
+                    if (straddle) {
+                        b0 = sel2(bsel(ck + t, 2 * c), bsel(ck + t, 2 * c + 1));
+                        b1 = sel2(bsel(ck + t, 2 * c + 8), bsel(ck + t, 2 * c + 9));
+                    }
+                    mma_16816(acc, d0, d1, d2, d3, b0, b1);
                 }
-                if (2 * c + 1 < SG) {
-                    row[16 * (2 * c + 1) + g] = h_round(acc[1]);
-                    row[16 * (2 * c + 1) + g + 8] = h_round(acc[3]);
+                __syncwarp();
+                cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
+                if ((ck += T) < S.K) continue;
+                ck = 0;
+                // ---- item complete: acc = (j16 = g, n = 2c), (g, 2c+1), (g+8, 2c), (g+8, 2c+1)
+                if (MM == 8) {
+                    // partial(chunk slot n, j8 = g) = D[g][n] + D[g+8][n]  -> staged row (nb CPT + n)
+                    const uint32_t r0 = nb * S.CPT;
+                    if (2 * c < S.CPT) s_stage[(r0 + 2 * c) * ST::SW + g] = h_round(acc[0] + acc[2]);
+                    if (2 * c + 1 < S.CPT) s_stage[(r0 + 2 * c + 1) * ST::SW + g] = h_round(acc[1] + acc[3]);
+                } else {
+                    // partial(j = 16 n + j16) = D[j16][n]
+                    float* row = s_stage + nb * ST::SW;
+                    if (2 * c < SG) {
+                        row[16 * (2 * c) + g] = h_round(acc[0]);
+                        row[16 * (2 * c) + g + 8] = h_round(acc[2]);
+                    }
+                    if (2 * c + 1 < SG) {
+                        row[16 * (2 * c + 1) + g] = h_round(acc[1]);
+                        row[16 * (2 * c + 1) + g + 8] = h_round(acc[3]);
+                    }
                 }
-            }
-            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-            ++it;
-            if (++nb == batch_items) {
-                flush(it - nb, nb);
-                nb = 0;
+                acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+                ++it;
+                if (++nb == batch_items) {
+                    flush(it - nb, nb);
+                    nb = 0;
+                }
             }
         }
         if (nb) flush(it - nb, nb);
@@ -1146,10 +1175,13 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     void (*fn)(SpParams, TrShape) = nullptr;
     uint32_t stage = 0;
     switch (g.m) {
-    case 8: fn = gm_tr_kernel<8, REPAIR>; stage = TrStage<8>::FLOATS; break;
-    case 32: fn = gm_tr_kernel<32, REPAIR>; stage = TrStage<32>::FLOATS; break;
-    case 64: fn = gm_tr_kernel<64, REPAIR>; stage = TrStage<64>::FLOATS; break;
-    case 128: fn = gm_tr_kernel<128, REPAIR>; stage = TrStage<128>::FLOATS; break;
+    case 8:
+        fn = S.K == 1 && !std::getenv("TCR_GM_TR8_SINGLE") ? gm_tr_kernel<8, 4, REPAIR> : gm_tr_kernel<8, 1, REPAIR>;
+        stage = TrStage<8>::FLOATS;
+        break;
+    case 32: fn = gm_tr_kernel<32, 1, REPAIR>; stage = TrStage<32>::FLOATS; break;
+    case 64: fn = gm_tr_kernel<64, 1, REPAIR>; stage = TrStage<64>::FLOATS; break;
+    case 128: fn = gm_tr_kernel<128, 1, REPAIR>; stage = TrStage<128>::FLOATS; break;
     default: return cudaErrorInvalidValue;
     }
     return launch_gm(fn, kGmWarps * (kGmTrDepth * 512u + stage * 4u) + tables, groups, p, S, s);
