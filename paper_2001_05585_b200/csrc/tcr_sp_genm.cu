@@ -766,18 +766,22 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
 // similar magnitude add exactly in fp32, so the order rarely matters).
 template <int SL, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams p, const uint32_t m) {
-    constexpr int D = kGmTrDepth;
+    // 2 KiB stages of 4 consecutive tiles of the warp's stream (rows / 8 * SL tiles per chunk,
+    // a multiple of 4): one issue / wait / sync per 4 tiles
+    constexpr uint32_t T = 4;
+    constexpr int D = kGmTrDepth / int(T);
+    constexpr uint32_t QS = SL > 4 ? uint32_t(SL) : 4u;         // tiles per consumer iteration
     extern __shared__ __align__(128) unsigned char s_ring[];   // ring | part[8][m] | tables
     __shared__ float s_scratch[32];
     __shared__ float s_wsum[kGmWarps];
     __shared__ int s_last;
-    float* s_part = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
+    float* s_part = reinterpret_cast<float*>(s_ring + kGmWarps * kGmTrDepth * 512);
     float* s_chunk = s_part + kGmWarps * m;
     const uint32_t Cg = p.G * p.W;
     float* s_block = s_chunk + Cg;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
-    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    const uint32_t ring = smem_u32(s_ring) + warp * kGmTrDepth * 512u;
     const uint64_t rows = uint64_t(p.R) * m;
     const uint64_t chunk_el = rows * m;
     const uint64_t span = rows / kGmWarps * m;                  // elements of this warp per chunk
@@ -797,10 +801,20 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
         uint64_t ioff = 0;                                         // issue cursor (chunk, offset)
         auto issue = [&]() {
             if (iit < Cg) {
-                const uint64_t e = gel0 + uint64_t(iit) * chunk_el + w_off + ioff + 8u * lane;
-                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
-                cp16(ring + islot * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
-                ioff += 256u;
+                const uint64_t e0 = gel0 + uint64_t(iit) * chunk_el + w_off + ioff + 8u * lane;
+                const uint32_t dst = ring + islot * (512u * T) + cp_dst;
+                if (e0 + 256u * T <= p.n) {
+#pragma unroll
+                    for (uint32_t q = 0; q < T; ++q) cp16(dst + 512u * q, x + e0 + 256u * q, 16u);
+                } else {
+#pragma unroll
+                    for (uint32_t q = 0; q < T; ++q) {
+                        const uint64_t e = e0 + 256u * q;
+                        const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                        cp16(dst + 512u * q, x + (e < p.n ? e : 0), bytes);
+                    }
+                }
+                ioff += 256u * T;
                 if (ioff == span) {
                     ioff = 0;
                     ++iit;
@@ -818,18 +832,22 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
             for (int sl = 0; sl < SL; ++sl)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[sl][0][q] = acc[sl][1][q] = 0.f;
-            for (uint64_t r = 0; r < rows / kGmWarps; ++r) {
+            for (uint64_t q0 = 0; q0 < rows / kGmWarps * SL; q0 += QS) {
 #pragma unroll
-                for (int sl = 0; sl < SL; ++sl) {
+                for (uint32_t h = 0; h < QS / T; ++h) {
                     issue();
                     cp_wait<D - 1>();
                     __syncwarp();
-                    uint32_t d0, d1, d2, d3;
-                    ldsm4t(ring + cslot * 512u + ld_off, d0, d1, d2, d3);
+#pragma unroll
+                    for (uint32_t q = 0; q < T; ++q) {
+                        const int sl = int((h * T + q) % uint32_t(SL));   // tile (row, slab) order
+                        uint32_t d0, d1, d2, d3;
+                        ldsm4t(ring + cslot * (512u * T) + 512u * q + ld_off, d0, d1, d2, d3);
+                        mma_16816(acc[sl][0], d0, d1, d2, d3, blo0, blo1);
+                        mma_16816(acc[sl][1], d0, d1, d2, d3, bhi0, bhi1);
+                    }
                     __syncwarp();
                     cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
-                    mma_16816(acc[sl][0], d0, d1, d2, d3, blo0, blo1);
-                    mma_16816(acc[sl][1], d0, d1, d2, d3, bhi0, bhi1);
                 }
             }
             // warp partials: D[j16][n] = column 256 sl + 16 n + j16 (n + 8 for the hi half)
@@ -881,7 +899,9 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
 // only 256 chunks at m = 1024: one CTA per chunk left most SMs idle.
 template <int SL, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_cluster_kernel(const SpParams p, const uint32_t m) {
-    constexpr int D = kGmTrDepth;
+    constexpr uint32_t T = 4;                                    // tiles per stage (as gm_wide_cta_kernel)
+    constexpr int D = kGmTrDepth / int(T);
+    constexpr uint32_t QS = SL > 4 ? uint32_t(SL) : 4u;
     extern __shared__ __align__(128) unsigned char s_ring[];   // ring | part[8][m] | cta[m] | tables
     __shared__ float s_scratch[32];
     __shared__ float s_wsum[kGmWarps];
@@ -890,14 +910,14 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cluster_kernel(const SpPar
     const uint32_t CS = cluster.num_blocks();
     const uint32_t rank = cluster.block_rank();
     const uint64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
-    float* s_part = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
+    float* s_part = reinterpret_cast<float*>(s_ring + kGmWarps * kGmTrDepth * 512);
     float* s_cta = s_part + kGmWarps * m;                       // this CTA's column sums
     float* s_chunk = s_cta + m;
     const uint32_t Cg = p.G * p.W;
     float* s_block = s_chunk + Cg;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
-    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    const uint32_t ring = smem_u32(s_ring) + warp * kGmTrDepth * 512u;
     const uint64_t rows = uint64_t(p.R) * m;
     const uint64_t chunk_el = rows * m;
     const uint64_t rpw = rows / (uint64_t(kGmWarps) * CS);     // rows of this warp per chunk
@@ -918,10 +938,20 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cluster_kernel(const SpPar
         uint64_t ioff = 0;                                         // issue cursor (chunk, offset)
         auto issue = [&]() {
             if (iit < Cg) {
-                const uint64_t e = gel0 + uint64_t(iit) * chunk_el + w_off + ioff + 8u * lane;
-                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
-                cp16(ring + islot * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
-                ioff += 256u;
+                const uint64_t e0 = gel0 + uint64_t(iit) * chunk_el + w_off + ioff + 8u * lane;
+                const uint32_t dst = ring + islot * (512u * T) + cp_dst;
+                if (e0 + 256u * T <= p.n) {
+#pragma unroll
+                    for (uint32_t q = 0; q < T; ++q) cp16(dst + 512u * q, x + e0 + 256u * q, 16u);
+                } else {
+#pragma unroll
+                    for (uint32_t q = 0; q < T; ++q) {
+                        const uint64_t e = e0 + 256u * q;
+                        const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                        cp16(dst + 512u * q, x + (e < p.n ? e : 0), bytes);
+                    }
+                }
+                ioff += 256u * T;
                 if (ioff == span) {
                     ioff = 0;
                     ++iit;
@@ -939,18 +969,22 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cluster_kernel(const SpPar
             for (int sl = 0; sl < SL; ++sl)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[sl][0][q] = acc[sl][1][q] = 0.f;
-            for (uint64_t r = 0; r < rpw; ++r) {
+            for (uint64_t q0 = 0; q0 < rpw * SL; q0 += QS) {
 #pragma unroll
-                for (int sl = 0; sl < SL; ++sl) {
+                for (uint32_t h = 0; h < QS / T; ++h) {
                     issue();
                     cp_wait<D - 1>();
                     __syncwarp();
-                    uint32_t d0, d1, d2, d3;
-                    ldsm4t(ring + cslot * 512u + ld_off, d0, d1, d2, d3);
+#pragma unroll
+                    for (uint32_t q = 0; q < T; ++q) {
+                        const int sl = int((h * T + q) % uint32_t(SL));   // tile (row, slab) order
+                        uint32_t d0, d1, d2, d3;
+                        ldsm4t(ring + cslot * (512u * T) + 512u * q + ld_off, d0, d1, d2, d3);
+                        mma_16816(acc[sl][0], d0, d1, d2, d3, blo0, blo1);
+                        mma_16816(acc[sl][1], d0, d1, d2, d3, bhi0, bhi1);
+                    }
                     __syncwarp();
                     cslot = cslot + 1 == uint32_t(D) ? 0 : cslot + 1;
-                    mma_16816(acc[sl][0], d0, d1, d2, d3, blo0, blo1);
-                    mma_16816(acc[sl][1], d0, d1, d2, d3, bhi0, bhi1);
                 }
             }
             // warp partials: D[j16][n] = column 256 sl + 16 n + j16 (n + 8 for the hi half)

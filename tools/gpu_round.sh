@@ -13,7 +13,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 timeout 900 python tools/ab.py --out $OUT/ab.json async:4:1:1024 async_D8:4:1:1024:TCR_DEBUG_MODE=9 async_D32:4:1:1024:TCR_DEBUG_MODE=10 bulk:1:1:1024 regs:3:1:1024 tc05:2:1:1024 > $OUT/ab.txt 2>&1
-timeout 600 python tools/ab.py --n 268435456 --rounds 3 --reps 5 --out $OUT/ab_m.json m2r1:0:1:128:M=2 m2r4:0:4:128:M=2 m4r1:0:1:128:M=4 m4r4:0:4:128:M=4 m4r1b1024:0:1:1024:M=4 m8r1:0:1:128:M=8 m8r4:0:4:128:M=8 m16r1:0:1:128 m16r4:0:4:128 m32r1:0:1:128:M=32 m64r1:0:1:128:M=64 m128r1:0:1:128:M=128 m256r1:0:1:128:M=256 m512r1:0:1:128:M=512 m1024r1:0:1:128:M=1024 m4r5b32:0:5:32:M=4 m2r3:0:3:128:M=2 > $OUT/ab_m.txt 2>&1
+timeout 600 python tools/ab.py --n 268435456 --rounds 3 --reps 5 --out $OUT/ab_m.json m2r1:0:1:128:M=2 m2r4:0:4:128:M=2 m4r1:0:1:128:M=4 m4r4:0:4:128:M=4 m4r1b1024:0:1:1024:M=4 m8r1:0:1:128:M=8 m8r4:0:4:128:M=8 m16r1:0:1:128 m16r4:0:4:128 m32r1:0:1:128:M=32 m64r1:0:1:128:M=64 m128r1:0:1:128:M=128 m256r1:0:1:128:M=256 m512r1:0:1:128:M=512 m1024r1:0:1:128:M=1024 m2048r1:0:1:128:M=2048 m4r1b1024:0:1:1024:M=4 m8r1b1024:0:1:1024:M=8 m4r5b32:0:5:32:M=4 m2r3:0:3:128:M=2 m8r3:0:3:128:M=8 > $OUT/ab_m.txt 2>&1
 timeout 1500 python tools/sweep.py --out $OUT/sweep.json > $OUT/sweep.log 2>&1
 timeout 900 oracle/_ref/ref_tests_b200 > $OUT/ref_unit_tests.txt 2>&1
 timeout 900 oracle/_ref/ref_acceptance_b200 > $OUT/ref_acceptance.txt 2>&1
