@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
 // invariant, chunk results leave through precomputed shared addresses, and the overflow note is
 // a NaN-propagating accumulator (x * 0 is NaN exactly when x is not finite) instead of per-value
 // tests.  Same arithmetic, operand order and chunk -> shared-table mapping as gm_nat_kernel.
-template <int M, int RBC, int UPS, int ND, bool REPAIR>
+template <int M, int RBC, int UPS, int ND, bool REPAIR, bool XG = true>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams p, const NatShape S) {
     constexpr uint32_t UNIT_EL = 256u * RBC;
     constexpr uint32_t UNIT_B = 2u * UNIT_EL;
@@ -371,11 +371,11 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
     };
     iset();
     auto issue = [&]() {
-        if (F != 0 && is == F) {
+        if (XG && F != 0 && is == F) {
             igi += gridDim.x;
             iset();
         }
-        if (F != 0 && igi < p.group_end) {
+        if (F != 0 && igi < p.group_end && is < F) {
             const uint32_t dst = ring + islot * STAGE_B;
             auto off = [&](uint32_t q) {
                 const uint32_t piece = lane + 32u * (q % RBC);
@@ -403,6 +403,15 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
     uint32_t cslot = 0;
 
     for (uint64_t gi = p.group_begin + blockIdx.x; gi < p.group_end; gi += gridDim.x) {
+        if (!XG && gi != p.group_begin + blockIdx.x) {   // per-group pipeline (A/B form)
+            cp_wait<0>();
+            igi = gi;
+            iset();
+            islot = 0;
+            cslot = 0;
+#pragma unroll
+            for (int f = 0; f < ND - 1; ++f) issue();
+        }
         const uint64_t gel1 = (gi + 1) * uint64_t(Cg) * ce;
         const bool full = gel1 <= p.n && Cg % (cpu * UPS) == 0;
         uint32_t cu0 = warp * UPS * cpu;                                  // first chunk of the stage
@@ -1157,17 +1166,21 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
             void (*ff)(SpParams, NatShape) = nullptr;
             uint32_t stage = 0, nd = 0;
             // (units per stage, stages): 2 KiB stages; one-row periods 3 stages -> 3 CTAs per SM
-            // (+7..38 % over 4 stages / 2 CTAs, A/B on m = 2, 4)
+            // (+7..38 % over 4 stages / 2 CTAs, A/B on m = 2, 4).  Cross-group prefetch (XG) for
+            // one-row periods (m = 2 R = 1: +9 %), per-group pipelines for 2- and 4-row periods
+            // (+1..3 %); knob value 3 flips both for A/B.
 #define TCR_NATF(MV, RBV, UPSV, NDV) \
     { ff = gm_nat_fast_kernel<MV, RBV, UPSV, NDV, REPAIR>; stage = 512u * RBV * UPSV; nd = NDV; }
+#define TCR_NATFX(MV, RBV, UPSV, NDV) \
+    { ff = gm_nat_fast_kernel<MV, RBV, UPSV, NDV, REPAIR, false>; stage = 512u * RBV * UPSV; nd = NDV; }
 #define TCR_NATF_M(MV)                                                        \
     switch (S.RB) {                                                           \
     case 1:                                                                   \
         if (a == 1) TCR_NATF(MV, 1, 4, 4) else if (a == 2) TCR_NATF(MV, 1, 2, 6) \
-        else TCR_NATF(MV, 1, 4, 3)                                            \
+        else if (a == 3) TCR_NATFX(MV, 1, 4, 3) else TCR_NATF(MV, 1, 4, 3)   \
         break;                                                                \
-    case 2: TCR_NATF(MV, 2, 2, 4) break;                                      \
-    case 4: TCR_NATF(MV, 4, 1, 4) break;                                      \
+    case 2: if (a == 3) TCR_NATF(MV, 2, 2, 4) else TCR_NATFX(MV, 2, 2, 4) break; \
+    case 4: if (a == 3) TCR_NATF(MV, 4, 1, 4) else TCR_NATFX(MV, 4, 1, 4) break; \
     case 8: TCR_NATF(MV, 8, 1, 2) break;                                      \
     default: TCR_NATF(MV, 16, 1, 2) break;                                    \
     }
@@ -1177,6 +1190,7 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
                 TCR_NATF_M(4)
             }
 #undef TCR_NATF_M
+#undef TCR_NATFX
 #undef TCR_NATF
             return launch_gm(ff, kGmWarps * nd * stage + tables, groups, p, S, s);
         }
