@@ -312,9 +312,8 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
 }
 
-// Natural layout, PR = RBC a power of two (the common shapes: m = 4 with R in {1, 2, 4, 8, 16},
-// m = 2 with any R whose period is <= 16 rows).  A unit (16 periods) is then 256 RBC CONTIGUOUS
-// elements and lane l's 16-byte piece q of a stage is elements 8 (l + 32 q): the stage of a warp
+// Natural layout, PR = RBC <= 8 or 16 rows (m = 4 with R <= 8 or 16, m = 2 with a period of that
+// many rows).  A unit (16 periods) is 256 RBC CONTIGUOUS elements and lane l's 16-byte piece q of a stage is elements 8 (l + 32 q): the stage of a warp
 // is UPS consecutive units (one 2 KiB cp.async burst per stage for the one-row shapes instead of
 // a 512-byte one), every address and ring offset is a compile-time constant plus a per-lane
 // invariant, chunk results leave through precomputed shared addresses, and the overflow note is
@@ -1159,7 +1158,8 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     if (g.m == 2 || g.m == 4) {
         NatShape S;
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
-        const bool fast = S.PR == S.RB && (S.RB & (S.RB - 1)) == 0;   // PR a power of two <= 16
+        // PR <= 8 or 16: a unit of 16 periods is one contiguous stage of 512 PR bytes
+        const bool fast = S.PR == S.RB && (S.PR <= 8 || S.PR == 16) && !std::getenv("TCR_GM_NAT_GENERIC");
         if (fast) {
             const char* alt = std::getenv("TCR_GM_NAT_ALT");           // knob: ring shape A/B
             const int a = alt ? std::atoi(alt) : 0;
@@ -1181,6 +1181,10 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         break;                                                                \
     case 2: if (a == 3) TCR_NATF(MV, 2, 2, 4) else TCR_NATFX(MV, 2, 2, 4) break; \
     case 4: if (a == 3) TCR_NATF(MV, 4, 1, 4) else TCR_NATFX(MV, 4, 1, 4) break; \
+    case 3: TCR_NATFX(MV, 3, 1, 4) break;                                     \
+    case 5: TCR_NATFX(MV, 5, 1, 3) break;                                     \
+    case 6: TCR_NATFX(MV, 6, 1, 3) break;                                     \
+    case 7: TCR_NATFX(MV, 7, 1, 3) break;                                     \
     case 8: TCR_NATF(MV, 8, 1, 2) break;                                      \
     default: TCR_NATF(MV, 16, 1, 2) break;                                    \
     }
