@@ -486,14 +486,17 @@ struct TrStage {
     static constexpr uint32_t FLOATS = ROWS * SW;                                 // per warp
 };
 
-template <int MM, int SI, bool REPAIR>   // MM = 8, 32, 64, 128
+template <int MM, int SI, int KC, bool REPAIR>   // MM = 8, 32, 64, 128
 __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, const TrShape S) {
     // stages of T tiles: m >= 32 items are K = R (m/16)^2 (a multiple of 4) contiguous tiles, so a
     // 2 KiB stage of 4 tiles stays inside one item (one issue / wait / sync per 4 tiles); m = 8
     // with one-tile items (K = 1: R = 1, 2, 4) is dealt to the warps in runs of SI = 4 adjacent
-    // items, a stage = one run (SI = 1: items dealt one by one, one tile per stage).
+    // items, a stage = one run (SI = 1: items dealt one by one, one tile per stage).  KC > 1:
+    // m = 8 items of exactly KC tiles (R = 3, 5, 7, 8, ...), one whole item per stage, the
+    // straddling selectors precomputed per tile.
     static_assert(SI == 1 || MM == 8, "item runs only for one-tile items");
-    constexpr uint32_t T = MM >= 32 ? 4u : uint32_t(SI);
+    static_assert(KC == 1 || (MM == 8 && SI == 1), "whole-item stages only for m = 8");
+    constexpr uint32_t T = MM >= 32 ? 4u : (SI > 1 ? uint32_t(SI) : uint32_t(KC));
     constexpr int D = kGmTrDepth / int(T);
     constexpr uint32_t SG = MM >= 32 ? MM / 16 : 1;    // column groups per chunk (m >= 32)
     using ST = TrStage<MM>;
@@ -520,6 +523,12 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
     };
     uint32_t b0 = sel2(bsel(0, 2 * c), bsel(0, 2 * c + 1)), b1 = sel2(bsel(0, 2 * c + 8), bsel(0, 2 * c + 9));
     const bool straddle = MM == 8 && S.CPT > 1 && S.K > 1;      // m = 8, R odd or R = 2 mod 4
+    uint32_t bk0[KC], bk1[KC];                                   // KC > 1: selectors of tile t
+#pragma unroll
+    for (int kt = 0; kt < KC; ++kt) {
+        bk0[kt] = sel2(bsel(kt, 2 * c), bsel(kt, 2 * c + 1));
+        bk1[kt] = sel2(bsel(kt, 2 * c + 8), bsel(kt, 2 * c + 9));
+    }
     // swizzled 16-byte lines (conflict-free transposing ldmatrix), as in tcr_sp_async.cu
     auto swz = [](uint32_t k, uint32_t h) { return 32u * k + 16u * (h ^ ((k >> 2) & 1u)); };
     const uint32_t cp_dst = swz(lane >> 1, lane & 1u);
@@ -613,7 +622,10 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
                 for (uint32_t t = 0; t < T; ++t) {
                     uint32_t d0, d1, d2, d3;
                     ldsm4t(ring + cslot * (512u * T) + 512u * t + ld_off, d0, d1, d2, d3);
-                    if (straddle) {
+                    if (KC > 1) {
+                        b0 = bk0[t % KC];
+                        b1 = bk1[t % KC];
+                    } else if (straddle) {
                         b0 = sel2(bsel(ck + t, 2 * c), bsel(ck + t, 2 * c + 1));
                         b1 = sel2(bsel(ck + t, 2 * c + 8), bsel(ck + t, 2 * c + 9));
                     }
@@ -1228,12 +1240,18 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     uint32_t stage = 0;
     switch (g.m) {
     case 8:
-        fn = S.K == 1 && !std::getenv("TCR_GM_TR8_SINGLE") ? gm_tr_kernel<8, 4, REPAIR> : gm_tr_kernel<8, 1, REPAIR>;
+        if (std::getenv("TCR_GM_TR8_SINGLE")) fn = gm_tr_kernel<8, 1, 1, REPAIR>;   // knob: A/B
+        else if (S.K == 1) fn = gm_tr_kernel<8, 4, 1, REPAIR>;
+        else if (S.K == 2) fn = gm_tr_kernel<8, 1, 2, REPAIR>;
+        else if (S.K == 3) fn = gm_tr_kernel<8, 1, 3, REPAIR>;
+        else if (S.K == 5) fn = gm_tr_kernel<8, 1, 5, REPAIR>;
+        else if (S.K == 7) fn = gm_tr_kernel<8, 1, 7, REPAIR>;
+        else fn = gm_tr_kernel<8, 1, 1, REPAIR>;
         stage = TrStage<8>::FLOATS;
         break;
-    case 32: fn = gm_tr_kernel<32, 1, REPAIR>; stage = TrStage<32>::FLOATS; break;
-    case 64: fn = gm_tr_kernel<64, 1, REPAIR>; stage = TrStage<64>::FLOATS; break;
-    case 128: fn = gm_tr_kernel<128, 1, REPAIR>; stage = TrStage<128>::FLOATS; break;
+    case 32: fn = gm_tr_kernel<32, 1, 1, REPAIR>; stage = TrStage<32>::FLOATS; break;
+    case 64: fn = gm_tr_kernel<64, 1, 1, REPAIR>; stage = TrStage<64>::FLOATS; break;
+    case 128: fn = gm_tr_kernel<128, 1, 1, REPAIR>; stage = TrStage<128>::FLOATS; break;
     default: return cudaErrorInvalidValue;
     }
     return launch_gm(fn, kGmWarps * (kGmTrDepth * 512u + stage * 4u) + tables, groups, p, S, s);
