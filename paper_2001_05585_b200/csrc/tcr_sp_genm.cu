@@ -681,15 +681,17 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
 // ascending-j finishing sum (:182, fragment.hpp:89-92), carried across the m / 256 slabs.
 template <bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, const uint32_t m) {
-    constexpr int D = kGmTrDepth;
+    // 2 KiB stages: tiles of 4 consecutive rows of one slab (R m rows, a multiple of 4)
+    constexpr uint32_t T = 4;
+    constexpr int D = kGmTrDepth / int(T);
     extern __shared__ __align__(128) unsigned char s_ring[];   // [kGmWarps][D][512] + tables
     __shared__ float s_scratch[32];
     __shared__ int s_last;
-    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * D * 512);
+    float* s_chunk = reinterpret_cast<float*>(s_ring + kGmWarps * kGmTrDepth * 512);
     float* s_block = s_chunk + p.G * p.W;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
-    const uint32_t ring = smem_u32(s_ring) + warp * D * 512u;
+    const uint32_t ring = smem_u32(s_ring) + warp * kGmTrDepth * 512u;
     const uint32_t Cg = p.G * p.W;
     const uint32_t rows = p.R * m;                  // rows of a chunk (R fragments)
     const uint32_t slabs = m / 256u;
@@ -708,7 +710,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
         uint32_t it, s, i;
     };
     auto advance = [&](Cur& q) {
-        if (++q.i == rows) {
+        if ((q.i += T) == rows) {
             q.i = 0;
             if (++q.s == slabs) {
                 q.s = 0;
@@ -723,10 +725,14 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
         uint32_t slot_i = 0, slot_c = 0;
         auto issue = [&]() {
             if (iq.it < my_items) {
-                const uint64_t e = gel0 + uint64_t(warp + iq.it * kGmWarps) * chunk_el + uint64_t(iq.i) * m +
-                                   256u * iq.s + 8u * lane;
-                const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
-                cp16(ring + slot_i * 512u + cp_dst, x + (e < p.n ? e : 0), bytes);
+                const uint64_t e0 = gel0 + uint64_t(warp + iq.it * kGmWarps) * chunk_el + uint64_t(iq.i) * m +
+                                    256u * iq.s + 8u * lane;
+#pragma unroll
+                for (uint32_t q = 0; q < T; ++q) {
+                    const uint64_t e = e0 + uint64_t(q) * m;
+                    const uint32_t bytes = e + 8 <= p.n ? 16u : (e < p.n ? uint32_t(p.n - e) * 2u : 0u);
+                    cp16(ring + slot_i * (512u * T) + 512u * q + cp_dst, x + (e < p.n ? e : 0), bytes);
+                }
                 advance(iq);
             }
             cp_commit();
@@ -740,15 +746,18 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
             issue();
             cp_wait<D - 1>();
             __syncwarp();
-            uint32_t d0, d1, d2, d3;
-            ldsm4t(ring + slot_c * 512u + ld_off, d0, d1, d2, d3);
+#pragma unroll
+            for (uint32_t q = 0; q < T; ++q) {
+                uint32_t d0, d1, d2, d3;
+                ldsm4t(ring + slot_c * (512u * T) + 512u * q + ld_off, d0, d1, d2, d3);
+                mma_16816(lo, d0, d1, d2, d3, blo0, blo1);
+                mma_16816(hi, d0, d1, d2, d3, bhi0, bhi1);
+            }
             __syncwarp();
             slot_c = slot_c + 1 == D ? 0 : slot_c + 1;
-            mma_16816(lo, d0, d1, d2, d3, blo0, blo1);
-            mma_16816(hi, d0, d1, d2, d3, bhi0, bhi1);
             const Cur done = cq;
             advance(cq);
-            if (done.i + 1 < rows) continue;
+            if (done.i + T < rows) continue;
             // ---- slab complete: D[j16][n] = partial of column 256 s + 16 n + j16 (n < 8 in lo)
             const float hl[4] = {h_round(lo[0]), h_round(lo[1]), h_round(lo[2]), h_round(lo[3])};
             const float hh[4] = {h_round(hi[0]), h_round(hi[1]), h_round(hi[2]), h_round(hi[3])};
