@@ -1,6 +1,7 @@
 // tcr_pipeline.cuh -- shared sm_100a pipeline pieces: mbarriers, TMA / bulk copies, named
 // barriers, the canonical pairwise trees and the last-CTA finaliser.
 #pragma once
+#include <type_traits>
 
 #include <cuda.h>
 #include <cstdint>
@@ -265,15 +266,19 @@ __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t b
     const uint32_t W = p.W;
     const unsigned lane = lane_id();
     if (W <= 8) {
-        for (uint32_t b = w * 32u + lane; b < nblk; b += nwarps * 32u) {
-            float x;
-            if (W == 1) x = chunks[b];
-            else if (W == 2) x = lane_block_tree<2>(chunks, W, b);
-            else if (W <= 4) x = lane_block_tree<4>(chunks, W, b);
-            else x = lane_block_tree<8>(chunks, W, b);
-            blocks[b] = x;
-            publish_block(p, block0 + b, x);
-        }
+        // the W dispatch hoisted out of the block loop (one loop per tree width)
+        auto run = [&](auto pw) {
+            constexpr int PW = decltype(pw)::value;
+            for (uint32_t b = w * 32u + lane; b < nblk; b += nwarps * 32u) {
+                const float x = PW == 1 ? chunks[b] : lane_block_tree<PW>(chunks, W, b);
+                blocks[b] = x;
+                publish_block(p, block0 + b, x);
+            }
+        };
+        if (W == 1) run(std::integral_constant<int, 1>{});
+        else if (W == 2) run(std::integral_constant<int, 2>{});
+        else if (W <= 4) run(std::integral_constant<int, 4>{});
+        else run(std::integral_constant<int, 8>{});
         return;
     }
     uint32_t P = 1;

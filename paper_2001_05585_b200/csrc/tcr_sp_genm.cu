@@ -96,7 +96,19 @@ __device__ __forceinline__ void group_tree_cta(const SpParams& p, uint64_t gi, c
     const uint32_t seg = G >= uint32_t(kGmThreads) ? G / kGmThreads : 1;
     const uint32_t lo = threadIdx.x * seg;
     float acc = 0.0f;
-    if (lo < G) {
+    if (seg <= 8 && lo < G) {
+        // short segments: the same adjacent tree unrolled in registers (no stack frame)
+        const float* v = blocks + lo;
+        if (seg == 1) {
+            acc = v[0];
+        } else if (seg == 2) {
+            acc = v[0] + v[1];
+        } else if (seg == 4) {
+            acc = (v[0] + v[1]) + (v[2] + v[3]);
+        } else {
+            acc = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+        }
+    } else if (lo < G) {
         float stk[16];
         int top = 0;
         for (uint32_t i = 0; i < seg; ++i) {

@@ -346,7 +346,11 @@ GENM = [(2, 1, 128), (2, 2, 64), (2, 4, 32), (4, 1, 128), (4, 4, 128), (4, 3, 96
         # R > 16: several row-block stages per period), wide fragments (m >= 256: column slabs)
         (2, 3, 128), (2, 5, 32), (2, 6, 96), (2, 7, 64), (2, 20, 32), (2, 68, 64), (4, 17, 32), (4, 33, 64),
         (8, 3, 128), (8, 5, 32), (8, 6, 64), (8, 7, 256), (8, 10, 32), (256, 1, 32), (256, 3, 64),
-        (512, 1, 32), (1024, 1, 32), (1024, 2, 64), (2048, 1, 32)]
+        (512, 1, 32), (1024, 1, 32), (1024, 2, 64), (2048, 1, 32),
+        # 2 KiB-stage forms: one-unit stages for 3..8-row periods (m = 4 R = 5 B = 32 is the
+        # reference's curve_config), whole-item m = 8 stages, item runs at B = 1024, m >= 4096
+        (4, 5, 32), (4, 6, 1024), (4, 7, 96), (4, 8, 128), (4, 16, 64), (8, 1, 1024), (8, 2, 1024),
+        (2, 1, 1024), (4096, 1, 32)]
 
 
 @pytest.mark.parametrize("m,R,B", GENM)
