@@ -172,25 +172,21 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
-// RBC == 0 (the instantiation launched): any PR, row blocks of S.RB rows.  Power-of-two periods
-// run gm_nat_fast_kernel below (RBC > 0 here is the earlier form of that fast path, kept
-// compilable for A/B builds).  A cross-group issue cursor and register-capped variants of this
-// generic kernel measured 1-10 % SLOWER on m = 4 R = 3, 5, 6 and m = 2 R = 3.
-template <int RBC>
-__host__ __device__ constexpr int nat_depth() { return RBC == 0 ? 2 : (8 / RBC > 2 ? 8 / RBC : 2); }
-
-template <int M, int RBC, bool REPAIR>
+// Generic natural layout for the periods gm_nat_fast_kernel does not take (9-15 rows, or more
+// than 16): stages are row blocks of RB = min(PR, 16) rows of all 16 periods, two per warp.  (A cross-group issue cursor and
+// register-capped variants measured 1-10 % slower here.)
+template <int M, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, const NatShape S) {
-    constexpr int ND = nat_depth<RBC>();
+    constexpr int ND = 2;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     const unsigned g = lane >> 2, c = lane & 3u;
     const uint32_t R = p.R;
-    const uint32_t RB = RBC ? uint32_t(RBC) : S.RB;
-    const uint32_t PR = RBC ? uint32_t(RBC) : S.PR;
-    const uint32_t nblk = RBC ? 1u : (PR + RB - 1) / RB;               // stages per unit
+    const uint32_t RB = S.RB;
+    const uint32_t PR = S.PR;
+    const uint32_t nblk = (PR + RB - 1) / RB;               // stages per unit
     const uint32_t stage_bytes = 16u * RB * 32u;
     float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * ND * stage_bytes);
     float* s_block = s_chunk + p.G * p.W;
@@ -227,19 +223,19 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
         uint32_t iu = 0, iblk = 0, islot = 0;                             // issue cursor
         auto issue = [&]() {
             if (iu < my_units) {
-                const uint32_t r0 = iblk * RB, rb = RBC ? uint32_t(RBC) : min(RB, PR - r0);
+                const uint32_t r0 = iblk * RB, rb = min(RB, PR - r0);
                 const uint64_t e_unit = gel0 + uint64_t(warp + iu * kGmWarps) * 16u * period_el + r0 * 16u;
                 const uint32_t dst = ring + islot * stage_bytes;
                 // piece = lane + 32 t = per * 2 rb + rr: compile-time shifts on the fast path,
                 // one division per stage then increments on the generic one (any rb <= 16)
-                const bool last = !RBC && rb != RB;
-                uint32_t per = RBC ? lane / (2u * RBC) : (last ? lane / (2u * rb) : gper0);
-                uint32_t rr = RBC ? lane % (2u * RBC) : (last ? lane % (2u * rb) : grr0);
-                const uint32_t dq = RBC ? 32u / (2u * RBC) : (last ? 32u / (2u * rb) : gdq);
-                const uint32_t dr = RBC ? 32u % (2u * RBC) : (last ? 32u % (2u * rb) : gdr);
+                const bool last = rb != RB;
+                uint32_t per = last ? lane / (2u * rb) : gper0;
+                uint32_t rr = last ? lane % (2u * rb) : grr0;
+                const uint32_t dq = last ? 32u / (2u * rb) : gdq;
+                const uint32_t dr = last ? 32u % (2u * rb) : gdr;
 #pragma unroll
-                for (uint32_t t = 0; t < (RBC ? uint32_t(RBC) : 16u); ++t) {
-                    if (!RBC && t >= rb) break;
+                for (uint32_t t = 0; t < 16u; ++t) {
+                    if (t >= rb) break;
                     const uint32_t piece = lane + 32u * t;
                     const uint64_t e = e_unit + per * period_el + rr * 8u;
                     if (full) {
@@ -273,10 +269,10 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
             __syncwarp();
             const uint32_t base = ring + cslot * stage_bytes;
             cslot = cslot + 1 == uint32_t(ND) ? 0 : cslot + 1;
-            const uint32_t r0 = cblk * RB, rb = RBC ? uint32_t(RBC) : min(RB, PR - r0);
+            const uint32_t r0 = cblk * RB, rb = min(RB, PR - r0);
 #pragma unroll
-            for (uint32_t i = 0; i < (RBC ? uint32_t(RBC) : 16u); ++i) {
-                if (!RBC && i >= rb) break;
+            for (uint32_t i = 0; i < 16u; ++i) {
+                if (i >= rb) break;
                 if (straddle) {
                     const uint32_t rho = r0 + i;
                     b0 = sel2(bsel(rho, 2 * c), bsel(rho, 2 * c + 1));
@@ -1232,8 +1228,8 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
             return launch_gm(ff, kGmWarps * nd * stage + tables, groups, p, S, s);
         }
         // any other period (rows not a power of two, or more than 16): row blocks of <= 16 rows
-        void (*fn)(SpParams, NatShape) = g.m == 2 ? gm_nat_kernel<2, 0, REPAIR> : gm_nat_kernel<4, 0, REPAIR>;
-        return launch_gm(fn, kGmWarps * uint32_t(nat_depth<0>()) * (16u * S.RB * 32u) + tables, groups, p, S, s);
+        void (*fn)(SpParams, NatShape) = g.m == 2 ? gm_nat_kernel<2, REPAIR> : gm_nat_kernel<4, REPAIR>;
+        return launch_gm(fn, kGmWarps * 2u * (16u * S.RB * 32u) + tables, groups, p, S, s);
     }
     if (g.m >= 256) {
         if (!wide_ok(g)) return cudaErrorInvalidValue;
