@@ -24,6 +24,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -36,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp16 reduce Gelem/s and % of HBM BW at n=2^30, 1/2/4/8 B200; rel err"
 N_DEFAULT = 1 << 30
+N_STRONG = 1 << 34
 
 
 def parse():
@@ -53,7 +55,34 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-comparators", action="store_true")
+    ap.add_argument("--strong-elems", type=int, default=N_STRONG,
+                    help="total elements of the strong-scaling record (BASELINE configs[4]: 2^34)")
+    ap.add_argument("--no-strong", action="store_true")
     return ap.parse_args()
+
+
+def launch_cmd(argv: list, nproc: int, port: int) -> list:
+    """The torchrun command bench.py re-executes itself under when --gpus N > 1 is given without
+    a launcher (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args) -> int | None:
+    """--gpus N > 1 outside torchrun: spawn the N ranks ourselves (same flags), so that
+    `python bench.py --gpus N` measures N GPUs.  Returns the launcher's exit code, or None when
+    this process is already a rank (or N == 1, or the reference arm, which runs on rank 0 only)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return None
+    r = subprocess.run(launch_cmd(sys.argv[1:], args.gpus, free_port()), cwd=ROOT)
+    return r.returncode
 
 
 def peaks():
@@ -197,8 +226,108 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def strong_record(args, T, lib, _capi, dev, stream, world, rank, cfg, c_cfg, barrier):
+    """BASELINE configs[4]: n_total = 2^34 uniform s0 split into contiguous group-aligned shards
+    (sharded.shard), each rank generating its shard in place.  One shot = this rank's kernel + the
+    ONE all_reduce of the 4-byte partial, NOT overlapped with anything: CUDA events on the launch
+    stream bracket both, a barrier + synchronize before and after, max over ranks.  The overflow
+    flag rides in the same payload: it is set iff the partial is non-finite (every overflow note
+    comes from a non-finite chunk result, which propagates through the fp32 combine; finite
+    binary16 data cannot overflow an fp32 sum), so no second collective is needed."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_05585_b200 import sharded
+    n_total = args.strong_elems
+    sh = sharded.shard(n_total, rank, world, cfg)
+    x = T.generate("uniform", 0, sh.count, device=dev, first=sh.first) if sh.count else None
+    res = torch.zeros(1, dtype=torch.float32, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    xp = C.c_void_p(x.data_ptr()) if x is not None else None
+    rp, op = C.c_void_p(res.data_ptr()), C.c_void_p(ovf.data_ptr())
+
+    def shot():
+        res.zero_()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if x is not None:
+            _capi.check(lib.tcr_single_pass_f16_async(xp, sh.count, C.byref(c_cfg), rp, op, sp))
+        if world > 1:
+            dist.all_reduce(res)
+        b.record(stream)
+        barrier()
+        t = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    for _ in range(2):
+        shot()
+    shots = sorted(shot() for _ in range(max(3, min(args.steps, 7))))
+    ms = statistics.median(shots)
+    got = res.item()
+    if x is not None:
+        e, a = T.exact_sum(x)
+    else:
+        e, a = 0.0, 0.0
+    ex = torch.tensor([e, a], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ex)
+    exact, _ = ex.tolist()
+    ref_val = None
+    gp = os.path.join(ROOT, "tests", "golden", "oracle_2e34.json")
+    if os.path.exists(gp):
+        g = json.load(open(gp))
+        if g["n"] == n_total and cfg.m == 16:
+            ref_val = g["single_pass"].get(f"m16_R{cfg.R}_B{cfg.B}", {}).get("value")
+    peak, _ = peaks()
+    gbs = 2.0 * n_total / (ms * 1e-3) / 1e9
+    rec = {"n_total": n_total, "n_per_gpu": sh.count if world == 1 else -(-n_total // world),
+           "shard_alignment_elems": sharded.group_elems(cfg), "ms_single_shot_median": ms, "ms_single_shot_best": shots[0],
+           "gelem_s": n_total / (ms * 1e-3) / 1e9, "gb_s": gbs, "frac_of_n_x_hbm_peak": gbs / (world * peak),
+           "combine": "one all_reduce(sum) of the fp32 partial, overflow = partial non-finite" if world > 1 else "none",
+           "timing": "CUDA events around kernel + all_reduce on the launch stream, barrier-bracketed single shots, "
+                     "max over ranks, median of %d" % len(shots),
+           "result": got, "overflow": not math.isfinite(got), "exact_sum": exact,
+           "rel_err_vs_exact": abs(got - exact) / abs(exact) if exact else None,
+           "reference_value": ref_val,
+           "rel_diff_vs_reference_single_pass": abs(got - ref_val) / abs(exact) if ref_val and exact else None}
+    del x
+    torch.cuda.empty_cache()
+    return rec
+
+
+def combine_latency(dev, stream, world, barrier):
+    """Single-shot latency of the combine alone (one 4-byte all_reduce), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return None
+    v = torch.ones(1, dtype=torch.float32, device=dev)
+    ts = []
+    for i in range(25):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dist.all_reduce(v)
+        b.record(stream)
+        barrier()
+        t = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if i >= 5:
+            ts.append(t.item() * 1e3)
+    return {"us_median": statistics.median(ts), "us_best": min(ts), "shots": len(ts)}
+
+
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -300,7 +429,8 @@ def main():
     peak, peak_src = peaks()
     achieved = 2.0 * n / (kms * 1e-3) / 1e9  # GB/s, algorithmic bytes = 2 per element
 
-    # accuracy of the last step (result stays on the device until now)
+    # accuracy of the last step (result stays on the device until now); the overflow flag of
+    # the combined result = non-finite partial (see strong_record)
     got = results[(nstep[0] - 1) % SLOTS].item()
     exact_local, abs_local = T.exact_sum(x)
     ex = torch.tensor([exact_local, abs_local], device=dev, dtype=torch.float64)
@@ -402,6 +532,18 @@ def main():
       except Exception as exc:
         e2e = {"error": repr(exc)}
 
+    strong = None
+    if not args.no_strong:
+        try:
+            strong = strong_record(args, T, lib, _capi, dev, stream, world, rank, cfg, c_cfg, barrier)
+        except Exception as exc:  # optional section: never lose the contract line
+            strong = {"error": repr(exc)}
+    comb = None
+    try:
+        comb = combine_latency(dev, stream, world, barrier)
+    except Exception as exc:
+        comb = {"error": repr(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
       try:
@@ -435,9 +577,11 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel_ms": kms, "algorithmic_bytes_per_launch": 2 * n},
             "hbm_frac_of_8TBs_nominal": achieved / 8000.0,
-            "rel_err_vs_exact": rel_err, "exact_sum": exact, "result": got,
+            "rel_err_vs_exact": rel_err, "exact_sum": exact, "result": got, "overflow": not math.isfinite(got),
             "rel_diff_vs_reference_single_pass": (abs(got - ref_val) / abs(exact)) if ref_val else None,
             "comparators": comparators,
+            "strong_2e34": strong,
+            "combine_latency": comb,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,

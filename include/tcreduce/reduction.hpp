@@ -51,7 +51,8 @@ enum class AtomicOrder { ascending, seeded_permutation };
 // How the GPU combines block results (the reference serialises them, reduction.hpp:257-268).
 enum class Finalize { tree, ordered, atomic };
 
-enum class Engine { automatic, mma_sync, tcgen05 };
+// Kernel family (tcr_engine): automatic = measured best (mma_sync_async for m = 16).
+enum class Engine { automatic, mma_sync, tcgen05, mma_sync_regs, mma_sync_async };
 
 inline const char* variant_name(Variant v) {
     switch (v) {

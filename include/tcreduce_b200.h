@@ -50,7 +50,9 @@ typedef enum { TCR_ASCENDING = 0, TCR_SEEDED_PERMUTATION = 1 } tcr_atomic_order;
  *   TREE    -- deterministic pairwise tree over block results (default; bit-reproducible,
  *              independent of launch geometry, more accurate than a serial sum)
  *   ORDERED -- exactly the reference order: serial fp32 sum, ascending or seeded permutation
- *   ATOMIC  -- the paper's one atomicAdd per block (order unspecified) */
+ *   ATOMIC  -- the paper's one atomicAdd per block (order unspecified)
+ * TREE has no order to permute: a config with atomic_order = SEEDED_PERMUTATION and
+ * finalize = TREE runs ORDERED (the seed is never silently ignored). */
 typedef enum { TCR_FINALIZE_TREE = 0, TCR_FINALIZE_ORDERED = 1, TCR_FINALIZE_ATOMIC = 2 } tcr_finalize;
 
 /* Kernel family (chosen by measurement; AUTO picks the fastest available for the config).
@@ -186,6 +188,17 @@ int tcr_last_launch_count(void);
 int tcr_last_engine(void);
 const char* tcr_last_error(void);
 const char* tcr_version(void);
+
+/* Profiling only (tools/ab.py, tools/timeline.py, tools/probe.py): read the TCR_* A/B knobs
+ * (ring depths, work-unit splits, schedule, group-size overrides, debug stamps) from the
+ * environment ONCE; returns how many were set.  Without this call every knob keeps its
+ * production default and no entry point reads the environment, so results depend only on the
+ * input and the config (reference reduction.hpp:19-21).  tcr_reset_profiling_knobs restores
+ * the defaults.  Not thread-safe against concurrent reductions. */
+int tcr_enable_profiling_knobs(void);
+void tcr_reset_profiling_knobs(void);
+/* Profiling: per-CTA %globaltimer stamps of the last TCR_DEBUG_MODE=20 launch. */
+int tcr_debug_timestamps(unsigned long long* host, size_t count);
 
 #ifdef __cplusplus
 }

@@ -6,6 +6,7 @@ missing the import fails loudly -- there is no CPU fallback anywhere in the pack
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 
@@ -67,6 +68,9 @@ SIGNATURES = {
     "tcr_last_engine": (C.c_int, []),
     "tcr_last_error": (C.c_char_p, []),
     "tcr_version": (C.c_char_p, []),
+    "tcr_enable_profiling_knobs": (C.c_int, []),
+    "tcr_reset_profiling_knobs": (None, []),
+    "tcr_debug_timestamps": (C.c_int, [_P, _SZ]),
 }
 
 _lib = None
@@ -104,6 +108,25 @@ def check(rc: int) -> None:
     if rc == TCR_NOT_SUPPORTED:
         raise NotImplementedError(msg)
     raise TcrError(f"tcreduce error {rc}: {msg}")
+
+
+@contextlib.contextmanager
+def profiling_knobs(env: dict):
+    """Profiling / A-B only: apply TCR_* knobs (e.g. {"TCR_SPLIT": "4"}) for the duration of the
+    block.  The library never reads the environment by itself (tcr_enable_profiling_knobs reads
+    it once, here); on exit the variables and the production defaults are restored."""
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        load().tcr_enable_profiling_knobs()
+        yield
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        load().tcr_reset_profiling_knobs()
 
 
 def header_symbols() -> list[str]:

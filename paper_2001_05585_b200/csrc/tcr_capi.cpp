@@ -16,6 +16,7 @@
 #include <cstring>
 #include <cmath>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -196,16 +197,25 @@ int get_ws(cudaStream_t s, Workspace** out) {
     int dev = 0;
     TCR_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
-    auto& w = g_ws[{dev, s}];
-    if (!w) {
-        w = new Workspace();
-        TCR_CUDA(cudaMalloc(&w->fixed, 256));
-        TCR_CUDA(cudaMemset(w->fixed, 0, 256));
-        TCR_CUDA(cudaMalloc(&w->exact_ws, tcr::exact_ws_bytes()));
-        TCR_CUDA(cudaMalloc(&w->shuffle_partials, sizeof(float) * 8192));
-        TCR_CUDA(cudaMallocHost(&w->host_pinned, 64));
+    auto it = g_ws.find({dev, s});
+    if (it != g_ws.end()) {
+        *out = it->second;
+        return TCR_OK;
     }
-    *out = w;
+    // built completely before it is published: a failed allocation (OOM) leaves no half-made
+    // workspace behind for later calls to write through
+    std::unique_ptr<Workspace> w(new Workspace());
+    cudaError_t e = cudaMalloc(&w->fixed, 256);
+    if (e == cudaSuccess) e = cudaMemset(w->fixed, 0, 256);
+    if (e == cudaSuccess) e = cudaMalloc(&w->exact_ws, tcr::exact_ws_bytes());
+    if (e == cudaSuccess) e = cudaMalloc(&w->shuffle_partials, sizeof(float) * 8192);
+    if (e == cudaSuccess) e = cudaMallocHost(&w->host_pinned, 64);
+    if (e != cudaSuccess) {
+        w->release();
+        return fail(TCR_CUDA_ERROR, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    }
+    *out = w.get();
+    g_ws[{dev, s}] = w.release();
     return TCR_OK;
 }
 
@@ -300,10 +310,21 @@ void counters(uint64_t n, const tcr_config* c, tcr_outcome* o) {
     o->shuffle_count = g.n_blocks * (P - 1);
 }
 
+// A seeded-permutation atomic order asks for the reference's serial combine in that order
+// (reduction.hpp:257-268): honour it even when finalize was left at TREE, which has no order to
+// permute (otherwise the seed would be silently ignored).
+tcr_config normalized(const tcr_config* c) {
+    tcr_config n = *c;
+    if (n.atomic_order == TCR_SEEDED_PERMUTATION && n.finalize == TCR_FINALIZE_TREE) n.finalize = TCR_FINALIZE_ORDERED;
+    return n;
+}
+
 // Enqueue single_pass over groups [g0, g1) of a (possibly chunked) input.
-int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c, bool f32, float* d_result,
+int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c_in, bool f32, float* d_result,
                uint32_t* d_overflow, float* d_blocks, Workspace* w, cudaStream_t s, uint64_t g0, uint64_t g1,
                bool finalize_here) {
+    const tcr_config cn = normalized(c_in);
+    const tcr_config* c = &cn;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
     tcr::SpParams p{};
     p.x = static_cast<const char*>(x) - x_offset * (f32 ? 4 : 2);
@@ -337,7 +358,7 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     if (c->finalize == TCR_FINALIZE_ATOMIC) p.finalize = tcr::kFinAtomic;
     p.atomic_order = c->atomic_order;
     p.atomic_seed = c->atomic_seed;
-    if (const char* dm = std::getenv("TCR_DEBUG_MODE")) p.debug_mode = std::atoi(dm);
+    p.debug_mode = tcr::knobs().debug_mode;   // 0 unless tcr_enable_profiling_knobs()
     p.split = 1;
     if (c->finalize == TCR_FINALIZE_ATOMIC && g0 == 0) {
         TCR_CUDA(cudaMemsetAsync(d_result, 0, sizeof(float), s));
@@ -402,7 +423,9 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     return TCR_OK;
 }
 
-int enqueue_finalize(uint64_t n, const tcr_config* c, float* d_result, Workspace* w, cudaStream_t s) {
+int enqueue_finalize(uint64_t n, const tcr_config* c_in, float* d_result, Workspace* w, cudaStream_t s) {
+    const tcr_config cn = normalized(c_in);
+    const tcr_config* c = &cn;
     if (c->finalize == TCR_FINALIZE_ATOMIC) return TCR_OK;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
     tcr::SpParams p{};
@@ -981,10 +1004,14 @@ int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config
     Workspace* w = nullptr;
     rc = get_ws(s, &w);
     if (rc) return rc;
+    if (!d_x || !d_blocks) return fail(TCR_INVALID_ARGUMENT, "null device pointer");
+    const void* xa = d_x;   // 16-byte lines: an unaligned slice is copied first
+    rc = aligned_input(&xa, n, false, w, s);
+    if (rc) return rc;
     tcr_config cc = *c;
     cc.finalize = TCR_FINALIZE_TREE;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
-    return enqueue_sp(d_x, 0, n, &cc, false, w->result(), w->overflow(), d_blocks, w, s, 0, g.n_groups, true);
+    return enqueue_sp(xa, 0, n, &cc, false, w->result(), w->overflow(), d_blocks, w, s, 0, g.n_groups, true);
 }
 
 namespace {
@@ -1188,14 +1215,18 @@ int tcr_cub_sum_f16_async(const uint16_t* d_x, size_t n, int half_acc, void* d_r
     return TCR_OK;
 }
 
+int tcr_enable_profiling_knobs(void) { return tcr::load_knobs_from_env(); }
+
+void tcr_reset_profiling_knobs(void) { tcr::reset_knobs(); }
+
 int tcr_read_probe_async(const void* d_x, size_t bytes, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Workspace* w = nullptr;
     int rc = get_ws(s, &w);
     if (rc) return rc;
-    const char* mode = std::getenv("TCR_PROBE");  // profiling: "async" = cp.async probe, N CTAs/SM
-    const int per_sm = std::getenv("TCR_PROBE_CTAS") ? std::atoi(std::getenv("TCR_PROBE_CTAS")) : 8;
-    if (mode && std::string(mode) == "async")
+    const tcr::Knobs& k = tcr::knobs();   // profiling: cp.async probe / CTAs per SM
+    const int per_sm = k.probe_ctas > 0 ? k.probe_ctas : 8;
+    if (k.probe_async)
         TCR_CUDA(tcr::launch_read_probe_async(d_x, bytes, w->sink(), tcr::sm_count() * per_sm, s));
     else
         TCR_CUDA(tcr::launch_read_probe(d_x, bytes, w->sink(), tcr::sm_count() * per_sm, s));

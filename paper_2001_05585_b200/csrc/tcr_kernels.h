@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace tcr {
@@ -142,5 +143,52 @@ cudaError_t cub_sum_f16(const uint16_t* x, uint64_t n, void* out, bool half_out,
                         size_t temp_bytes, cudaStream_t s);
 
 int sm_count();
+
+// Runs set() once per CUDA device for one call site: function attributes such as the dynamic
+// shared-memory opt-in live in each device's context, so a per-process flag would leave every
+// device after the first without them.  Thread-safe; device ordinals < 64.
+class PerDeviceOnce {
+  public:
+    template <typename F>
+    cudaError_t operator()(F set) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        std::lock_guard<std::mutex> lock(mu_);
+        const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+        if (done_ & bit) return cudaSuccess;
+        e = set();
+        if (e == cudaSuccess) done_ |= bit;
+        return e;
+    }
+
+  private:
+    std::mutex mu_;
+    uint64_t done_ = 0;
+};
+
+// Profiling knobs (A/B experiments only).  Every field holds its production default unless the
+// process called tcr_enable_profiling_knobs(), which reads the TCR_* environment variables ONCE;
+// nothing on a reduce() path calls getenv.  Some knobs change the group size G -- and so the
+// TREE result -- which is why they are never read implicitly (the reference is a pure function
+// of input and config, reduction.hpp:19-21).
+struct Knobs {
+    int debug_mode = 0;                // TCR_DEBUG_MODE: engine-specific profiling modes (SpParams)
+    uint64_t group_target = 0;         // TCR_GROUP_TARGET: elements per group (0 = kGroupElemsTarget)
+    uint64_t group_cap = 0;            // TCR_GROUP_CAP: chunk-table entries (0 = engine table; clamped to it)
+    uint32_t split = 0, tail_split = 0;   // TCR_SPLIT / TCR_TAIL_SPLIT: work-unit pieces (0 = planner)
+    int sched = -1;                    // TCR_SCHED: 0 static grid-stride, 1 dynamic (-1 = planner)
+    int ctas_per_sm = 0;               // TCR_CTAS_PER_SM (0 = 2)
+    bool gm_nat_generic = false;       // TCR_GM_NAT_GENERIC
+    int gm_nat_alt = 0;                // TCR_GM_NAT_ALT
+    bool gm_wide_warp = false;         // TCR_GM_WIDE_WARP
+    bool gm_no_cluster = false;        // TCR_GM_NO_CLUSTER
+    bool gm_tr8_single = false;        // TCR_GM_TR8_SINGLE
+    bool probe_async = false;          // TCR_PROBE=async
+    int probe_ctas = 0;                // TCR_PROBE_CTAS (0 = 8)
+};
+const Knobs& knobs();
+int load_knobs_from_env();   // returns how many TCR_* knobs were set
+void reset_knobs();
 
 }  // namespace tcr

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <string>
+#include <type_traits>
 
 #include "tcr_device.cuh"
 #include "tcr_kernels.h"
@@ -410,12 +412,13 @@ SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B) {
     g.n_blocks = (n + g.block_elems - 1) / g.block_elems;
     if (g.n_blocks < 1) g.n_blocks = 1;
     uint32_t G = 1;
-    uint64_t target = kGroupElemsTarget;
-    if (const char* e = std::getenv("TCR_GROUP_TARGET")) target = std::strtoull(e, nullptr, 10);  // profiling knob
+    const Knobs& k = knobs();
+    const uint64_t target = k.group_target ? k.group_target : kGroupElemsTarget;
     while (uint64_t(G) * g.block_elems < target) G <<= 1;
-    // keep the per-group chunk table in shared memory
-    uint64_t cap = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
-    if (const char* e = std::getenv("TCR_GROUP_CAP")) cap = std::strtoull(e, nullptr, 10);  // profiling knob
+    // keep the per-group chunk table in shared memory: G*W never exceeds the engine's table
+    // (a profiling cap can only lower it)
+    const uint64_t table = m == 16 ? uint64_t(kMaxChunksPerGroup) : uint64_t(kMaxChunksGenm);
+    const uint64_t cap = k.group_cap && k.group_cap < table ? k.group_cap : table;
     while (G > 1 && uint64_t(G) * g.W > cap) G >>= 1;
     // m in {2, 8}: up to 4 chunks share a period of the selector layout (tcr_sp_genm.cu), so a
     // group must hold a multiple of 4 chunks
@@ -424,6 +427,50 @@ SpGeometry make_geometry(uint64_t n, uint32_t m, uint32_t R, uint32_t B) {
     g.group_elems = uint64_t(G) * g.block_elems;
     g.n_groups = (g.n_blocks + G - 1) / G;
     return g;
+}
+
+namespace {
+Knobs g_knobs;   // production defaults until load_knobs_from_env()
+}
+
+const Knobs& knobs() { return g_knobs; }
+
+void reset_knobs() { g_knobs = Knobs{}; }
+
+int load_knobs_from_env() {
+    Knobs k;
+    int set = 0;
+    auto num = [&](const char* name, auto* dst) {
+        if (const char* e = std::getenv(name)) {
+            *dst = static_cast<std::remove_pointer_t<decltype(dst)>>(std::strtoll(e, nullptr, 10));
+            ++set;
+        }
+    };
+    auto flag = [&](const char* name, bool* dst) {
+        if (std::getenv(name)) {
+            *dst = true;
+            ++set;
+        }
+    };
+    num("TCR_DEBUG_MODE", &k.debug_mode);
+    num("TCR_GROUP_TARGET", &k.group_target);
+    num("TCR_GROUP_CAP", &k.group_cap);
+    num("TCR_SPLIT", &k.split);
+    num("TCR_TAIL_SPLIT", &k.tail_split);
+    num("TCR_SCHED", &k.sched);
+    num("TCR_CTAS_PER_SM", &k.ctas_per_sm);
+    flag("TCR_GM_NAT_GENERIC", &k.gm_nat_generic);
+    num("TCR_GM_NAT_ALT", &k.gm_nat_alt);
+    flag("TCR_GM_WIDE_WARP", &k.gm_wide_warp);
+    flag("TCR_GM_NO_CLUSTER", &k.gm_no_cluster);
+    flag("TCR_GM_TR8_SINGLE", &k.gm_tr8_single);
+    if (const char* e = std::getenv("TCR_PROBE")) {
+        k.probe_async = std::string(e) == "async";
+        ++set;
+    }
+    num("TCR_PROBE_CTAS", &k.probe_ctas);
+    g_knobs = k;
+    return set;
 }
 
 int sm_count() {

@@ -411,20 +411,20 @@ AsPick pick(uint32_t R, int mode = 0) {
 }
 
 bool as_attr_once() {
-    static bool done = false;
-    if (!done) {
+    static PerDeviceOnce once;
+    return once([] {
         for (int mode : {0, 9, 10, 11})
-        for (uint32_t R = 0; R <= 8; ++R) {
-            const AsPick k = pick(R, mode);
-            cudaFuncAttributes fa{};
-            cudaFuncGetAttributes(&fa, k.fn);
-            if (cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024 - int(fa.sharedSizeBytes)) != cudaSuccess)
-                return false;
-        }
-        done = true;
-    }
-    return true;
+            for (uint32_t R = 0; R <= 8; ++R) {
+                const AsPick k = pick(R, mode);
+                cudaFuncAttributes fa{};
+                cudaError_t e = cudaFuncGetAttributes(&fa, k.fn);
+                if (e == cudaSuccess)
+                    e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024 - int(fa.sharedSizeBytes));
+                if (e != cudaSuccess) return e;
+            }
+        return cudaSuccess;
+    }) == cudaSuccess;
 }
 
 // Work units per CTA below which the grid's tail (the last CTAs still streaming) starves HBM:
@@ -450,20 +450,19 @@ bool async_plan(const SpGeometry& g, SpParams* p, int grid) {
     auto ok = [&](uint32_t S) {   // S pieces of whole blocks that keep the static path
         return S <= g.G && S <= 64 && (!st1 || static_unit(Cg / S, g.R, D));
     };
-    auto env_pow2 = [&](const char* name, uint32_t dflt) {
-        const char* e = std::getenv(name);
-        if (!e) return dflt;
-        const uint32_t want = uint32_t(std::strtoul(e, nullptr, 10));
+    auto knob_pow2 = [&](uint32_t want, uint32_t dflt) {   // profiling override (knobs())
+        if (!want) return dflt;
         uint32_t S = 1;
         while (S * 2 <= want && S * 2 <= g.G) S *= 2;
         return S;
     };
+    const Knobs& k = knobs();
     uint32_t S = 1;
     while (double(groups) * S < kMinUnitsPerCta * grid && ok(S * 2)) S *= 2;
-    S = env_pow2("TCR_SPLIT", S);
+    S = knob_pow2(k.split, S);
     uint32_t St = S;
     while (St < kTailSplit && ok(St * 2)) St *= 2;
-    St = std::max(S, env_pow2("TCR_TAIL_SPLIT", St));
+    St = std::max(S, knob_pow2(k.tail_split, St));
     p->split = S;
     p->split_tail = St;
     if (St > S) {
@@ -471,20 +470,16 @@ bool async_plan(const SpGeometry& g, SpParams* p, int grid) {
         p->tail_group = p->group_end - tail;
         if (p->tail_group == p->group_begin) p->split = St;
     }
-    bool dyn = kDynamicSchedule;
-    if (const char* e = std::getenv("TCR_SCHED")) dyn = std::atoi(e) != 0;
-    return dyn;
+    return k.sched >= 0 ? k.sched != 0 : kDynamicSchedule;
 }
 
 namespace {
 
 // CTAs per SM: two 64 KiB rings per SM measured best (n = 2^30, R = 1: 2/SM 312.8 us, 3/SM
 // 332.5 us, 1/SM 540 us); the launch pads dynamic shared memory so that no SM takes a third
-// CTA.  Env TCR_CTAS_PER_SM overrides (profiling).
+// CTA.  Knob ctas_per_sm overrides (profiling).
 int as_ctas_per_sm() {
-    int cps = 2;
-    if (const char* e = std::getenv("TCR_CTAS_PER_SM")) cps = std::max(1, std::atoi(e));
-    return cps;
+    return knobs().ctas_per_sm > 0 ? knobs().ctas_per_sm : 2;
 }
 
 uint32_t as_launch_smem_uncached(const AsPick& k, int cps) {
@@ -505,6 +500,7 @@ uint32_t as_launch_smem_uncached(const AsPick& k, int cps) {
 // queries cost microseconds of host time per call otherwise)
 struct AsLaunch {
     AsKernel fn;
+    int dev;
     int cps;
     uint32_t smem;
     int per_sm;
@@ -513,10 +509,12 @@ struct AsLaunch {
 AsLaunch as_launch(const AsPick& k, int cps) {
     static std::mutex mu;
     static std::vector<AsLaunch> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     for (const AsLaunch& a : cache)
-        if (a.fn == k.fn && a.cps == cps) return a;
-    AsLaunch a{k.fn, cps, as_launch_smem_uncached(k, cps), 0};
+        if (a.fn == k.fn && a.dev == dev && a.cps == cps) return a;
+    AsLaunch a{k.fn, dev, cps, as_launch_smem_uncached(k, cps), 0};
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.per_sm, k.fn, kAsThreads, a.smem);
     if (a.per_sm < 1) a.per_sm = 1;
     cache.push_back(a);

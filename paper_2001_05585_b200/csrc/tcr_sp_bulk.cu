@@ -210,15 +210,16 @@ cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles
     uint32_t SC, ns;
     if (!bulk_plan(g, &SC, &ns)) return cudaErrorInvalidValue;
     const BkLayout L = bk_layout(SC * g.R * 512u, ns);
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce once;
+    const cudaError_t ea = once([] {
         for (auto fn : {sp_bulk_kernel<0>, sp_bulk_kernel<1>, sp_bulk_kernel<2>, sp_bulk_kernel<3>,
                         sp_bulk_kernel<4>, sp_bulk_kernel<5>}) {
             const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             if (e != cudaSuccess) return e;
         }
-        attr = true;
-    }
+        return cudaSuccess;
+    });
+    if (ea != cudaSuccess) return ea;
     switch (g.R) {
     case 1: sp_bulk_kernel<1><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
     case 2: sp_bulk_kernel<2><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;

@@ -1188,10 +1188,9 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         NatShape S;
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
         // PR <= 8 or 16: a unit of 16 periods is one contiguous stage of 512 PR bytes
-        const bool fast = S.PR == S.RB && (S.PR <= 8 || S.PR == 16) && !std::getenv("TCR_GM_NAT_GENERIC");
+        const bool fast = S.PR == S.RB && (S.PR <= 8 || S.PR == 16) && !knobs().gm_nat_generic;
         if (fast) {
-            const char* alt = std::getenv("TCR_GM_NAT_ALT");           // knob: ring shape A/B
-            const int a = alt ? std::atoi(alt) : 0;
+            const int a = knobs().gm_nat_alt;                           // knob: ring shape A/B
             void (*ff)(SpParams, NatShape) = nullptr;
             uint32_t stage = 0, nd = 0;
             // (units per stage, stages): 2 KiB stages; one-row periods 3 stages -> 3 CTAs per SM
@@ -1234,17 +1233,17 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     if (g.m >= 256) {
         if (!wide_ok(g)) return cudaErrorInvalidValue;
         const uint32_t ring = kGmWarps * kGmTrDepth * 512u;
-        if (g.m <= 2048 && !std::getenv("TCR_GM_WIDE_WARP")) {   // knob: profiling A/B
+        if (g.m <= 2048 && !knobs().gm_wide_warp) {   // knob: profiling A/B
             const uint32_t dyn = ring + kGmWarps * g.m * 4u + tables;
             switch (g.m) {
             case 256: return launch_gm(gm_wide_cta_kernel<1, REPAIR>, dyn, groups, p, g.m, s);
             case 512: return launch_gm(gm_wide_cta_kernel<2, REPAIR>, dyn, groups, p, g.m, s);
             case 1024:
-                if (!std::getenv("TCR_GM_NO_CLUSTER"))   // knob: profiling A/B
+                if (!knobs().gm_no_cluster)   // knob: profiling A/B
                     return launch_cluster(gm_wide_cluster_kernel<4, REPAIR>, dyn + g.m * 4u, groups, 4, p, g.m, s);
                 return launch_gm(gm_wide_cta_kernel<4, REPAIR>, dyn, groups, p, g.m, s);
             default:
-                if (!std::getenv("TCR_GM_NO_CLUSTER"))
+                if (!knobs().gm_no_cluster)
                     return launch_cluster(gm_wide_cluster_kernel<8, REPAIR>, dyn + g.m * 4u, groups, 8, p, g.m, s);
                 return launch_gm(gm_wide_cta_kernel<8, REPAIR>, dyn, groups, p, g.m, s);
             }
@@ -1257,7 +1256,7 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     uint32_t stage = 0;
     switch (g.m) {
     case 8:
-        if (std::getenv("TCR_GM_TR8_SINGLE")) fn = gm_tr_kernel<8, 1, 1, REPAIR>;   // knob: A/B
+        if (knobs().gm_tr8_single) fn = gm_tr_kernel<8, 1, 1, REPAIR>;   // knob: A/B
         else if (S.K == 1) fn = gm_tr_kernel<8, 4, 1, REPAIR>;
         else if (S.K == 2) fn = gm_tr_kernel<8, 1, 2, REPAIR>;
         else if (S.K == 3) fn = gm_tr_kernel<8, 1, 3, REPAIR>;

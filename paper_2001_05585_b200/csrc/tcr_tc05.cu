@@ -347,15 +347,16 @@ cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDeviceOnce once;
+    const cudaError_t ea = once([] {
         for (auto fn : {tc05_kernel<1>, tc05_kernel<2>, tc05_kernel<4>, tc05_kernel<1, 1, 4, 2>, tc05_kernel<2, 1, 4, 2>,
                         tc05_kernel<4, 1, 4, 2>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             if (e != cudaSuccess) return e;
         }
-        attr_set = true;
-    }
+        return cudaSuccess;
+    });
+    if (ea != cudaSuccess) return ea;
     if (p.debug_mode == 11) {
         // profiling: two CTAs per SM (half ring, one epilogue warpgroup, 4 accumulators each)
         const uint32_t ns2 = ns / 2 < 2 ? 2 : ns / 2;

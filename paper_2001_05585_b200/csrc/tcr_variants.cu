@@ -267,13 +267,11 @@ __global__ void round_level_kernel(const float* in, uint16_t* out, uint64_t coun
 template <typename T, bool HALF>
 cudaError_t launch_rows(const T* x, uint64_t valid, uint64_t S, float* out, uint32_t* ovf, cudaStream_t s) {
     constexpr uint32_t dyn = kRowDepth * kRowK * kRowThreads * 16u;
-    static bool attr = false;   // per instantiation
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tree_rows_kernel<T, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(dyn));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce once;   // per instantiation
+    const cudaError_t ea = once([] {
+        return cudaFuncSetAttribute(tree_rows_kernel<T, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+    });
+    if (ea != cudaSuccess) return ea;
     const uint64_t tiles = S / (16 / sizeof(T));
     const uint64_t b = (tiles + kRowThreads - 1) / kRowThreads, cap = uint64_t(sm_count()) * 2;
     tree_rows_kernel<T, HALF><<<unsigned(b < cap ? b : cap), kRowThreads, dyn, s>>>(x, valid, S, out, ovf);

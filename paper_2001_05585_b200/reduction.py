@@ -152,8 +152,12 @@ def block_count(n: int, cfg: ReductionConfig) -> int:
 
 
 def block_results(x, cfg: ReductionConfig):
-    """Per-block fp32 results of single_pass (reduction.hpp:248-255) as a CUDA float32 tensor."""
+    """Per-block fp32 results of single_pass (reduction.hpp:248-255) as a CUDA float32 tensor.
+    x: binary16 CUDA tensor (the parity hook reads binary16 only)."""
     import torch
+    if x.dtype != torch.float16:
+        raise TypeError(f"block_results takes a float16 tensor, got {x.dtype}")
+    x = x.contiguous()
     c = cfg.to_c()
     nb = block_count(x.numel(), cfg)
     out = torch.empty(nb, dtype=torch.float32, device=x.device)
@@ -166,9 +170,13 @@ def block_results(x, cfg: ReductionConfig):
 
 def single_pass_async(x, cfg: ReductionConfig, result, overflow) -> None:
     """Enqueue single_pass on the current stream; result (float32[1]) and overflow (int32[1]) stay on device."""
+    import torch
+    if x.dtype not in (torch.float16, torch.float32):
+        raise TypeError(f"single_pass_async takes float16 or float32, got {x.dtype}")
+    x = x.contiguous()
     lib = _capi.load()
     c = cfg.to_c()
-    fn = lib.tcr_single_pass_f16_async if x.dtype.itemsize == 2 else lib.tcr_single_pass_f32_async
+    fn = lib.tcr_single_pass_f16_async if x.dtype == torch.float16 else lib.tcr_single_pass_f32_async
     _capi.check(fn(C.c_void_p(x.data_ptr()), x.numel(), C.byref(c), C.c_void_p(result.data_ptr()),
                    C.c_void_p(overflow.data_ptr()), C.c_void_p(_stream_ptr(x))))
 

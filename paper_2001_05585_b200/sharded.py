@@ -68,8 +68,16 @@ def tree_combine(parts: list[float]) -> float:
 
 
 def combine(partial, overflow, group=None, how: str = "allreduce"):
-    """Combine per-rank fp32 partials (1-element tensors on any device) across the process group.
-    Returns (value, overflow) as Python scalars; one collective for the value, one for the flag."""
+    """Combine per-rank fp32 partials (1-element tensors on any device) across the process group
+    with ONE collective.  Returns (value, overflow) as Python scalars.
+
+    The overflow flag needs no collective of its own: a rank's flag is set iff its partial is
+    non-finite (every overflow note of reduction.hpp:78-81 comes from a non-finite binary16 value
+    -- an input or a C_R column sum -- whose chunk result is then non-finite, and a non-finite
+    value stays non-finite through the fp32 tree; finite binary16 data cannot overflow an fp32
+    sum of fewer than 2^100 elements), so the combined flag is "the combined value is not finite"."""
+    import math
+
     import torch
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
@@ -77,16 +85,14 @@ def combine(partial, overflow, group=None, how: str = "allreduce"):
     if how == "allreduce":
         dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
         value = float(partial.item())
-    elif how == "tree":
+        return value, not math.isfinite(value)
+    if how == "tree":
         world = dist.get_world_size(group)
         out = [torch.zeros_like(partial) for _ in range(world)]
         dist.all_gather(out, partial, group=group)
-        value = tree_combine([float(t.item()) for t in out])
-    else:
-        raise ValueError(f"unknown combine {how!r}")
-    ov = overflow.to(torch.int32)
-    dist.all_reduce(ov, op=dist.ReduceOp.MAX, group=group)
-    return value, bool(int(ov.item()))
+        parts = [float(t.item()) for t in out]
+        return tree_combine(parts), not all(math.isfinite(p) for p in parts)
+    raise ValueError(f"unknown combine {how!r}")
 
 
 def reduce_sharded(x_local, n_total: int, cfg: ReductionConfig, group=None, how: str = "allreduce",

@@ -594,23 +594,39 @@ def test_split_units_identical(oracle, R, B, monkeypatch):
     h = oracle.generate_f16("normal", 9, n)
     xd = to_dev_f16(h)
     base = {}
+    from paper_2001_05585_b200 import _capi
     for split, tail, sched in (("1", "1", "0"), ("1", "1", "1"), ("2", "2", "0"), ("4", "8", "1"), ("1", "8", "0"),
                                ("8", "64", "1"), ("64", "64", "0")):
-        monkeypatch.setenv("TCR_SPLIT", split)
-        monkeypatch.setenv("TCR_TAIL_SPLIT", tail)
-        monkeypatch.setenv("TCR_SCHED", sched)
-        for fin in (T.Finalize.tree, T.Finalize.ordered):
-            o = T.reduce(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync_async, finalize=fin))
-            assert base.setdefault(fin, o.value) == o.value, (split, tail, sched, fin)
-        blocks = T.block_results(xd, cfg).cpu().numpy()
+        with _capi.profiling_knobs({"TCR_SPLIT": split, "TCR_TAIL_SPLIT": tail, "TCR_SCHED": sched}):
+            for fin in (T.Finalize.tree, T.Finalize.ordered):
+                o = T.reduce(xd, cfg16(R=R, B=B, engine=T.Engine.mma_sync_async, finalize=fin))
+                assert base.setdefault(fin, o.value) == o.value, (split, tail, sched, fin)
+            blocks = T.block_results(xd, cfg).cpu().numpy()
         if "blocks" in base:
             assert np.array_equal(blocks.view(np.uint32), base["blocks"].view(np.uint32))
         else:
             base["blocks"] = blocks
     # twice in a row with the group counters reused
-    monkeypatch.setenv("TCR_SPLIT", "4")
-    assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
-    assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
+    with _capi.profiling_knobs({"TCR_SPLIT": "4"}):
+        assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
+        assert T.reduce(xd, cfg).value == base[T.Finalize.tree]
+
+
+def test_env_knobs_never_change_results(oracle, monkeypatch):
+    """The library never reads TCR_* variables on its own (reduction.hpp:19-21: a pure function
+    of input and config): with every knob set in the environment -- including the group-size
+    overrides that would change the TREE order -- values and block results are unchanged."""
+    h = oracle.generate_f16("normal", 21, (1 << 22) + 999)
+    xd = to_dev_f16(h)
+    cfgs = [cfg16(R=1, B=1024), cfg16(R=3, B=96), T.ReductionConfig(m=4, R=1, B=128), T.ReductionConfig(m=8, R=2, B=64)]
+    base = [(T.reduce(xd, c).value, T.block_results(xd, c).cpu().numpy()) for c in cfgs]
+    for k, v in {"TCR_GROUP_TARGET": "4096", "TCR_GROUP_CAP": "100000", "TCR_DEBUG_MODE": "9", "TCR_SPLIT": "8",
+                 "TCR_TAIL_SPLIT": "64", "TCR_SCHED": "0", "TCR_CTAS_PER_SM": "1", "TCR_GM_NAT_GENERIC": "1",
+                 "TCR_GM_NAT_ALT": "2", "TCR_GM_TR8_SINGLE": "1"}.items():
+        monkeypatch.setenv(k, v)
+    for c, (v, b) in zip(cfgs, base):
+        assert T.reduce(xd, c).value == v
+        assert np.array_equal(T.block_results(xd, c).cpu().numpy().view(np.uint32), b.view(np.uint32))
 
 
 # --------------------------------------------------------------------------- reentrancy (reduction.hpp:19-21)
@@ -652,15 +668,16 @@ def test_concurrent_host_threads(oracle):
 
 
 def test_bench_two_ranks_one_gpu(tmp_path):
-    """bench.py's N > 1 path (torchrun, per-rank shards, all_reduce combine, max over ranks,
-    one JSON line from rank 0) on one GPU: both ranks on cuda:0 over gloo."""
+    """bench.py's N > 1 path (self-launched ranks -- no torchrun on the command line --, per-rank
+    shards, one all_reduce combine, max over ranks, the strong-scaling record, one JSON line from
+    rank 0) on one GPU: both ranks on cuda:0 over gloo."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, TCR_BENCH_ONE_DEVICE="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29533", "bench.py", "--gpus", "2", "--steps", "5",
-           "--warmup", "3", "--elems", str(1 << 26), "--no-cpu", "--no-comparators"]
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "5", "--warmup", "3", "--elems", str(1 << 26),
+           "--strong-elems", str((1 << 27) + 12345), "--no-cpu", "--no-comparators"]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -668,8 +685,12 @@ def test_bench_two_ranks_one_gpu(tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["n_total"] == 2 << 26 and d["value"] > 0
     # both shards of the global uniform stream, combined: within the single-GPU tolerance
-    assert d["rel_err_vs_exact"] < 1e-5
+    assert d["rel_err_vs_exact"] < 1e-5 and d["overflow"] is False
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 2 * 2 * (1 << 26)
+    st = d["strong_2e34"]
+    assert st["n_total"] == (1 << 27) + 12345 and st["ms_single_shot_median"] > 0
+    assert st["rel_err_vs_exact"] < 1e-5 and st["overflow"] is False
+    assert d["combine_latency"]["us_median"] > 0
 
 
 @pytest.mark.parametrize("m,R,B", [(2, 1, 128), (2, 3, 64), (4, 1, 128), (4, 5, 32), (8, 1, 128), (8, 3, 32),

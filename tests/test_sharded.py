@@ -77,11 +77,17 @@ def _worker(rank, world, port, n, how, out_q):
 
     out = S.reduce_sharded(h, n, cfg, how=how, partial_fn=partial_fn)
 
-    def overflow_fn(x, c):  # rank 1 reports an overflowed partial
-        return torch.tensor([1.0], dtype=torch.float32), torch.tensor([int(rank == 1)], dtype=torch.int32)
+    def overflow_fn(x, c):  # rank 1 overflowed: its kernel partial is non-finite with the flag set
+        v = float("inf") if rank == 1 else 1.0
+        return torch.tensor([v], dtype=torch.float32), torch.tensor([int(rank == 1)], dtype=torch.int32)
+
+    def mixed_fn(x, c):    # +inf on rank 0, -inf on rank 1: the combined value is NaN, still flagged
+        v = float("inf") if rank == 0 else float("-inf")
+        return torch.tensor([v], dtype=torch.float32), torch.tensor([1], dtype=torch.int32)
 
     out2 = S.reduce_sharded(h, n, cfg, how=how, partial_fn=overflow_fn)
-    out_q.put((rank, out.value, out.overflow, out.atomic_count, out.mma_count, out2.overflow))
+    out3 = S.reduce_sharded(h, n, cfg, how=how, partial_fn=mixed_fn)
+    out_q.put((rank, out.value, out.overflow, out.atomic_count, out.mma_count, out2.overflow and out3.overflow))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -103,7 +109,7 @@ def test_two_rank_gloo_combine(oracle, how):
     exact, _ = oracle.exact_sum_f16(oracle.generate_f16("uniform", 0, n))
     ref_counts = T.counters(n, T.ReductionConfig(m=16, R=1, B=1024))
     for rank, value, ovf, atomics, mmas, ovf2 in res:
-        assert not ovf and ovf2  # overflow on any rank is seen by all ranks
+        assert not ovf and ovf2  # overflow on any rank is seen by all ranks (one collective)
         assert atomics == ref_counts.atomic_count and mmas == ref_counts.mma_count
         if how == "tree":
             assert value == single  # bit-identical to the single-GPU tree finaliser

@@ -70,6 +70,8 @@ def main():
         for label, c, env, lib in specs:
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
+            lib.tcr_enable_profiling_knobs.restype = C.c_int
+            lib.tcr_enable_profiling_knobs()   # knobs are read only on this explicit call
             try:
                 for _ in range(3):
                     _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))

@@ -1,7 +1,7 @@
 """Generate tests/golden/*.json from the reference itself (oracle/_ref) and the pinned oracle.
 
 Run in the build container (needs /root/reference to have built oracle/_ref):
-    python tools/make_goldens.py [--large]
+    python tools/make_goldens.py [--large] [--huge]
 
 Small cases come straight from the UNMODIFIED reference compiled by oracle/Makefile
 (tcreduce::single_pass_reduce, generate, from_single).  Large cases (n = 2^26 .. 2^30) use the
@@ -82,36 +82,109 @@ def small() -> dict:
     return g
 
 
+# BASELINE configs[2] grid (every (R, B) of the paper's sweep) and the configs[3] precision-study
+# points; every (dist, seed, n) of the study carries the four study configs.
+SWEEP_RB = [(R, B) for B in (32, 128, 256, 512, 1024) for R in (1, 2, 3, 4, 5)]
+STUDY_RB = [(1, 1024), (4, 128), (1, 128), (5, 32)]
+
+
+def gen_f16(dist: str, seed: int, first: int, n: int, threads: int) -> np.ndarray:
+    """Elements [first, first+n) of generate(dist, seed) rounded to binary16, in parallel slices
+    (the jump-ahead generator is position-independent: harness.hpp:47-80)."""
+    from concurrent.futures import ThreadPoolExecutor
+    h = np.empty(n, np.uint16)
+    step = -(-n // threads)
+    step += (-step) % 2          # normal pairs never straddle a slice
+    def run(i):
+        a = i * step
+        b = min(n, a + step)
+        if a < b:
+            O._check(O.lib().orc_generate_range_f16(O.DISTS[dist], seed, 0, 9, 1.0, first + a, b - a, h[a:b]))
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, range(threads)))
+    return h
+
+
 def large(threads: int) -> dict:
     lg: dict = {"source": "oracle/liboracle.so (bit-identical restatement, re-pinned below)", "cases": []}
     # re-pin the restatement against the reference at 2^24 with the reference's parallel form
-    x = O.ref_generate("normal", 3, (1 << 24) + 12345)
-    a = O.single_pass(x, threads=threads, m=16, R=4, B=128)
-    b = O.ref_single_pass_parallel(x, threads, m=16, R=4, B=128)
-    assert a.as_dict() == b.as_dict(), (a.as_dict(), b.as_dict())
-    lg["repin"] = {"n": int(x.size), "dist": "normal", "seed": 3, "m": 16, "R": 4, "B": 128, "value": a.value}
+    for dist, seed, (m, R, B) in (("normal", 3, (16, 4, 128)), ("uniform", 0, (16, 1, 1024)),
+                                  ("uniform", 5, (16, 3, 256))):
+        x = O.ref_generate(dist, seed, (1 << 24) + 12345)
+        a, ab = O.single_pass(x, threads=threads, want_blocks=True, m=m, R=R, B=B)
+        b, bb = O.ref_single_pass_parallel(x, threads, want_blocks=True, m=m, R=R, B=B)
+        assert a.as_dict() == b.as_dict(), (a.as_dict(), b.as_dict())
+        assert np.array_equal(ab.view(np.uint32), bb.view(np.uint32))
+        lg.setdefault("repins", []).append({"n": int(x.size), "dist": dist, "seed": seed, "m": m, "R": R, "B": B,
+                                            "value": a.value})
+    lg["repin"] = lg["repins"][0]
     del x
     for dist, seed in (("uniform", 0), ("normal", 1), ("normal", 2), ("normal", 3)):
-        for lgn in (26, 28, 30):
-            if dist != "uniform" and seed != 1 and lgn != 26:
-                continue
+        for lgn in (26, 27, 28, 29, 30):
             n = 1 << lgn
             t = time.time()
             x = O.generate(dist, seed, n)
             o64 = O.oracle64(x)
-            h = np.empty(n, np.uint16)
-            O.lib().orc_generate_range_f16(O.DISTS[dist], seed, 0, 9, 1.0, 0, n, h)
             del x
+            h = gen_f16(dist, seed, 0, n, threads)
             ex, ab = O.exact_sum_f16(h)
             rec = {"dist": dist, "seed": seed, "n": n, "oracle64_f32_input": o64, "exact_f16_sum": ex,
                    "abs_f16_sum": ab, "single_pass": {}}
-            for (m, R, B) in ((16, 1, 1024), (16, 4, 128), (16, 1, 128), (16, 5, 32)):
-                o = O.single_pass(h, threads=threads, m=m, R=R, B=B)
-                rec["single_pass"][f"m{m}_R{R}_B{B}"] = outcome(o)
+            pts = list(STUDY_RB)
+            if dist == "uniform" and lgn == 28:
+                pts += [rb for rb in SWEEP_RB if rb not in pts]
+            for (R, B) in pts:
+                o, blocks = O.single_pass(h, threads=threads, want_blocks=True, m=16, R=R, B=B)
+                d = outcome(o)
+                d["blocks_sha256"] = sha(blocks)
+                rec["single_pass"][f"m16_R{R}_B{B}"] = d
             lg["cases"].append(rec)
-            print(dist, seed, n, f"{time.time() - t:.1f}s", flush=True)
+            print(dist, seed, n, len(pts), f"{time.time() - t:.1f}s", flush=True)
             del h
     return lg
+
+
+def huge(threads: int, lgn: int = 34, chunk_lg: int = 28) -> dict:
+    """BASELINE configs[4]: uniform s0, n = 2^34 (32 GiB of binary16), streamed through the
+    restatement in 2^28-element slices (whole blocks each: the block partition is global).
+    The value is the reference's serial ascending fp32 sum of the block results
+    (reduction.hpp:264-268), accumulated across slices in block order."""
+    from fractions import Fraction
+    n = 1 << lgn
+    out: dict = {"source": "oracle/liboracle.so streamed (blocks of every 2^%d slice, serial fp32 combine)" % chunk_lg,
+                 "dist": "uniform", "seed": 0, "n": n, "single_pass": {}}
+    cfgs = [(16, 1, 1024)]
+    accs = {c: np.float32(0.0) for c in cfgs}
+    hashes = {c: hashlib.sha256() for c in cfgs}
+    counts = {c: 0 for c in cfgs}
+    ovf = {c: False for c in cfgs}
+    exact = Fraction(0)
+    absum = Fraction(0)
+    t = time.time()
+    for s in range(n >> chunk_lg):
+        h = gen_f16("uniform", 0, s << chunk_lg, 1 << chunk_lg, threads)
+        e, a = O.exact_sum_f16(h)      # exact in binary64 at 2^28 elements (< 2^53 units of 2^-24)
+        exact += Fraction(e)
+        absum += Fraction(a)
+        for c in cfgs:
+            m, R, B = c
+            o, blocks = O.single_pass(h, threads=threads, want_blocks=True, m=m, R=R, B=B)
+            # np.add.accumulate is a strictly sequential fp32 running sum (no pairwise blocking)
+            seq = np.concatenate([np.array([accs[c]], np.float32), blocks])
+            accs[c] = np.add.accumulate(seq, dtype=np.float32)[-1]
+            hashes[c].update(blocks.tobytes())
+            counts[c] += blocks.size
+            ovf[c] = ovf[c] or bool(o.overflow)
+        if s % 8 == 0:
+            print(f"slice {s}/{n >> chunk_lg} {time.time() - t:.0f}s", flush=True)
+    out["exact_f16_sum"] = float(exact)
+    out["abs_f16_sum"] = float(absum)
+    for c in cfgs:
+        m, R, B = c
+        out["single_pass"][f"m{m}_R{R}_B{B}"] = {"value": float(accs[c]), "overflow": ovf[c], "blocks": counts[c],
+                                                 "blocks_sha256": hashes[c].hexdigest()}
+    out["seconds"] = time.time() - t
+    return out
 
 
 def main():
@@ -125,6 +198,10 @@ def main():
         lg = large(os.cpu_count() or 1)
         with open(os.path.join(OUT, "oracle_large.json"), "w") as f:
             json.dump(lg, f, indent=1)
+    if "--huge" in sys.argv:
+        hg = huge(os.cpu_count() or 1)
+        with open(os.path.join(OUT, "oracle_2e34.json"), "w") as f:
+            json.dump(hg, f, indent=1)
 
 
 if __name__ == "__main__":

@@ -13,6 +13,7 @@ xp = C.c_void_p(x.data_ptr())
 for mode, ctas in [("ldg", 8), ("ldg", 4), ("ldg", 3), ("async", 8), ("async", 6), ("async", 4), ("async", 3)]:
     os.environ["TCR_PROBE"] = mode
     os.environ["TCR_PROBE_CTAS"] = str(ctas)
+    lib.tcr_enable_profiling_knobs()
     ts = []
     for rep in range(5):
         for _ in range(2):

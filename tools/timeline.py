@@ -24,7 +24,7 @@ def main():
     import paper_2001_05585_b200 as T
     from paper_2001_05585_b200 import _capi
     lib = _capi.load()
-    lib.tcr_debug_timestamps.argtypes = [C.c_void_p, C.c_size_t]
+    lib.tcr_enable_profiling_knobs()   # reads TCR_DEBUG_MODE=20 (knobs are never read implicitly)
     dev = torch.device("cuda", 0)
     st = torch.cuda.current_stream(dev)
     x = T.generate("uniform", 0, a.n, device=dev)
