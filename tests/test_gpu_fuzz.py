@@ -67,6 +67,13 @@ def test_random_config_matches_reference(oracle, k):
         return
     assert not got.overflow, tag
     exact, absum = oracle.exact_sum_f16(h)
+    if variant == "single_pass" and fin == T.Finalize.ordered:
+        # ORDERED is the reference's own combine: wherever the block results are bit-identical
+        # the value must be too (reduction.hpp:257-268)
+        _, ref_blocks = oracle.single_pass(h, threads=4, want_blocks=True, m=m, R=R, B=B)
+        gb = T.block_results(xd, T.ReductionConfig(m=m, R=R, B=B, engine=engine)).cpu().numpy()
+        if np.array_equal(gb.view(np.uint32), ref_blocks.view(np.uint32)):
+            assert got.value == ref.value, (tag, got.value, ref.value)
     if variant in ("shuffle32", "half_tree"):
         assert got.value == ref.value, tag                     # bit-exact strided trees
     elif dist == "integers" and 9 * R * m <= 2048 and absum < 2 ** 24:

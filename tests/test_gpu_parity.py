@@ -310,9 +310,15 @@ def _large():
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("lgn", [26, 28, 30])
-@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1)])
+@pytest.mark.parametrize("lgn", [26, 27, 28, 29, 30])
+@pytest.mark.parametrize("dist,seed", [("uniform", 0), ("normal", 1), ("normal", 2), ("normal", 3)])
 def test_full_size_against_golden(dist, seed, lgn, engine):
+    """BASELINE configs[2]/[3] against the reference's single_pass_reduce values (the pinned
+    restatement, tests/golden/oracle_large.json): every (R, B) of the paper's sweep at 2^28 uniform,
+    the four precision-study configs at every (dist, seed, n).  TREE and ORDERED within the bars;
+    ORDERED bit for bit wherever the device block results are bit-identical to the reference's
+    (sha256 of the block array in the golden)."""
+    import hashlib
     recs = [r for r in _large()["cases"] if r["dist"] == dist and r["seed"] == seed and r["n"] == 1 << lgn]
     if not recs:
         pytest.skip("no golden")
@@ -320,20 +326,64 @@ def test_full_size_against_golden(dist, seed, lgn, engine):
     x = T.generate(dist, seed, rec["n"])
     s, a = T.exact_sum(x)
     assert s == rec["exact_f16_sum"] and a == rec["abs_f16_sum"]  # generator is bit-exact at full size
+    same_r1 = []
     for key, ref in rec["single_pass"].items():
         R, B = int(key.split("_")[1][1:]), int(key.split("_")[2][1:])
+        blocks = T.block_results(x, cfg16(R=R, B=B, engine=engine)).cpu().numpy()
+        same = hashlib.sha256(blocks.tobytes()).hexdigest() == ref["blocks_sha256"]
+        if R == 1:
+            same_r1.append(same)
         for fin in (T.Finalize.tree, T.Finalize.ordered):
             got = T.reduce(x, cfg16(R=R, B=B, finalize=fin, engine=engine))
             assert got.overflow == ref["overflow"]
             assert got.atomic_count == ref["atomic_count"] and got.mma_count == ref["mma_count"]
             err_exact = abs(got.value - s)
             err_ref = abs(got.value - ref["value"])
-            print(f"\n{engine.name} {dist} 2^{lgn} {key} {fin.name}: gpu {got.value!r} ref {ref['value']!r} exact {s!r} "
-                  f"rel_err_exact {err_exact / abs(s):.3e} rel_vs_ref {err_ref / abs(s):.3e}")
+            print(f"\n{engine.name} {dist} s{seed} 2^{lgn} {key} {fin.name}: gpu {got.value!r} ref {ref['value']!r} "
+                  f"exact {s!r} rel_err_exact {err_exact / abs(s):.3e} rel_vs_ref {err_ref / abs(s):.3e} "
+                  f"blocks_identical {same}")
             if dist == "uniform":
                 assert err_exact / abs(s) <= 1e-5 and err_ref / abs(s) <= 2e-5
             else:
                 assert err_exact / a <= 1e-6 and err_ref / a <= 1e-6
+            if fin == T.Finalize.ordered and same:
+                assert got.value == ref["value"]
+    if dist == "uniform":
+        # measured: with one MMA per chunk (R = 1) every block is identical on uniform data; longer
+        # chains sum more products per column before the binary16 rounding, and a handful of
+        # blocks per 2^26 can round the other way (ORDERED still matched the reference value)
+        assert all(same_r1)
+    del x
+    torch.cuda.empty_cache()
+
+
+def test_2e34_single_gpu_against_golden():
+    """BASELINE configs[4] on one GPU: n = 2^34 uniform s0 (32 GiB of binary16) against the
+    streamed restatement (tests/golden/oracle_2e34.json): block results bit-identical (sha256 of
+    all 2^21), ORDERED equal to the reference's serial combine bit for bit, TREE within the bar."""
+    import hashlib
+    p = os.path.join(GOLDEN, "oracle_2e34.json")
+    if not os.path.exists(p):
+        pytest.skip("oracle_2e34.json not generated")
+    g = json.load(open(p))
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 << 30:
+        pytest.skip("needs 40 GiB of free HBM")
+    n = g["n"]
+    x = T.generate("uniform", 0, n)
+    s, a = T.exact_sum(x)
+    assert abs(s - g["exact_f16_sum"]) <= 1e-12 * abs(s)
+    ref = g["single_pass"]["m16_R1_B1024"]
+    cfg = cfg16(R=1, B=1024)
+    blocks = T.block_results(x, cfg).cpu().numpy()
+    assert blocks.size == ref["blocks"]
+    assert hashlib.sha256(blocks.tobytes()).hexdigest() == ref["blocks_sha256"]
+    del blocks
+    o = T.reduce(x, cfg16(R=1, B=1024, finalize=T.Finalize.ordered))
+    assert o.value == ref["value"] and not o.overflow
+    t = T.reduce(x, cfg)
+    assert abs(t.value - s) / s <= 1e-5 and abs(t.value - ref["value"]) / s <= 2e-5 and not t.overflow
+    print(f"\n2^34: ordered {o.value!r} == reference {ref['value']!r}; tree {t.value!r}; exact {s!r}")
     del x
     torch.cuda.empty_cache()
 

@@ -1,5 +1,6 @@
 #!/usr/bin/env python3
-"""Kernel time vs n for the north-star single_pass (AUTO engine) and the read probe: fits
+"""Kernel time vs n for the north-star single_pass (AUTO engine), the read probe and the
+warp-shuffle comparator: fits
 t(n) = a + b n to expose the fixed per-launch cost (pipeline fill, tail, last-CTA finalise).
 Profiling tool.   python tools/size_scan.py"""
 import ctypes as C
@@ -46,11 +47,12 @@ def main():
         n = 1 << lg
         t_sp = timed(lambda: _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(cfg), rp, op, sp)))
         t_rd = timed(lambda: _capi.check(lib.tcr_read_probe_async(xp, 2 * n, sp)))
-        rec = {"n": n, "single_pass_us": t_sp, "read_probe_us": t_rd, "sp_TBs": 2 * n / t_sp / 1e6,
-               "probe_TBs": 2 * n / t_rd / 1e6}
+        t_sh = timed(lambda: _capi.check(lib.tcr_shuffle_f16_async(xp, n, rp, sp)))
+        rec = {"n": n, "single_pass_us": t_sp, "read_probe_us": t_rd, "warp_shuffle_us": t_sh,
+               "sp_TBs": 2 * n / t_sp / 1e6, "probe_TBs": 2 * n / t_rd / 1e6, "shuffle_TBs": 2 * n / t_sh / 1e6}
         out.append(rec)
         print(json.dumps(rec), flush=True)
-    for key in ("single_pass_us", "read_probe_us"):
+    for key in ("single_pass_us", "read_probe_us", "warp_shuffle_us"):
         a = out[-3]  # 2^29
         b = out[-1]  # 2^31
         slope = (b[key] - a[key]) / (b["n"] - a["n"])
