@@ -128,6 +128,37 @@ __device__ __forceinline__ float lane_segment_tree(LD ld, uint32_t base, uint32_
     }
 }
 
+// Adjacent tree over seg (power of two, 4..128) consecutive values at a 16-byte aligned address,
+// read with 16-byte L2 loads (__ldcg), all in flight.
+template <int SEG>
+__device__ __forceinline__ float vec_tree(const float* v) {
+    float x[SEG];
+#pragma unroll
+    for (int i = 0; i < SEG / 4; ++i) {
+        const float4 q = __ldcg(reinterpret_cast<const float4*>(v) + i);
+        x[4 * i] = q.x;
+        x[4 * i + 1] = q.y;
+        x[4 * i + 2] = q.z;
+        x[4 * i + 3] = q.w;
+    }
+#pragma unroll
+    for (int len = SEG; len > 1; len >>= 1)
+#pragma unroll
+        for (int i = 0; i < len / 2; ++i) x[i] = x[2 * i] + x[2 * i + 1];
+    return x[0];
+}
+
+__device__ __forceinline__ float vec_segment_tree(const float* v, uint32_t seg) {
+    switch (seg) {
+    case 4: return vec_tree<4>(v);
+    case 8: return vec_tree<8>(v);
+    case 16: return vec_tree<16>(v);
+    case 32: return vec_tree<32>(v);
+    case 64: return vec_tree<32>(v) + vec_tree<32>(v + 32);
+    default: return (vec_tree<32>(v) + vec_tree<32>(v + 32)) + (vec_tree<32>(v + 64) + vec_tree<32>(v + 96));
+    }
+}
+
 // Canonical adjacent tree over vals[0,count) (zero padded to a power of two) by the first
 // `nthr` threads (power of two, multiple of 32); every thread of the CTA must call it.
 // REG: per-thread segments of <= 128 values as compile-time register trees with all loads in
@@ -141,7 +172,11 @@ __device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, flo
     if (seg == 0) seg = 1;
     float acc = 0.0f;
     const uint64_t lo = uint64_t(threadIdx.x) * seg;
-    if (REG && seg <= 128) {
+    if (REG && seg >= 4 && seg <= 128 && lo + seg <= count) {
+        // whole segment inside: 16-byte L2 loads, all in flight, compact code (this path runs
+        // once per launch, cold in the instruction cache: fewer instructions = fewer misses)
+        if (threadIdx.x < nthr) acc = vec_segment_tree(vals + lo, uint32_t(seg));
+    } else if (REG && seg <= 128) {
         if (threadIdx.x < nthr && lo < P)
             acc = lane_segment_tree([&](uint32_t i) { return i < count ? __ldcg(vals + i) : 0.0f; }, uint32_t(lo),
                                     uint32_t(seg));
@@ -182,46 +217,68 @@ __device__ __forceinline__ float cta_tree(const float* vals, uint64_t count, flo
 }
 
 
+// reduction.hpp:257-268: serial binary32 accumulation of the block results, ascending or in the
+// seeded Fisher-Yates permutation (SplitMix64, rng.hpp).  One thread.
+__device__ __forceinline__ float ordered_sum(const SpParams& p) {
+    float acc = 0.0f;
+    if (p.atomic_order == 1) {
+        uint32_t* order = p.order_scratch;
+        for (uint64_t i = 0; i < p.n_blocks; ++i) order[i] = uint32_t(i);
+        uint64_t st = p.atomic_seed;
+        for (uint64_t i = p.n_blocks; i > 1; --i) {
+            st += 0x9E3779B97F4A7C15ull;
+            uint64_t z = st;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            const uint64_t r = z % i;
+            const uint32_t tt = order[i - 1];
+            order[i - 1] = order[r];
+            order[r] = tt;
+        }
+        for (uint64_t i = 0; i < p.n_blocks; ++i) acc += __ldcg(p.block_partials + order[i]);
+    } else {
+        for (uint64_t b = 0; b < p.n_blocks; ++b) acc += __ldcg(p.block_partials + b);
+    }
+    return acc;
+}
+
 // Last-CTA-done finaliser shared by the persistent engines: every thread of the CTA calls it
 // after publishing its partials (__threadfence + __syncthreads done by the caller).
+// The caller's __syncthreads() after its last global writes makes them visible to thread 0, whose
+// fence before the ticket then releases them grid-wide (cumulativity; the cooperative-groups grid
+// barrier pattern): no fence by every thread.  stamps (profiling, may be null): %globaltimer
+// after the ticket and after the tree, last CTA only.
+__device__ __forceinline__ unsigned long long fin_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <bool REG = false>
-__device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_scratch, int* s_last, unsigned nthr) {
+__device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_scratch, int* s_last, unsigned nthr,
+                                                  unsigned long long* stamps = nullptr) {
     if (!(p.finalize == kFinTree || p.finalize == kFinOrdered)) return;
     if (threadIdx.x == 0) {
-        const unsigned tk = atomicAdd(p.ticket, 1u);
+        // one acquire-release RMW: releases the CTA's writes (made visible to thread 0 by the
+        // caller's barrier) and, for the last CTA, acquires everybody else's
+        unsigned tk;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(tk) : "l"(p.ticket) : "memory");
         *s_last = (tk == gridDim.x - 1);
     }
     __syncthreads();
     if (!*s_last) return;
-    __threadfence();
+    if (stamps && threadIdx.x == 0) stamps[0] = fin_gtimer();
     if (p.finalize == kFinTree) {
         const float r = cta_tree<REG>(p.group_partials, p.n_groups, s_scratch, nthr);
         if (threadIdx.x == 0) *p.result = r;
     } else if (threadIdx.x == 0) {
-        // reduction.hpp:257-268: serial binary32 accumulation, ascending or seeded permutation
-        float acc = 0.0f;
-        if (p.atomic_order == 1) {
-            uint32_t* order = p.order_scratch;
-            for (uint64_t i = 0; i < p.n_blocks; ++i) order[i] = uint32_t(i);
-            uint64_t st = p.atomic_seed;
-            for (uint64_t i = p.n_blocks; i > 1; --i) {
-                st += 0x9E3779B97F4A7C15ull;
-                uint64_t z = st;
-                z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-                z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-                z ^= z >> 31;
-                const uint64_t r = z % i;
-                const uint32_t tt = order[i - 1];
-                order[i - 1] = order[r];
-                order[r] = tt;
-            }
-            for (uint64_t i = 0; i < p.n_blocks; ++i) acc += __ldcg(p.block_partials + order[i]);
-        } else {
-            for (uint64_t b = 0; b < p.n_blocks; ++b) acc += __ldcg(p.block_partials + b);
-        }
-        *p.result = acc;
+        *p.result = ordered_sum(p);
     }
-    if (threadIdx.x == 0) *p.ticket = 0u;
+    if (threadIdx.x == 0) {
+        *p.ticket = 0u;
+        if (stamps) stamps[1] = fin_gtimer();
+    }
 }
 
 // Block stage (reference pairwise tree over W chunk results, reduction.hpp:253, :90-101) for the

