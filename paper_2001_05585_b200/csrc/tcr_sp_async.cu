@@ -355,12 +355,17 @@ __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) 
             else if (warp == 0) tile_tree_group(p, gi, s_block);
         } else {
             for (uint32_t b = threadIdx.x; b < Gu; b += kAsThreads) p.block_scratch[b0 + b] = s_block[b];
-            __threadfence();
             __syncthreads();
-            if (threadIdx.x == 0) s_glast = atomicAdd(p.group_count + gi, 1u) == S - 1;
+            if (threadIdx.x == 0) {
+                // one acquire-release RMW releases the CTA's block results (visible to thread 0
+                // through the barrier) and, for the piece that completes the group, acquires
+                // the other pieces' (the cooperative-groups grid-barrier pattern)
+                unsigned t;
+                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(p.group_count + gi) : "memory");
+                s_glast = t == S - 1;
+            }
             __syncthreads();
             if (s_glast) {
-                __threadfence();
                 if (G >= 256) {
                     tile_tree_group_cta<true>(p, gi, p.block_scratch + gi * G);
                 } else if (warp == 0) {
