@@ -146,6 +146,10 @@ int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const in
  * reduction.hpp:248-255) into d_blocks[tcr_block_count(n, cfg)]. */
 int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* cfg, float* d_blocks,
                                  void* cuda_stream);
+/* The same from the reference's own fp32 input (from_single, half.hpp:32-59, applied by the
+ * fp32 paths exactly as reduce(std::span<const float>) does). */
+int tcr_block_results_f32_device(const float* d_x, size_t n, const tcr_config* cfg, float* d_blocks,
+                                 void* cuda_stream);
 size_t tcr_block_count(size_t n, const tcr_config* cfg);
 
 /* Shard alignment for multi-GPU single_pass: elements per kernel group (G logical blocks).

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tcr_single_pass_f16_async": (C.c_int, [_P, _SZ, _CFG, _P, _P, _P]),
     "tcr_single_pass_f32_async": (C.c_int, [_P, _SZ, _CFG, _P, _P, _P]),
     "tcr_block_results_f16_device": (C.c_int, [_P, _SZ, _CFG, _P, _P]),
+    "tcr_block_results_f32_device": (C.c_int, [_P, _SZ, _CFG, _P, _P]),
     "tcr_reduce_f16_sharded": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.POINTER(C.c_int32), C.c_int32,
                                          _CFG, _OUT]),
     "tcr_block_count": (_SZ, [_SZ, _CFG]),

@@ -365,10 +365,11 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
         ++g_launches;
     }
     if (c->m != 16) {
-        // m != 16: the selector-matrix engine (binary16 input; fp32 callers convert first)
-        if (f32) return fail(TCR_NOT_SUPPORTED, "internal: m != 16 needs binary16 input");
+        // m != 16: the selector-matrix engine; fp32 input straight in where the natural layout
+        // takes it (from_single fused into the load), else callers convert first
+        if (f32 && !tcr::genm_f32_supported(g)) return fail(TCR_NOT_SUPPORTED, "internal: this m needs binary16 input");
         g_engine = TCR_ENGINE_MMA_SYNC_ASYNC;
-        TCR_CUDA(tcr::launch_genm(p, g, s, g_repair));
+        TCR_CUDA(tcr::launch_genm(p, g, s, g_repair, f32));
         ++g_launches;
         return TCR_OK;
     }
@@ -474,7 +475,7 @@ int sp_async(const void* d_x, size_t n, const tcr_config* c, bool f32, float* d_
     rc = aligned_input(&d_x, n, f32, w, s);
     if (rc) return rc;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
-    if (f32 && c->m != 16) {
+    if (f32 && c->m != 16 && !tcr::genm_f32_supported(g)) {
         // from_single (fragment.hpp:68) applied up front, then the binary16 engine
         rc = ensure(&w->conv, &w->conv_cap, n, s);
         if (rc) return rc;
@@ -590,7 +591,7 @@ int run_recurrence(const void* d_x, bool f32, uint64_t n0, const tcr_config* c, 
         rc = ensure(&w->lvl16[nb], &w->lvl16_cap[nb], count, s);
         if (rc) return rc;
         const tcr::SpGeometry g = tcr::make_geometry(n, cb.m, cb.R, cb.B);
-        if (cur_f32 && cb.m != 16) {
+        if (cur_f32 && cb.m != 16 && !tcr::genm_f32_supported(g)) {
             rc = ensure(&w->conv, &w->conv_cap, n, s);
             if (rc) return rc;
             TCR_CUDA(tcr::launch_convert_f32_f16(static_cast<const float*>(cur), w->conv, n, s));
@@ -990,12 +991,16 @@ int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const in
     return TCR_OK;
 }
 
-int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_blocks,
-                                 void* stream) {
-    NvtxRange nvtx_("tcr_block_results_f16_device");
+}  // extern "C"
+
+namespace {
+
+// Per-block results of single_pass into d_blocks[n_blocks] (parity hook): binary16 or fp32 input
+// through the same kernels the reductions use (fp32: from_single fused into the load where the
+// engine has it, else one conversion pass first).
+int block_results(const void* d_x, size_t n, const tcr_config* c, bool f32, float* d_blocks, cudaStream_t s) {
     RepairScope rs(c && c->m != 16);   // parity hook: per-block values exact for non-finite data too
     g_launches = 0;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0) return fail(TCR_INVALID_ARGUMENT, "input must be non-empty");
     int rc = validate_cfg(c);
     if (rc) return rc;
@@ -1006,12 +1011,36 @@ int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config
     if (rc) return rc;
     if (!d_x || !d_blocks) return fail(TCR_INVALID_ARGUMENT, "null device pointer");
     const void* xa = d_x;   // 16-byte lines: an unaligned slice is copied first
-    rc = aligned_input(&xa, n, false, w, s);
+    rc = aligned_input(&xa, n, f32, w, s);
     if (rc) return rc;
     tcr_config cc = *c;
     cc.finalize = TCR_FINALIZE_TREE;
+    cc.atomic_order = TCR_ASCENDING;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
-    return enqueue_sp(xa, 0, n, &cc, false, w->result(), w->overflow(), d_blocks, w, s, 0, g.n_groups, true);
+    if (f32 && c->m != 16 && !tcr::genm_f32_supported(g)) {
+        rc = ensure(&w->conv, &w->conv_cap, n, s);
+        if (rc) return rc;
+        TCR_CUDA(tcr::launch_convert_f32_f16(static_cast<const float*>(xa), w->conv, n, s));
+        ++g_launches;
+        xa = w->conv;
+        f32 = false;
+    }
+    return enqueue_sp(xa, 0, n, &cc, f32, w->result(), w->overflow(), d_blocks, w, s, 0, g.n_groups, true);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tcr_block_results_f16_device(const uint16_t* d_x, size_t n, const tcr_config* c, float* d_blocks,
+                                 void* stream) {
+    NvtxRange nvtx_("tcr_block_results_f16_device");
+    return block_results(d_x, n, c, false, d_blocks, static_cast<cudaStream_t>(stream));
+}
+
+int tcr_block_results_f32_device(const float* d_x, size_t n, const tcr_config* c, float* d_blocks, void* stream) {
+    NvtxRange nvtx_("tcr_block_results_f32_device");
+    return block_results(d_x, n, c, true, d_blocks, static_cast<cudaStream_t>(stream));
 }
 
 namespace {
@@ -1108,6 +1137,7 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
     tcr_config cc = *c;
     TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
     const char* xb = static_cast<const char*>(x);
+    const bool f32_direct = f32 && cc.m != 16 && tcr::genm_f32_supported(g);
     for (uint64_t k = 0; k < n_chunks; ++k) {
         const int slot = int(k & 1);
         const uint64_t e0 = k * chunk_elems;
@@ -1121,7 +1151,7 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
         TCR_CUDA(cudaStreamWaitEvent(s, w->copied[slot], 0));
         const bool last = (k + 1 == n_chunks);
         // single chunk: finalise in the same launch; otherwise one finaliser at the end
-        if (!f32 || cc.m == 16) {
+        if (!f32 || cc.m == 16 || f32_direct) {
             rc = enqueue_sp(dst, e0, n, &cc, f32, w->result(), w->overflow(), nullptr, w, s, g0, g1,
                             last && n_chunks == 1);
         } else {

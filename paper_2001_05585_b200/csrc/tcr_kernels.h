@@ -102,7 +102,9 @@ bool async_plan(const SpGeometry& g, SpParams* p, int grid);
 bool genm_supported(const SpGeometry& g);
 // repair: instantiations that recompute NaN chunk results exactly (non-finite inputs; see
 // group_epilogue in tcr_sp_genm.cu).
-cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair);
+// f32: fp32 input with from_single fused into the load (genm_f32_supported shapes only).
+bool genm_f32_supported(const SpGeometry& g);
+cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair, bool f32 = false);
 
 // Variants (tcr_variants.cu): bit-exact strided pairwise trees (shuffle32 / half_tree), binary64
 // sum (oracle64), and the recurrence level rounding.

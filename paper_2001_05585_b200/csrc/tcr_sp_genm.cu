@@ -63,7 +63,8 @@ __device__ __forceinline__ float h_round(float v) { return h_to_f32(f32_to_h(v))
 // core.  Slow path for a chunk whose tensor-core result is NaN: the selector engines multiply
 // every binary16 by 0/1 entries, and a non-finite input times 0 is NaN where the reference's
 // all-ones products keep +-inf -- recomputing keeps the reference's non-finite value.
-__device__ __forceinline__ float chunk_exact(const uint16_t* x, uint64_t n, uint64_t e0, uint32_t m, uint32_t R) {
+template <bool F32 = false>
+__device__ __forceinline__ float chunk_exact(const void* xv, uint64_t n, uint64_t e0, uint32_t m, uint32_t R) {
     float fin = 0.0f;
     for (uint32_t j = 0; j < m; ++j) {
         float c = 0.0f;
@@ -71,7 +72,9 @@ __device__ __forceinline__ float chunk_exact(const uint16_t* x, uint64_t n, uint
             float col = 0.0f;
             for (uint32_t k = 0; k < m; ++k) {
                 const uint64_t e = e0 + uint64_t(r) * m * m + uint64_t(k) * m + j;
-                col = col + (e < n ? h_to_f32(x[e]) : 0.0f);   // zero padding (reduction.hpp:244-245)
+                float v = 0.0f;   // zero padding (reduction.hpp:244-245)
+                if (e < n) v = F32 ? h_round(static_cast<const float*>(xv)[e]) : h_to_f32(static_cast<const uint16_t*>(xv)[e]);
+                col = col + v;
             }
             c = col + c;
         }
@@ -125,7 +128,12 @@ __device__ __forceinline__ void group_tree_cta(const SpParams& p, uint64_t gi, c
         static_assert(kGmWarps == 8, "three pairing levels");
         const float a = (s_w[0] + s_w[1]) + (s_w[2] + s_w[3]);
         const float b = (s_w[4] + s_w[5]) + (s_w[6] + s_w[7]);
-        p.group_partials[gi] = a + b;
+        const float v = a + b;
+        p.group_partials[gi] = v;
+        // overflow note (reduction.hpp:78-81): some binary16 of the group -- input or C_R
+        // partial -- was non-finite iff a chunk result was, iff the group partial is (finite
+        // chunk results of one group cannot overflow binary32)
+        if (!isfinite(v)) atomicOr(p.overflow, 1u);
     }
 }
 
@@ -135,7 +143,7 @@ __device__ __forceinline__ void group_tree_cta(const SpParams& p, uint64_t gi, c
 // non-finite chunk result already set the thread's overflow note (`ovf`, reduction.hpp:78-81),
 // so only then does the CTA scan its chunk table and recompute the NaN chunks exactly
 // (chunk_exact) before the block stage.  The default instantiations carry none of this code.
-template <bool REPAIR>
+template <bool REPAIR, bool F32 = false>
 __device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, float* s_chunk, float* s_block,
                                                uint32_t m, bool ovf) {
     if constexpr (REPAIR) {
@@ -144,7 +152,7 @@ __device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, f
             const uint64_t ce = uint64_t(p.R) * m * m;
             for (uint32_t i = threadIdx.x; i < Cg; i += kGmThreads)
                 if (isnan(s_chunk[i]))
-                    s_chunk[i] = chunk_exact(static_cast<const uint16_t*>(p.x), p.n, (gi * Cg + i) * ce, m, p.R);
+                    s_chunk[i] = chunk_exact<F32>(p.x, p.n, (gi * Cg + i) * ce, m, p.R);
             __syncthreads();
         }
     } else {
@@ -170,6 +178,17 @@ struct NatShape {
 
 __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+// predicated shared store (one STS with a predicate, no branch)
+__device__ __forceinline__ void sts_pred(uint32_t addr, float v, bool on) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}" ::"r"(addr), "f"(v),
+                 "r"(uint32_t(on))
+                 : "memory");
 }
 
 // Generic natural layout for the periods gm_nat_fast_kernel does not take (9-15 rows, or more
@@ -327,12 +346,21 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
 // invariant, chunk results leave through precomputed shared addresses, and the overflow note is
 // a NaN-propagating accumulator (x * 0 is NaN exactly when x is not finite) instead of per-value
 // tests.  Same arithmetic, operand order and chunk -> shared-table mapping as gm_nat_kernel.
-template <int M, int RBC, int UPS, int ND, bool REPAIR, bool XG = true>
+//
+// F32: the reference's own input format (reduce(std::span<const float>)) streamed as is, from_single
+// (half.hpp:32-59) fused into the load: the stage holds the fp32 bytes unswizzled, lane (g, c)
+// reads 16 bytes = elements 4c .. 4c+3 of rows g and g + 8 (LDS.128, conflict-free) and packs
+// them with cvt.rn.f16x2.f32 into its A registers -- a permutation of the MMA's k index
+// (k = 2c, 2c+1, 2c+8, 2c+9 <-> element 4c .. 4c+3) that the selector B follows, so D is
+// unchanged.  4 bytes per element from HBM, no conversion pass.
+template <int M, int RBC, int UPS, int ND, bool REPAIR, bool XG = true, bool F32 = false>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams p, const NatShape S) {
+    constexpr uint32_t ESZ = F32 ? 4u : 2u;                            // bytes per input element
+    constexpr uint32_t EP = 16u / ESZ;                                 // elements per 16-byte piece
     constexpr uint32_t UNIT_EL = 256u * RBC;
-    constexpr uint32_t UNIT_B = 2u * UNIT_EL;
+    constexpr uint32_t UNIT_B = ESZ * UNIT_EL;
     constexpr uint32_t STAGE_EL = UNIT_EL * UPS;
-    constexpr uint32_t STAGE_B = 2u * STAGE_EL;
+    constexpr uint32_t STAGE_B = ESZ * STAGE_EL;
     constexpr uint32_t NQ = STAGE_B / 512u;                           // 16-byte pieces per lane per stage
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ float s_scratch[32];
@@ -347,18 +375,22 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
     const uint32_t CP = S.CP, cpu = S.chunks_per_unit;
     const uint32_t Cg = p.G * p.W;
     const uint32_t sunits = ((Cg + cpu - 1) / cpu + UPS - 1) / UPS;  // stages per group
-    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const char* xb = static_cast<const char*>(p.x);
     auto bsel = [&](uint32_t rho, uint32_t k) -> bool {
         const uint32_t e = 16u * rho + k;
         return (e / ce) * M + (e % M) == g;
     };
+    // the element of the row that MMA index k holds (F32: the permutation above)
+    auto kel = [&](uint32_t k) -> uint32_t { return F32 ? 4u * ((k & 7u) >> 1) + (k & 1u) + 2u * (k >> 3) : k; };
     const bool straddle = CP > 1 && RBC > 1;
-    uint32_t b0 = sel2(bsel(0, 2 * c), bsel(0, 2 * c + 1)), b1 = sel2(bsel(0, 2 * c + 8), bsel(0, 2 * c + 9));
+    uint32_t b0 = sel2(bsel(0, kel(2 * c)), bsel(0, kel(2 * c + 1))),
+             b1 = sel2(bsel(0, kel(2 * c + 8)), bsel(0, kel(2 * c + 9)));
     const uint32_t bfin = sel2((2 * c) / M == g, (2 * c + 1) / M == g);
     const uint32_t rho8 = (lane & 7u) + 8u * ((lane >> 3) & 1u), half = lane >> 4;
     // chunk slots this lane owns after the finishing MMA: columns 2c, 2c+1 of rows g, g+8
     const bool own0 = 2 * c < CP, own1 = 2 * c + 1 < CP;
-    const uint32_t sa = smem_u32(s_chunk) + 4u * (g * CP + 2 * c), srow8 = 4u * 8u * CP;
+    float* const s_own = s_chunk + g * CP + 2 * c;
+    const uint32_t s_own_a = smem_u32(s_chunk) + 4u * g;   // M = 4 (CP = 1)
     float nanacc = 0.0f;
     bool ovf = false;
     const uint32_t F = sunits > warp ? (sunits - warp + kGmWarps - 1) / kGmWarps : 0;   // stages per group
@@ -373,7 +405,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
         const uint64_t gel0 = igi * uint64_t(Cg) * ce, gel1 = gel0 + uint64_t(Cg) * ce;
         ilim = gel1 < p.n ? gel1 : p.n;
         ifull = gel1 <= p.n && Cg % (cpu * UPS) == 0;
-        e_issue = gel0 + uint64_t(warp) * STAGE_EL + 8u * lane;          // this lane's piece 0
+        e_issue = gel0 + uint64_t(warp) * STAGE_EL + EP * lane;          // this lane's piece 0
         is = 0;
     };
     iset();
@@ -385,18 +417,19 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
         if (F != 0 && igi < p.group_end && is < F) {
             const uint32_t dst = ring + islot * STAGE_B;
             auto off = [&](uint32_t q) {
+                if constexpr (F32) return q * 512u + 16u * lane;       // linear: LDS.128 rows are conflict-free
                 const uint32_t piece = lane + 32u * (q % RBC);
                 return (q / RBC) * UNIT_B + ((piece ^ ((piece / (2u * RBC)) & 7u)) * 16u);
             };
             if (ifull) {
 #pragma unroll
-                for (uint32_t q = 0; q < NQ; ++q) cp16(dst + off(q), x + e_issue + 256u * q, 16u);
+                for (uint32_t q = 0; q < NQ; ++q) cp16(dst + off(q), xb + (e_issue + 32u * EP * q) * ESZ, 16u);
             } else {
 #pragma unroll
                 for (uint32_t q = 0; q < NQ; ++q) {
-                    const uint64_t e = e_issue + 256u * q;
-                    const uint32_t bytes = e + 8 <= ilim ? 16u : (e < ilim ? uint32_t(ilim - e) * 2u : 0u);
-                    cp16(dst + off(q), x + (e < ilim ? e : 0), bytes);
+                    const uint64_t e = e_issue + 32u * EP * q;
+                    const uint32_t bytes = e + EP <= ilim ? 16u : (e < ilim ? uint32_t(ilim - e) * ESZ : 0u);
+                    cp16(dst + off(q), xb + (e < ilim ? e : 0) * ESZ, bytes);
                 }
             }
             e_issue += uint64_t(kGmWarps) * STAGE_EL;
@@ -428,47 +461,81 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
             __syncwarp();
             const uint32_t base = ring + cslot * STAGE_B;
             cslot = cslot + 1 == uint32_t(ND) ? 0 : cslot + 1;
+            // The UPS units of the stage are independent: their ldmatrix -> HMMA -> binary16 ->
+            // finishing HMMA chains are interleaved (all loads, then all chains' MMAs, ...) so a
+            // warp has UPS chains in flight instead of one (the kernel is latency-bound per warp).
+            float acc[UPS][4];
+#pragma unroll
+            for (uint32_t j = 0; j < UPS; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+            for (uint32_t i = 0; i < RBC; ++i) {
+                if (straddle) {
+                    b0 = sel2(bsel(i, kel(2 * c)), bsel(i, kel(2 * c + 1)));
+                    b1 = sel2(bsel(i, kel(2 * c + 8)), bsel(i, kel(2 * c + 9)));
+                }
+                uint32_t d[UPS][4];
+                if constexpr (F32) {
+                    // rows g and g + 8 of the unit's row block i, elements 4c .. 4c+3 (16 bytes)
+#pragma unroll
+                    for (uint32_t j = 0; j < UPS; ++j) {
+                        const uint32_t r0 = base + j * UNIT_B + ((g * RBC + i) * 16u + 4u * c) * 4u;
+                        const float4 lo = lds_f4(r0), hi = lds_f4(r0 + 8u * RBC * 64u);
+                        d[j][0] = pack_h2(lo.x, lo.y);   // k = 2c, 2c+1     (rows 0-7)
+                        d[j][1] = pack_h2(hi.x, hi.y);   //                  (rows 8-15)
+                        d[j][2] = pack_h2(lo.z, lo.w);   // k = 2c+8, 2c+9   (rows 0-7)
+                        d[j][3] = pack_h2(hi.z, hi.w);   //                  (rows 8-15)
+                    }
+                } else {
+                    const uint32_t unit16 = 2u * (rho8 * RBC + i) + half;
+#pragma unroll
+                    for (uint32_t j = 0; j < UPS; ++j)
+                        ldsm4(base + j * UNIT_B + ((unit16 ^ (rho8 & 7u)) * 16u), d[j][0], d[j][1], d[j][2], d[j][3]);
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < UPS; ++j) mma_16816(acc[j], d[j][0], d[j][1], d[j][2], d[j][3], b0, b1);
+            }
+            float d2s[UPS][4];
 #pragma unroll
             for (uint32_t j = 0; j < UPS; ++j) {
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                d2s[j][0] = d2s[j][1] = d2s[j][2] = d2s[j][3] = 0.f;
+                mma_16816(d2s[j], pack_h2(acc[j][0], acc[j][1]), pack_h2(acc[j][2], acc[j][3]), 0u, 0u, bfin, 0u);
+            }
 #pragma unroll
-                for (uint32_t i = 0; i < RBC; ++i) {
-                    if (straddle) {
-                        b0 = sel2(bsel(i, 2 * c), bsel(i, 2 * c + 1));
-                        b1 = sel2(bsel(i, 2 * c + 8), bsel(i, 2 * c + 9));
-                    }
-                    const uint32_t unit16 = 2u * (rho8 * RBC + i) + half;
-                    uint32_t d0, d1, d2, d3;
-                    ldsm4(base + j * UNIT_B + ((unit16 ^ (rho8 & 7u)) * 16u), d0, d1, d2, d3);
-                    mma_16816(acc, d0, d1, d2, d3, b0, b1);
+            for (uint32_t j = 0; j < UPS; ++j) {
+                const float* d2 = d2s[j];
+                if constexpr (REPAIR) {
+                    // non-owner columns are 0 unless an input is non-finite, which its owner sees
+                    // too.  (The default instantiations read the overflow note off the group
+                    // partial instead: group_tree_cta.)
+                    nanacc = fmaf(d2[0], 0.0f, nanacc);
+                    nanacc = fmaf(d2[1], 0.0f, nanacc);
+                    nanacc = fmaf(d2[2], 0.0f, nanacc);
+                    nanacc = fmaf(d2[3], 0.0f, nanacc);
                 }
-                float d2[4] = {0.f, 0.f, 0.f, 0.f};
-                mma_16816(d2, pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), 0u, 0u, bfin, 0u);
-                // non-owner columns are 0 unless an input is non-finite, which its owner sees too
-                nanacc = fmaf(d2[0], 0.0f, nanacc);
-                nanacc = fmaf(d2[1], 0.0f, nanacc);
-                nanacc = fmaf(d2[2], 0.0f, nanacc);
-                nanacc = fmaf(d2[3], 0.0f, nanacc);
                 const uint32_t cu = cu0 + j * cpu;
-                const uint32_t ca = cu + g * CP + 2 * c;
-                if (own0) {
-                    if (full || ca < Cg) sts_f32(sa + 4u * cu, d2[0]);
-                    if (full || ca + 8 * CP < Cg) sts_f32(sa + 4u * cu + srow8, d2[2]);
-                }
-                if (own1) {
-                    if (full || ca + 1 < Cg) sts_f32(sa + 4u * cu + 4u, d2[1]);
-                    if (full || ca + 1 + 8 * CP < Cg) sts_f32(sa + 4u * cu + 4u + srow8, d2[3]);
+                if constexpr (M == 4) {
+                    // one chunk per period (CP = 1): lanes c = 0 own chunks g and g + 8 of the unit;
+                    // predicated stores at compile-time offsets, no branches
+                    const uint32_t ca = cu + g;
+                    sts_pred(s_own_a + 4u * cu, d2[0], c == 0 && (full || ca < Cg));
+                    sts_pred(s_own_a + 4u * cu + 32u, d2[2], c == 0 && (full || ca + 8 < Cg));
+                } else {
+                    const uint32_t ca = cu + g * CP + 2 * c;
+                    float* sp = s_own + cu;
+                    if (own0 && (full || ca < Cg)) sp[0] = d2[0];
+                    if (own0 && (full || ca + 8 * CP < Cg)) sp[8 * CP] = d2[2];
+                    if (own1 && (full || ca + 1 < Cg)) sp[1] = d2[1];
+                    if (own1 && (full || ca + 1 + 8 * CP < Cg)) sp[8 * CP + 1] = d2[3];
                 }
             }
             __syncwarp();
             cu0 += kGmWarps * UPS * cpu;
         }
         ovf = nanacc != nanacc;
-        group_epilogue<REPAIR>(p, gi, s_chunk, s_block, M, ovf);
+        group_epilogue<REPAIR, F32>(p, gi, s_chunk, s_block, M, ovf);
     }
     cp_wait<0>();
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
-    __threadfence();
     __syncthreads();
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
 }
@@ -1205,7 +1272,9 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     switch (S.RB) {                                                           \
     case 1:                                                                   \
         if (a == 1) TCR_NATF(MV, 1, 4, 4) else if (a == 2) TCR_NATF(MV, 1, 2, 6) \
-        else if (a == 3) TCR_NATFX(MV, 1, 4, 3) else TCR_NATF(MV, 1, 4, 3)   \
+        else if (a == 3) TCR_NATFX(MV, 1, 4, 3) else if (a == 4) TCR_NATF(MV, 1, 4, 5) \
+        else if (a == 5) TCR_NATF(MV, 1, 2, 8) else if (a == 6) TCR_NATF(MV, 1, 2, 5) \
+        else TCR_NATF(MV, 1, 4, 3)   \
         break;                                                                \
     case 2: if (a == 3) TCR_NATF(MV, 2, 2, 4) else TCR_NATFX(MV, 2, 2, 4) break; \
     case 4: if (a == 3) TCR_NATF(MV, 4, 1, 4) else TCR_NATFX(MV, 4, 1, 4) break; \
@@ -1273,7 +1342,50 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
     return launch_gm(fn, kGmWarps * (kGmTrDepth * 512u + stage * 4u) + tables, groups, p, S, s);
 }
 
-cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair) {
+// fp32 input straight into the natural-layout kernel (m in {2, 4}, periods of <= 8 rows that
+// the fast kernel takes): from_single fused into the load.
+bool genm_f32_supported(const SpGeometry& g) {
+    if (!(g.m == 2 || g.m == 4) || knobs().gm_nat_generic) return false;
+    NatShape S;
+    if (!nat_shape(g.m, g.R, g.G * g.W, &S)) return false;
+    return S.PR == S.RB && S.PR <= 8;
+}
+
+template <bool REPAIR>
+cudaError_t launch_genm_f32_t(const SpParams& p, const SpGeometry& g, cudaStream_t s) {
+    const uint32_t Cg = g.G * g.W;
+    const uint64_t groups = p.group_end - p.group_begin;
+    const uint32_t tables = (Cg + g.G + 3u) / 4u * 16u;
+    NatShape S;
+    if (!genm_f32_supported(g) || !nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
+    void (*ff)(SpParams, NatShape) = nullptr;
+    uint32_t stage = 0, nd = 0;
+    // 2-4 KiB stages of fp32 (twice the bytes of the binary16 unit)
+#define TCR_NATF32(MV, RBV, UPSV, NDV, XGV) \
+    { ff = gm_nat_fast_kernel<MV, RBV, UPSV, NDV, REPAIR, XGV, true>; stage = 1024u * RBV * UPSV; nd = NDV; }
+#define TCR_NATF32_M(MV)                          \
+    switch (S.RB) {                               \
+    case 1: TCR_NATF32(MV, 1, 2, 3, true) break;  \
+    case 2: TCR_NATF32(MV, 2, 1, 4, false) break; \
+    case 3: TCR_NATF32(MV, 3, 1, 3, false) break; \
+    case 4: TCR_NATF32(MV, 4, 1, 3, false) break; \
+    case 5: TCR_NATF32(MV, 5, 1, 2, false) break; \
+    case 6: TCR_NATF32(MV, 6, 1, 2, false) break; \
+    case 7: TCR_NATF32(MV, 7, 1, 2, false) break; \
+    default: TCR_NATF32(MV, 8, 1, 2, false) break; \
+    }
+    if (g.m == 2) {
+        TCR_NATF32_M(2)
+    } else {
+        TCR_NATF32_M(4)
+    }
+#undef TCR_NATF32_M
+#undef TCR_NATF32
+    return launch_gm(ff, kGmWarps * nd * stage + tables, groups, p, S, s);
+}
+
+cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair, bool f32) {
+    if (f32) return repair ? launch_genm_f32_t<true>(p, g, s) : launch_genm_f32_t<false>(p, g, s);
     return repair ? launch_genm_t<true>(p, g, s) : launch_genm_t<false>(p, g, s);
 }
 

@@ -153,18 +153,20 @@ def block_count(n: int, cfg: ReductionConfig) -> int:
 
 def block_results(x, cfg: ReductionConfig):
     """Per-block fp32 results of single_pass (reduction.hpp:248-255) as a CUDA float32 tensor.
-    x: binary16 CUDA tensor (the parity hook reads binary16 only)."""
+    x: binary16 CUDA tensor, or float32 (the reference's format: from_single applied by the fp32
+    paths, fused into the load where the engine has it)."""
     import torch
-    if x.dtype != torch.float16:
-        raise TypeError(f"block_results takes a float16 tensor, got {x.dtype}")
+    if x.dtype not in (torch.float16, torch.float32):
+        raise TypeError(f"block_results takes a float16 or float32 tensor, got {x.dtype}")
     x = x.contiguous()
     c = cfg.to_c()
     nb = block_count(x.numel(), cfg)
     out = torch.empty(nb, dtype=torch.float32, device=x.device)
+    lib = _capi.load()
+    fn = lib.tcr_block_results_f16_device if x.dtype == torch.float16 else lib.tcr_block_results_f32_device
     with torch.cuda.device(x.device):
-        _capi.check(_capi.load().tcr_block_results_f16_device(C.c_void_p(x.data_ptr()), x.numel(), C.byref(c),
-                                                              C.c_void_p(out.data_ptr()),
-                                                              C.c_void_p(_stream_ptr(x))))
+        _capi.check(fn(C.c_void_p(x.data_ptr()), x.numel(), C.byref(c), C.c_void_p(out.data_ptr()),
+                       C.c_void_p(_stream_ptr(x))))
     return out
 
 

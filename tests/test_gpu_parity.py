@@ -891,3 +891,76 @@ def test_cluster_engine_many_chunks(oracle, m, R, B, dist, seed):
     exact, absum = oracle.exact_sum_f16(h)
     assert abs(o.value - ref.value) <= max(2e-5 * abs(exact), 1e-6 * absum)
     assert o.atomic_count == ref.atomic_count and o.mma_count == ref.mma_count
+
+
+# --------------------------------------------------------------------------- fp32 input (the reference's format)
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("B", [32, 96, 128, 1024])
+def test_fp32_fused_natural_layout_equals_binary16(oracle, m, R, B):
+    """m in {2, 4}: fp32 input goes straight into the natural-layout kernel with from_single
+    (half.hpp:32-59) fused into the load (cvt.rn.f16x2.f32, permuted MMA k index).  Block results,
+    both finalize orders and the host drop-in path equal the binary16 path on the rounded values
+    bit for bit."""
+    x = oracle.generate("normal", 7 + R, (1 << 20) + 4099)
+    x[5] = 70000.0          # from_single overflow -> +inf: the flag and value class must match too
+    x = x if (R + B) % 2 else np.where(np.arange(x.size) == 5, np.float32(1.5), x)
+    h = np.array(x.astype(np.float16).view(np.uint16))
+    xd32, xd16 = torch.from_numpy(x).to(DEV), to_dev_f16(h)
+    cfg = T.ReductionConfig(m=m, R=R, B=B)
+    b32 = T.block_results(xd32, cfg).cpu().numpy()
+    b16 = T.block_results(xd16, cfg).cpu().numpy()
+    assert np.array_equal(b32.view(np.uint32), b16.view(np.uint32))
+    for fin in (T.Finalize.tree, T.Finalize.ordered):
+        c2 = T.ReductionConfig(m=m, R=R, B=B, finalize=fin)
+        a, b = T.reduce(xd32, c2), T.reduce(xd16, c2)
+        assert (a.value == b.value or (math.isnan(a.value) and math.isnan(b.value))) and a.overflow == b.overflow
+    hst = T.reduce(x, cfg)   # host fp32 drop-in (pipelined)
+    dev = T.reduce(xd16, cfg)
+    assert (hst.value == dev.value or (math.isnan(hst.value) and math.isnan(dev.value))) and hst.overflow == dev.overflow
+
+
+# test_half.cpp:22-53 KATs and the binary16 rounding boundaries (half.hpp:32-59)
+_FROM_SINGLE_KATS = [1.0, 0.1, -0.1, 65504.0, 65519.0, 65519.99, 65520.0, -65520.0, 1e9, -0.0, 0.0,
+                     2.0 ** -24, 2.0 ** -25, 3 * 2.0 ** -25, 2.0 ** -26, 1.5 * 2.0 ** -24, 2.0 ** -14,
+                     2.0 ** -14 - 2.0 ** -25, 1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11, 1.0 + 2.0 ** -11 + 2.0 ** -20,
+                     2049.0, 2051.0, 4097.0, 1e-8, -1e-8, 3.14159265, -2.71828]
+
+
+@pytest.mark.parametrize("m,R", [(16, 1), (4, 1), (2, 1), (8, 1)])
+def test_from_single_edges_through_fp32_paths(oracle, m, R):
+    """Every value through the fp32 device paths (m = 16: register engine with cvt fused; m = 2, 4:
+    fused natural layout; m = 8: conversion pass), one value per chunk (B = 32: a block is one
+    chunk, the rest of the chunk zero): each block result must be to_single(from_single(x))
+    exactly -- the KATs of test_half.cpp:22-53, the RNE midpoints, subnormals, +-65504 / 65519 /
+    65520, -0 -- and 10^5 random fp32 of every exponent; non-finite values (inf, NaN) must give
+    non-finite blocks and the overflow note, as the reference."""
+    rng = np.random.default_rng(42)
+    bits = rng.integers(0, 2 ** 32, 100_000, dtype=np.uint64).astype(np.uint32)
+    rnd = bits.view(np.float32)
+    rnd = rnd[np.isfinite(rnd)]
+    vals = np.concatenate([np.array(_FROM_SINGLE_KATS, np.float32), rnd.astype(np.float32)])
+    ce = R * m * m
+    x = np.zeros(vals.size * ce, np.float32)
+    x[::ce] = vals
+    got = T.block_results(torch.from_numpy(x).to(DEV), T.ReductionConfig(m=m, R=R, B=32)).cpu().numpy()
+    _, want = oracle.single_pass(x, threads=os.cpu_count() or 8, want_blocks=True, m=m, R=R, B=32)
+    # the reference's block of a lone value is to_single(from_single(x)) (its column sums start
+    # from +0, so -0 comes out +0)
+    rt = np.array([oracle.to_single(oracle.from_single(float(v))) for v in vals], np.float32)
+    nz = rt != 0   # values rounding to -0 come out +0 (the column sums start from +0)
+    assert np.array_equal(want[nz].view(np.uint32), rt[nz].view(np.uint32))
+    fin = np.isfinite(want)
+    assert np.array_equal(got[fin].view(np.uint32), want[fin].view(np.uint32))
+    assert np.all(~np.isfinite(got[~fin]))   # |x| >= 65520 -> inf (half.hpp:52-57)
+    # single-element reductions: value and overflow flag as the reference, NaN / inf included
+    for v in list(_FROM_SINGLE_KATS) + [float("inf"), float("-inf"), float("nan")]:
+        xs = torch.tensor([v], dtype=torch.float32, device=DEV)
+        o = T.reduce(xs, T.ReductionConfig(m=m, R=R, B=32))
+        ref = oracle.single_pass(np.array([v], np.float32), threads=1, m=m, R=R, B=32)
+        assert o.overflow == ref.overflow, v
+        if math.isnan(ref.value):
+            assert math.isnan(o.value), v
+        else:
+            assert o.value == ref.value, v
