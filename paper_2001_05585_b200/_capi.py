@@ -72,6 +72,7 @@ SIGNATURES = {
     "tcr_enable_profiling_knobs": (C.c_int, []),
     "tcr_reset_profiling_knobs": (None, []),
     "tcr_debug_timestamps": (C.c_int, [_P, _SZ]),
+    "tcr_ordered_stats": (C.c_int, [_P]),
 }
 
 _lib = None

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtcreduce_b200.so")
 
-SOURCES = ["tcr_single_pass.cu", "tcr_tc05.cu", "tcr_sp_bulk.cu", "tcr_sp_async.cu", "tcr_sp_genm.cu", "tcr_variants.cu", "tcr_aux.cu", "tcr_capi.cpp"]
+SOURCES = ["tcr_single_pass.cu", "tcr_tc05.cu", "tcr_sp_bulk.cu", "tcr_sp_async.cu", "tcr_sp_genm.cu", "tcr_variants.cu", "tcr_ordered.cu", "tcr_aux.cu", "tcr_capi.cpp"]
 HEADERS = ["tcr_device.cuh", "tcr_kernels.h", "tcr_pipeline.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -80,8 +80,12 @@ struct Workspace {
     size_t gp_cap = 0;
     float* block_partials = nullptr;
     size_t bp_cap = 0;
-    uint32_t* order = nullptr;
+    uint32_t* order = nullptr;   // seeded-permutation block order (host-computed, cached)
     size_t order_cap = 0;
+    uint64_t order_nb = 0, order_seed = 0;
+    bool order_ok = false;
+    uint32_t* ord_ws = nullptr;   // ascending ORDERED: group records, runs (tcr_ordered.cu)
+    size_t ord_cap = 0;
     // small fixed area: result(float), overflow(u32), ticket(u32), shuffle ticket, exact out[3]
     unsigned char* fixed = nullptr;
     void* exact_ws = nullptr;
@@ -128,7 +132,7 @@ struct Workspace {
         };
         f(group_partials); f(block_partials); f(order); f(fixed); f(exact_ws); f(shuffle_partials); f(cub_temp);
         f(conv); f(tree_cols); f(dpart); f(lvl_f32); f(lvl16[0]); f(lvl16[1]); f(block_scratch); f(group_count);
-        f(work_counter); f(stage); f(unaligned); f(ring[0]); f(ring[1]); f(ring16[0]); f(ring16[1]);
+        f(work_counter); f(ord_ws); f(stage); f(unaligned); f(ring[0]); f(ring[1]); f(ring16[0]); f(ring16[1]);
         if (host_pinned) cudaFreeHost(host_pinned);
         host_pinned = nullptr;
         for (cudaEvent_t* e : {&copied[0], &copied[1], &consumed[0], &consumed[1], &fork, &join})
@@ -319,10 +323,11 @@ tcr_config normalized(const tcr_config* c) {
     return n;
 }
 
-// Enqueue single_pass over groups [g0, g1) of a (possibly chunked) input.
-int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c_in, bool f32, float* d_result,
-               uint32_t* d_overflow, float* d_blocks, Workspace* w, cudaStream_t s, uint64_t g0, uint64_t g1,
-               bool finalize_here) {
+// Enqueue single_pass over groups [g0, g1) of a (possibly chunked) input: the streaming kernel
+// (block results, group partials, TREE / ATOMIC finalise in its last CTA).
+int enqueue_sp_main(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c_in, bool f32, float* d_result,
+                    uint32_t* d_overflow, float* d_blocks, Workspace* w, cudaStream_t s, uint64_t g0, uint64_t g1,
+                    bool finalize_here) {
     const tcr_config cn = normalized(c_in);
     const tcr_config* c = &cn;
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
@@ -424,10 +429,73 @@ int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c
     return TCR_OK;
 }
 
+// The reference's block order for a seeded permutation (reduction.hpp:257-268: Fisher-Yates driven
+// by SplitMix64(atomic_seed), rng.hpp), computed once on the host per (blocks, seed) and kept in
+// the workspace.
+int ensure_order(Workspace* w, uint64_t nb, uint64_t seed, cudaStream_t s) {
+    if (w->order_nb == nb && w->order_seed == seed && w->order_ok) return TCR_OK;
+    std::vector<uint32_t> ord(nb);
+    for (uint64_t i = 0; i < nb; ++i) ord[i] = uint32_t(i);
+    uint64_t st = seed;
+    for (uint64_t i = nb; i > 1; --i) {
+        st += 0x9E3779B97F4A7C15ull;
+        uint64_t z = st;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        std::swap(ord[i - 1], ord[z % i]);
+    }
+    w->order_ok = false;
+    int rc = ensure(&w->order, &w->order_cap, nb, s);
+    if (rc) return rc;
+    TCR_CUDA(cudaMemcpyAsync(w->order, ord.data(), nb * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    TCR_CUDA(cudaStreamSynchronize(s));   // the host vector goes out of scope
+    w->order_nb = nb;
+    w->order_seed = seed;
+    w->order_ok = true;
+    return TCR_OK;
+}
+
+// ORDERED finalise: the serial chain over the published block results (tcr_ordered.cu).
+int enqueue_ordered(uint64_t n, const tcr_config* c, const float* blocks, float* d_result, Workspace* w, cudaStream_t s) {
+    const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
+    const uint32_t* order = nullptr;
+    if (c->atomic_order == TCR_SEEDED_PERMUTATION) {
+        int rc = ensure_order(w, g.n_blocks, c->atomic_seed, s);
+        if (rc) return rc;
+        order = w->order;
+    } else if (tcr::knobs().debug_mode != 40) {   // 40: profiling only, the serial chain
+        // ascending: the parallel exact evaluation over the group partials' binades
+        const size_t bytes = tcr::ordered_ws_bytes(g.n_groups, tcr::ordered_grid(g.n_groups));
+        int rc = ensure_zero(&w->ord_ws, &w->ord_cap, (bytes + 3) / 4, s);   // look-back flags start at 0
+        if (rc) return rc;
+        TCR_CUDA(tcr::launch_ordered_ascending(blocks, w->group_partials, g.n_blocks, g.n_groups, g.G, w->ord_ws,
+                                               w->ticket(), d_result, s));
+        ++g_launches;
+        return TCR_OK;
+    }
+    TCR_CUDA(tcr::launch_ordered(blocks, order, g.n_blocks, d_result, s));
+    ++g_launches;
+    return TCR_OK;
+}
+
+int enqueue_sp(const void* x, uint64_t x_offset, uint64_t n, const tcr_config* c_in, bool f32, float* d_result,
+               uint32_t* d_overflow, float* d_blocks, Workspace* w, cudaStream_t s, uint64_t g0, uint64_t g1,
+               bool finalize_here) {
+    const tcr_config cn = normalized(c_in);
+    if (cn.finalize != TCR_FINALIZE_ORDERED || !finalize_here)
+        return enqueue_sp_main(x, x_offset, n, &cn, f32, d_result, d_overflow, d_blocks, w, s, g0, g1, finalize_here);
+    // ORDERED: the streaming kernel publishes the block results, then the ordered chain
+    int rc = enqueue_sp_main(x, x_offset, n, &cn, f32, d_result, d_overflow, d_blocks, w, s, g0, g1, false);
+    if (rc) return rc;
+    return enqueue_ordered(n, &cn, d_blocks ? d_blocks : w->block_partials, d_result, w, s);
+}
+
 int enqueue_finalize(uint64_t n, const tcr_config* c_in, float* d_result, Workspace* w, cudaStream_t s) {
     const tcr_config cn = normalized(c_in);
     const tcr_config* c = &cn;
     if (c->finalize == TCR_FINALIZE_ATOMIC) return TCR_OK;
+    if (c->finalize == TCR_FINALIZE_ORDERED) return enqueue_ordered(n, c, w->block_partials, d_result, w, s);
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
     tcr::SpParams p{};
     p.n = n;
@@ -1246,6 +1314,8 @@ int tcr_cub_sum_f16_async(const uint16_t* d_x, size_t n, int half_acc, void* d_r
 }
 
 int tcr_enable_profiling_knobs(void) { return tcr::load_knobs_from_env(); }
+
+int tcr_ordered_stats(unsigned long long* host4) { return tcr::ordered_stats(host4); }
 
 void tcr_reset_profiling_knobs(void) { tcr::reset_knobs(); }
 

@@ -964,3 +964,69 @@ def test_from_single_edges_through_fp32_paths(oracle, m, R):
             assert math.isnan(o.value), v
         else:
             assert o.value == ref.value, v
+
+
+# --------------------------------------------------------------------------- ORDERED: the serial combine, in parallel
+
+def _designed_blocks(kind, nblocks, rng):
+    """binary16 values that become the block results one to one (m = 16, R = 1, B = 32: a block
+    is one 256-element chunk; one nonzero element per chunk makes the block that value exactly)."""
+    if kind == "random_all_exponents":
+        bits = rng.integers(0, 0x7C00, nblocks).astype(np.uint16) | (rng.integers(0, 2, nblocks).astype(np.uint16) << 15)
+        return bits.view(np.float16).astype(np.float32)
+    if kind == "odd_integers_ties":          # running sum passes 2^24: exact ties all the way
+        return (2 * rng.integers(0, 1024, nblocks) + 1).astype(np.float32)
+    if kind == "zero_crossing_walk":        # small signed steps: sign and binade change constantly
+        return rng.choice(np.array([-3, -2, -1, -0.5, 0.5, 1, 2, 3], np.float32), nblocks)
+    if kind == "powers_of_two":             # running sum lands on binade boundaries exactly
+        return np.ldexp(np.float32(1.0), rng.integers(-14, 15, nblocks)).astype(np.float32)
+    if kind == "large_then_cancel":         # big values cancelling to a tiny remainder, then growth
+        v = rng.integers(1, 60000, nblocks).astype(np.float32)
+        v[1::2] = -v[0::2][: v[1::2].size]
+        return v
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["random_all_exponents", "odd_integers_ties", "zero_crossing_walk",
+                                  "powers_of_two", "large_then_cancel"])
+@pytest.mark.parametrize("nblocks", [1, 7, 5000, 1 << 16])
+def test_ordered_parallel_equals_serial_chain(oracle, kind, nblocks):
+    """The ascending ORDERED combine runs in parallel (tcr_ordered.cu: binade-local integer
+    records with tie-parity maps, composed into runs, walked with the actual running sum); it must
+    equal the reference's serial fp32 loop (reduction.hpp:264-268) bit for bit on sequences built
+    to hit every hard case: exact ties (odd integers past 2^24), sign and binade changes every few
+    steps, sums landing exactly on powers of two, cancellation to tiny remainders."""
+    rng = np.random.default_rng(nblocks + len(kind))
+    vals = _designed_blocks(kind, nblocks, rng)
+    x = np.zeros(nblocks * 256, np.float32)
+    x[::256] = vals
+    h = x.astype(np.float16).view(np.uint16)
+    xd = to_dev_f16(h)
+    cfg = T.ReductionConfig(m=16, R=1, B=32, finalize=T.Finalize.ordered)
+    ref = oracle.single_pass(h, threads=os.cpu_count() or 8, m=16, R=1, B=32)
+    got = T.reduce(xd, cfg)
+    assert got.overflow == ref.overflow
+    assert np.float32(got.value).view(np.uint32) == np.float32(ref.value).view(np.uint32), (got.value, ref.value)
+    # the same through the serial chain (profiling mode 40) and with groups of 32 blocks (B = 1024)
+    from paper_2001_05585_b200 import _capi
+    with _capi.profiling_knobs({"TCR_DEBUG_MODE": "40"}):
+        ser = T.reduce(xd, cfg)
+    assert np.float32(ser.value).view(np.uint32) == np.float32(ref.value).view(np.uint32)
+
+
+@pytest.mark.parametrize("dist,seed,lgn", [("integers", 0, 26), ("normal", 1, 24), ("normal", 2, 26), ("uniform", 0, 26)])
+@pytest.mark.parametrize("m,R,B", [(16, 1, 1024), (16, 4, 128), (4, 1, 128), (8, 2, 64), (2, 3, 32)])
+def test_ordered_parallel_real_inputs(oracle, dist, seed, lgn, m, R, B):
+    """ORDERED on generated inputs: the parallel evaluation == the serial chain over the SAME device
+    block results, bit for bit (and == the reference value wherever the block results are)."""
+    h = oracle.generate_f16(dist, seed, (1 << lgn) + 333)
+    xd = to_dev_f16(h)
+    cfg = T.ReductionConfig(m=m, R=R, B=B, finalize=T.Finalize.ordered)
+    par = T.reduce(xd, cfg)
+    from paper_2001_05585_b200 import _capi
+    with _capi.profiling_knobs({"TCR_DEBUG_MODE": "40"}):
+        ser = T.reduce(xd, cfg)
+    assert np.float32(par.value).view(np.uint32) == np.float32(ser.value).view(np.uint32), (par.value, ser.value)
+    if dist == "integers":
+        ref = oracle.single_pass(h, threads=os.cpu_count() or 8, m=m, R=R, B=B)
+        assert par.value == ref.value
