@@ -122,6 +122,11 @@ def ref():
         L.ref_warp_offset.restype = C.c_size_t
         L.ref_single_pass_parallel.argtypes = [_F32P, C.c_size_t, C.POINTER(Config), C.c_int,
                                                C.POINTER(Outcome), C.c_void_p]
+        L.ref_csv_header.restype = C.c_char_p
+        L.ref_csv_row.argtypes = [C.POINTER(Config), C.c_uint64, C.c_uint64, C.c_char_p, C.c_double, C.c_int,
+                                  C.c_double, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_char_p, C.c_size_t]
+        L.ref_run_point_csv.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_size_t,
+                                        C.POINTER(Config), C.c_char_p, C.c_size_t]
         _ref = L
     return _ref
 
@@ -225,6 +230,30 @@ def ref_reduce(x: np.ndarray, **cfg) -> Outcome:
     x = np.ascontiguousarray(x, np.float32)
     _check(ref().ref_reduce(x, x.size, C.byref(c), C.byref(out)))
     return out
+
+
+def ref_csv_header() -> str:
+    """csv.hpp:14-15 kCsvHeader, from the compiled reference."""
+    return ref().ref_csv_header().decode()
+
+
+def ref_csv_row(n, seed, dist, value, error_pct, overflow, sim_steps, mma_count, atomic_count, **cfg) -> str:
+    """csv.hpp:19-48 csv_row of a SweepRecord with these fields (error_pct None = nullopt)."""
+    c = make_config(**cfg)
+    buf = C.create_string_buffer(1024)
+    _check(ref().ref_csv_row(C.byref(c), n, seed, dist.encode(), value, 0 if error_pct is None else 1,
+                             0.0 if error_pct is None else error_pct, int(bool(overflow)), sim_steps, mma_count,
+                             atomic_count, buf, len(buf)))
+    return buf.value.decode()
+
+
+def ref_run_point_csv(dist="uniform", seed=0, n=1, lo=0, hi=9, c=1.0, **cfg) -> str:
+    """harness.hpp:103-117 run_point on the CPU reference, as its csv.hpp row."""
+    kind = DISTS[dist] if isinstance(dist, str) else dist
+    cf = make_config(**cfg)
+    buf = C.create_string_buffer(1024)
+    _check(ref().ref_run_point_csv(kind, seed, lo, hi, c, n, C.byref(cf), buf, len(buf)))
+    return buf.value.decode()
 
 
 def ref_single_pass_parallel(x: np.ndarray, threads: int, want_blocks: bool = False, **cfg):

@@ -15,6 +15,7 @@
 #include <thread>
 #include <vector>
 
+#include "tcreduce/csv.hpp"
 #include "tcreduce/harness.hpp"
 #include "tcreduce/reduction.hpp"
 
@@ -166,6 +167,54 @@ int ref_single_pass_parallel(const float* x, size_t n, const ref_config* c, int 
         out->atomic_count = blocks;
         out->shuffle_count = blocks * (P - 1);
     });
+}
+
+// csv.hpp:14-15 as shipped.
+const char* ref_csv_header() { return kCsvHeader; }
+
+static int put(const std::string& s, char* buf, size_t cap) {
+    if (s.size() + 1 > cap) return -3;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+// csv.hpp:19-48 as shipped, on a SweepRecord built from explicit fields (has_err = 0: nullopt).
+int ref_csv_row(const ref_config* c, uint64_t n, uint64_t seed, const char* dist, double value, int has_err,
+                double err, int overflow, uint64_t sim_steps, uint64_t mma_count, uint64_t atomic_count, char* buf,
+                size_t cap) {
+    int rc = 0;
+    const int g = guard([&] {
+        SweepRecord rec;
+        rec.config = to_cfg(c);
+        rec.n = n;
+        rec.seed = seed;
+        rec.dist = dist;
+        rec.value = value;
+        if (has_err) rec.error_pct = err;
+        rec.overflow = overflow != 0;
+        rec.sim_steps = sim_steps;
+        rec.mma_count = mma_count;
+        rec.atomic_count = atomic_count;
+        rc = put(csv_row(rec), buf, cap);
+    });
+    return g ? g : rc;
+}
+
+// harness.hpp:103-117 (run_point: generate, reduce, oracle64 error) as shipped, returned as its
+// csv.hpp row.
+int ref_run_point_csv(int kind, uint64_t seed, int64_t lo, int64_t hi, double cc, size_t n, const ref_config* c,
+                      char* buf, size_t cap) {
+    int rc = 0;
+    const int g = guard([&] {
+        Distribution d;
+        d.kind = static_cast<DistKind>(kind);
+        d.seed = seed;
+        d.lo = lo;
+        d.hi = hi;
+        d.c = cc;
+        rc = put(csv_row(run_point(d, n, to_cfg(c))), buf, cap);
+    });
+    return g ? g : rc;
 }
 
 }  // extern "C"

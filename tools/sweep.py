@@ -9,8 +9,10 @@ back-to-back calls, inputs > L2),
 Gelem/s, GB/s and fraction of the measured HBM copy bandwidth; precision points add the
 relative error against the exact sum of the binary16 inputs (device fixed-point sum) and
 against the reference single_pass value (tests/golden/oracle_large.json, produced by the
-pinned oracle from the reference algorithm).  Also writes the reference's 14-column CSV
-schema (csv.hpp:14-15) with a wall-clock column appended.
+pinned oracle from the reference algorithm).  --reference-csv runs the reference's own sweeps
+(sweep_br, sweep_split, error_curve; harness.hpp:136-206) through the mirrored harness
+(paper_2001_05585_b200/harness.py) and writes them in the csv.hpp:14-48 schema with two
+wall-clock columns appended.
 """
 from __future__ import annotations
 
@@ -30,11 +32,13 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--precision", action="store_true")
     ap.add_argument("--variants", action="store_true")
+    ap.add_argument("--reference-csv", action="store_true",
+                    help="the reference's sweep_br / sweep_split / error_curve in its csv.hpp schema")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     args = ap.parse_args()
-    if not (args.sweep or args.precision or args.variants):
-        args.sweep = args.precision = args.variants = True
+    if not (args.sweep or args.precision or args.variants or args.reference_csv):
+        args.sweep = args.precision = args.variants = args.reference_csv = True
 
     import torch
 
@@ -67,7 +71,6 @@ def main():
         return statistics.median(ts), min(ts)
 
     out = {"peak_hbm_gbs": peak, "device": torch.cuda.get_device_name(0)}
-    csv_rows = []
 
     if args.sweep:
         n = 1 << 28
@@ -87,7 +90,6 @@ def main():
                                 "gelem_s": n / med / 1e6, "gb_s": 2 * n / med / 1e6,
                                 "frac_hbm": 2 * n / med / 1e6 / peak, "value": val,
                                 "launches": lib.tcr_last_launch_count()})
-                    csv_rows.append(("uniform", 0, n, "single_pass", 16, R, B, val, med, engine.name))
                     print(json.dumps(pts[-1]), flush=True)
         # fragment sides m != 16 (selector-matrix engine), the reference default m = 4 first
         mpts = []
@@ -189,16 +191,34 @@ def main():
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(out, f, indent=1)
-    if csv_rows:
-        # csv.hpp:14-15 schema + wall-clock columns
-        with open(os.path.splitext(args.out)[0] + ".csv", "w") as f:
-            f.write("dist,seed,n,variant,m,R,B,f,value,error_pct,overflow,sim_steps,mma_count,atomic_count,"
-                    "ms,engine\n")
-            for (dist, seed, n, var, m, R, B, val, ms, eng) in csv_rows:
-                c = T.counters(n, T.ReductionConfig(m=m, R=R, B=B))
-                f.write(f"{dist},{seed},{n},{var},{m},{R},{B},0.5,{val:.9g},,0,{c.sim_steps},{c.mma_count},"
-                        f"{c.atomic_count},{ms:.6f},{eng}\n")
-
+    if args.reference_csv:
+        # the reference's own sweeps (harness.hpp:136-206) through the mirrored harness: fp32 inputs,
+        # reduce() + oracle64 on the B200, rows in the csv.hpp:14-48 schema (+ ms, Gelem/s of the
+        # synchronous reduce call)
+        from paper_2001_05585_b200 import harness as H
+        du = H.Distribution(T.DistKind.uniform, 0)
+        dists = [du] + [H.Distribution(T.DistKind.normal, s) for s in (1, 2, 3)]
+        sizes = [1 << k for k in range(26, 31)]
+        sets = {
+            "sweep_br_m16": lambda: H.sweep_br(du, 1 << 28, T.Variant.single_pass, H.default_block_grid(),
+                                               H.default_chain_grid(), m=16),
+            "sweep_br_m4": lambda: H.sweep_br(du, 1 << 28, T.Variant.single_pass, H.default_block_grid(),
+                                              H.default_chain_grid()),
+            "sweep_split": lambda: H.sweep_split(du, 1 << 28, H.default_fraction_grid()),
+            "error_curve": lambda: [r for d in dists for v in (T.Variant.single_pass, T.Variant.recurrence,
+                                                                T.Variant.split, T.Variant.shuffle32,
+                                                                T.Variant.half_tree)
+                                    for r in H.error_curve(d, v, sizes)],
+        }
+        base = os.path.splitext(args.out)[0]
+        for name, fn in sets.items():
+            recs = fn()
+            with open(f"{base}_{name}.csv", "w") as f:
+                H.write_csv(f, recs, wall_clock=True)
+            best = H.best_by_steps_per_element(recs)
+            print(f"{name}: {len(recs)} rows -> {base}_{name}.csv; best by sim_steps/element: {H.csv_row(best)}",
+                  flush=True)
+            torch.cuda.empty_cache()
 
 if __name__ == "__main__":
     main()
