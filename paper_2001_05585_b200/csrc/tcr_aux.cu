@@ -13,6 +13,7 @@
 
 #include "tcr_device.cuh"
 #include "tcr_kernels.h"
+#include "tcr_pipeline.cuh"
 
 namespace tcr {
 
@@ -314,7 +315,55 @@ __global__ void __launch_bounds__(256) read_probe_async_kernel(const uint4* x, u
     if (acc == 0x9E3779B9u) sink[0] = acc;
 }
 
+// Streaming-read probe through 1-D TMA (cp.async.bulk): each CTA streams one contiguous range
+// in `slot`-byte copies through an NSLOT ring, one producer thread, one consumer warp touching
+// one word per slot (profiling: the bulk-copy path's ceiling with large copies).
+template <int NSLOT>
+__global__ void __launch_bounds__(64) read_probe_tma_kernel(const char* x, uint64_t bytes, uint32_t slot, uint32_t* sink) {
+    extern __shared__ __align__(128) unsigned char pring[];
+    __shared__ uint64_t full[NSLOT], empty[NSLOT];
+    const uint64_t per = (bytes / gridDim.x) & ~uint64_t(15);
+    const uint64_t b0 = per * blockIdx.x, b1 = blockIdx.x + 1 == gridDim.x ? (bytes & ~uint64_t(15)) : b0 + per;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSLOT; ++i) {
+            pipe::mbar_init(&full[i], 1);
+            pipe::mbar_init(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    uint32_t acc = 0;
+    uint32_t t = 0;
+    for (uint64_t off = b0; off < b1; off += slot, ++t) {
+        const uint32_t si = t % NSLOT, ph = (t / NSLOT) & 1u;
+        const uint32_t sz = uint32_t(min(uint64_t(slot), b1 - off));
+        if (warp == 0) {
+            if (lane == 0) {
+                pipe::mbar_wait(&empty[si], ph ^ 1u);
+                pipe::mbar_expect_tx(&full[si], sz);
+                pipe::bulk_load_1d(pring + size_t(si) * slot, x + off, sz, &full[si], pipe::evict_first_policy());
+            }
+        } else {
+            pipe::mbar_wait(&full[si], ph);
+            if (lane == 0) {
+                acc ^= *reinterpret_cast<const uint32_t*>(pring + size_t(si) * slot);
+                pipe::mbar_arrive(&empty[si]);
+            }
+        }
+    }
+    if (acc == 0x9E3779B9u) sink[0] = acc;
+}
+
 }  // namespace
+
+cudaError_t launch_read_probe_tma(const void* x, uint64_t bytes, uint32_t* sink, int grid, uint32_t slot, cudaStream_t s) {
+    const uint32_t nslot = 4;
+    const uint32_t smem = nslot * slot;
+    cudaFuncSetAttribute(read_probe_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    read_probe_tma_kernel<4><<<grid, 64, smem, s>>>(static_cast<const char*>(x), bytes, slot, sink);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_read_probe_async(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s) {
     read_probe_async_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(x), bytes / 16, sink);

@@ -284,7 +284,7 @@ int pick_engine(const tcr_config* c, const tcr::SpGeometry& g, bool f32) {
     const bool full = g.n / g.group_elems > 0;
     switch (c->engine) {
     case TCR_ENGINE_TCGEN05: return full && tcr::tc05_plan(g, &a, &b) ? TCR_ENGINE_TCGEN05 : TCR_ENGINE_MMA_SYNC_REGS;
-    case TCR_ENGINE_MMA_SYNC: return full && tcr::bulk_plan(g, &a, &b) ? TCR_ENGINE_MMA_SYNC : TCR_ENGINE_MMA_SYNC_REGS;
+    case TCR_ENGINE_MMA_SYNC: return tcr::bulk_supported(g) ? TCR_ENGINE_MMA_SYNC : TCR_ENGINE_MMA_SYNC_REGS;
     case TCR_ENGINE_MMA_SYNC_REGS: return TCR_ENGINE_MMA_SYNC_REGS;
     case TCR_ENGINE_MMA_SYNC_ASYNC: return TCR_ENGINE_MMA_SYNC_ASYNC;
     default:
@@ -405,9 +405,38 @@ int enqueue_sp_main(const void* x, uint64_t x_offset, uint64_t n, const tcr_conf
         ++g_launches;
         return TCR_OK;
     }
-    if (engine == TCR_ENGINE_TCGEN05 || engine == TCR_ENGINE_MMA_SYNC) {
-        // full groups on a TMA-fed persistent engine (one CTA per SM), the ragged tail (< 1 group)
-        // on the register engine; the last launch finalises
+    if (engine == TCR_ENGINE_MMA_SYNC) {
+        // full groups on the TMA-fed engine, the ragged tail group (if any) on the register
+        // engine in a second launch that finalises
+        const uint64_t n_tiles = n / g.group_elems;
+        tcr::SpParams pt = p;
+        pt.group_begin = 0;
+        pt.group_end = n_tiles;
+        if (n_tiles < g.n_groups) pt.finalize = tcr::kFinNone;
+        if (c->finalize == TCR_FINALIZE_ATOMIC) pt.finalize = tcr::kFinAtomic;
+        const int maxg = tcr::bulk_max_grid(c->R, p.debug_mode);
+        if (maxg <= 0) return fail(TCR_CUDA_ERROR, "TMA engine: shared-memory opt-in failed");
+        tcr::bulk_plan(g, &pt, maxg);
+        if (pt.split > 1 || pt.split_tail > 1) {
+            rc = ensure(&w->block_scratch, &w->bs_cap, g.n_groups * g.G, s);
+            if (rc) return rc;
+            rc = ensure_zero(&w->group_count, &w->gc_cap, g.n_groups, s);
+            if (rc) return rc;
+            pt.block_scratch = w->block_scratch;
+            pt.group_count = w->group_count;
+        }
+        rc = ensure_zero(&w->work_counter, &w->wc_cap, 1, s);
+        if (rc) return rc;
+        pt.work_counter = w->work_counter;
+        const uint64_t units = (pt.tail_group - pt.group_begin) * pt.split + (pt.group_end - pt.tail_group) * pt.split_tail;
+        TCR_CUDA(tcr::launch_bulk(pt, int(std::min<uint64_t>(units, uint64_t(maxg))), s));
+        ++g_launches;
+        if (n_tiles == g.n_groups) return TCR_OK;
+        p.group_begin = n_tiles;
+    }
+    if (engine == TCR_ENGINE_TCGEN05) {
+        // full groups on the tcgen05 engine (one CTA per SM), the ragged tail (< 1 group) on the
+        // register engine; the last launch finalises
         const uint64_t n_tiles = n / g.group_elems;
         tcr::SpParams pt = p;
         pt.group_begin = 0;
@@ -415,8 +444,7 @@ int enqueue_sp_main(const void* x, uint64_t x_offset, uint64_t n, const tcr_conf
         if (n_tiles < g.n_groups) pt.finalize = tcr::kFinNone;
         if (c->finalize == TCR_FINALIZE_ATOMIC) pt.finalize = tcr::kFinAtomic;
         const int grid = int(std::min<uint64_t>(n_tiles, uint64_t(tcr::sm_count())));
-        if (engine == TCR_ENGINE_TCGEN05) TCR_CUDA(tcr::launch_tc05(pt, g, n_tiles, grid, s));
-        else TCR_CUDA(tcr::launch_bulk(pt, g, n_tiles, grid, s));
+        TCR_CUDA(tcr::launch_tc05(pt, g, n_tiles, grid, s));
         ++g_launches;
         if (n_tiles == g.n_groups) return TCR_OK;
         p.group_begin = n_tiles;
@@ -1326,7 +1354,10 @@ int tcr_read_probe_async(const void* d_x, size_t bytes, void* stream) {
     if (rc) return rc;
     const tcr::Knobs& k = tcr::knobs();   // profiling: cp.async probe / CTAs per SM
     const int per_sm = k.probe_ctas > 0 ? k.probe_ctas : 8;
-    if (k.probe_async)
+    if (k.probe_tma)
+        TCR_CUDA(tcr::launch_read_probe_tma(d_x, bytes, w->sink(), tcr::sm_count() * (k.probe_ctas > 0 ? k.probe_ctas : 2),
+                                            k.probe_slot > 0 ? uint32_t(k.probe_slot) : 16384u, s));
+    else if (k.probe_async)
         TCR_CUDA(tcr::launch_read_probe_async(d_x, bytes, w->sink(), tcr::sm_count() * per_sm, s));
     else
         TCR_CUDA(tcr::launch_read_probe(d_x, bytes, w->sink(), tcr::sm_count() * per_sm, s));

@@ -83,9 +83,14 @@ cudaError_t launch_finalize(const SpParams& p, cudaStream_t s);
 bool tc05_plan(const SpGeometry& g, uint32_t* Q, uint32_t* ring_slots);
 cudaError_t launch_tc05(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
 
-// TMA-staged mma.sync engine (1-D bulk copies into a smem ring, ldmatrix.trans + HMMA) over the
-// first n_tiles FULL groups.  bulk_plan picks the slot (SC chunks) and ring depth.
-bool bulk_plan(const SpGeometry& g, uint32_t* SC, uint32_t* ring_slots);
+// TMA-fed mma.sync engine (tcr_sp_bulk.cu): per-warp rings refilled by 1-D bulk copies, a manager
+// warp claiming work units ahead (p.work_counter, zero on entry and exit) and running the trees.
+// FULL groups [p.group_begin, p.group_end) only.  bulk_plan sets split / split_tail / tail_group
+// (pieces need p.block_scratch and p.group_count, zero on entry and exit).
+bool bulk_supported(const SpGeometry& g);
+int bulk_max_grid(uint32_t R, int debug_mode = 0);
+void bulk_plan(const SpGeometry& g, SpParams* p, int grid);
+cudaError_t launch_bulk(const SpParams& p, int grid, cudaStream_t s);
 
 // Per-warp cp.async pipeline engine (LDGSTS ring per warp, ldmatrix.trans + HMMA); handles any
 // group range including the ragged tail (zero-fill copies).  binary16 input.
@@ -130,7 +135,6 @@ cudaError_t launch_round_level(const float* in, uint16_t* out, uint64_t count, u
 
 // fp32 -> binary16 (RNE, from_single) conversion of count elements.
 cudaError_t launch_convert_f32_f16(const float* in, uint16_t* out, uint64_t count, cudaStream_t s);
-cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s);
 int single_pass_m16_max_grid(bool f32_input, uint32_t R);
 
 // Input generation (harness.hpp:47-80 with SplitMix64 jump-ahead), binary16 or fp32 output.
@@ -149,6 +153,7 @@ int shuffle_max_grid();
 
 // Pure streaming-read probe: the achievable read bandwidth ceiling.
 cudaError_t launch_read_probe(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s);
+cudaError_t launch_read_probe_tma(const void* x, uint64_t bytes, uint32_t* sink, int grid, uint32_t slot, cudaStream_t s);
 cudaError_t launch_read_probe_async(const void* x, uint64_t bytes, uint32_t* sink, int grid, cudaStream_t s);
 
 // CUB DeviceReduce::Sum comparators.
@@ -199,6 +204,8 @@ struct Knobs {
     bool gm_no_cluster = false;        // TCR_GM_NO_CLUSTER
     bool gm_tr8_single = false;        // TCR_GM_TR8_SINGLE
     bool probe_async = false;          // TCR_PROBE=async
+    bool probe_tma = false;            // TCR_PROBE=tma (TCR_PROBE_SLOT bytes per copy, default 16384)
+    int probe_slot = 0;
     int probe_ctas = 0;                // TCR_PROBE_CTAS (0 = 8)
 };
 const Knobs& knobs();

@@ -466,9 +466,11 @@ int load_knobs_from_env() {
     flag("TCR_GM_TR8_SINGLE", &k.gm_tr8_single);
     if (const char* e = std::getenv("TCR_PROBE")) {
         k.probe_async = std::string(e) == "async";
+        k.probe_tma = std::string(e) == "tma";
         ++set;
     }
     num("TCR_PROBE_CTAS", &k.probe_ctas);
+    num("TCR_PROBE_SLOT", &k.probe_slot);
     g_knobs = k;
     return set;
 }

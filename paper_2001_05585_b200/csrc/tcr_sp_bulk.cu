@@ -1,18 +1,30 @@
-// tcr_sp_bulk.cu -- single-pass chained reduction, m = 16, TMA-staged mma.sync engine.
+// tcr_sp_bulk.cu -- single-pass chained reduction, m = 16: the TMA-fed mma.sync engine.
 //
-// Same element partition / block stage / group stage as tcr_single_pass.cu and tcr_tc05.cu
-// (reference reduction.hpp:164-184, :238-275).  Data path:
+// Same element partition, block stage and group stage as the other engines (reference
+// reduction.hpp:164-184, :238-275).  Warp-specialised persistent CTA, 8 streaming warps + 1
+// manager warp:
 //
-//   warp 0 (one thread)  cp.async.bulk (1-D TMA) of whole slots -- SC consecutive warp-chunks,
-//                        16-32 KB -- into a shared-memory ring, completion on an mbarrier.
-//   warps 1..8           per fragment ONE ldmatrix.x4.trans + ONE HMMA.16816: the transposing
-//                        matrix load hands every lane the A fragment whose row j is column j of
-//                        the 16x16 fragment (all 16 k), so D[j][*] = ones x M_r + C exactly as
-//                        reduction.hpp:177; C_R -> binary16, finishing HMMA per two chunks;
-//                        chunk results into the tile table, then block and group trees.
+//   streaming warp w   owns a ring of NS 2 KiB stages (4 fragments) and its own full-mbarriers;
+//                      lane 0 refills the stage it has just consumed with ONE cp.async.bulk
+//                      (1-D TMA, L2 evict-first) of the next 2 KiB of the warp's stream, so NS
+//                      stages are always in flight with no per-lane copy instructions.  The
+//                      warp's stream is its contiguous share (1/8) of every work unit, unit
+//                      after unit: the issue cursor runs into the NEXT unit before the current
+//                      one is consumed, so a unit boundary never drains the pipeline.
+//                      Per fragment: ldmatrix.x4.trans + two HMMA.16816 in the column-sum form
+//                      (A = ones, B = the fragment's column halves: C_r = ones x M_r + C_{r-1},
+//                      reduction.hpp:177); C_R -> binary16 (:179-181) stays in the lanes of
+//                      group g = chunk mod 8, one finishing HMMA per 8 chunks (:182).
+//   manager warp       claims work units QD ahead (atomic counter) into a shared queue, and per
+//                      unit -- off the streaming warps' critical path, double-buffered chunk
+//                      tables -- runs the block trees (:253), the group tree or, for a piece of
+//                      a group, publishes its block results and takes the group ticket (the
+//                      piece that completes the group runs the group tree).
 //
-// No data passes through registers before it is consumed, so memory-level parallelism is the
-// ring depth (~190 KB per SM), not a register budget.
+// Units: whole groups, then the last ~2 x grid units as pieces of a few blocks, so every CTA
+// finishes within one small piece of the others.  Full groups only (the ragged tail group, if
+// any, runs on the register engine in a second launch that finalises).
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include "tcr_device.cuh"
@@ -25,10 +37,12 @@ namespace {
 
 using namespace pipe;
 
-constexpr int kBkConsumers = 16;                      // consumer warps
-constexpr int kBkThreads = 32 * (1 + kBkConsumers);
-constexpr uint32_t kBkRingBytes = 192 * 1024;
-constexpr int kBkTileBufs = 2;
+constexpr int kBkWarps = 8;                        // streaming warps
+constexpr int kBkThreads = 32 * (kBkWarps + 1);    // + the manager warp
+constexpr int kBkQ = 8;                            // unit queue slots
+constexpr int kBkQD = 6;                           // units claimed ahead
+constexpr uint32_t kBkTailPieceBytes = 64 * 1024;  // target size of the tail pieces
+constexpr uint32_t kBkTailUnitsPerCta = 2;
 
 __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& d0, uint32_t& d1, uint32_t& d2, uint32_t& d3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -36,198 +50,353 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& d0, uint3
                  : "r"(addr));
 }
 
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-    return d;
-}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-struct BkLayout {
-    uint32_t bar_off, misc_off, total;
+__host__ __device__ constexpr uint32_t bk_gcd(uint32_t a, uint32_t b) { return b ? bk_gcd(b, a % b) : a; }
+__host__ __device__ constexpr uint32_t bk_lcm(uint32_t a, uint32_t b) { return a / bk_gcd(a, b) * b; }
+
+struct BkShared {
+    uint64_t full[kBkWarps][8];        // per-warp stage barriers (NS <= 8)
+    uint64_t qfull[kBkQ];              // unit queue slot written
+    uint64_t done[2];                  // chunk table b complete (8 streaming warps)
+    uint64_t freed[2];                 // chunk table b consumed by the manager
+    unsigned long long q[kBkQ];        // unit queue
+    float chunk[2][kMaxChunksPerGroup];
+    float block[kMaxChunksPerGroup];
+    float scratch[32];
+    int last;
 };
 
-__host__ __device__ inline BkLayout bk_layout(uint32_t slot_bytes, uint32_t ns) {
-    BkLayout L;
-    L.bar_off = slot_bytes * ns;
-    L.misc_off = L.bar_off + 16 * ns + 16;
-    L.total = L.misc_off + 4 * (2 * kBkTileBufs * kMaxChunksPerGroup + 32 + 8) + 128;
-    return L;
-}
-
-// Reduce SCW chunks of one warp in a slot.  Returns nothing; writes chunk results.
-template <int RT>
-__device__ __forceinline__ void bk_warp_chunks(uint32_t slot_saddr, uint32_t lane_off, uint32_t R, uint32_t scw,
-                                               uint32_t cw, float* chunks, uint32_t chunk_base, bool& ovf) {
-    const unsigned lane = lane_id();
-    const unsigned c = lane & 3u;
-    const uint32_t Rr = RT > 0 ? uint32_t(RT) : R;
-    const uint32_t chunk_bytes = Rr * 512u;
-    // two chunks per finishing MMA
-    for (uint32_t i = 0; i < scw; i += 2) {
-        uint32_t a01[2], a23[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t ci = cw + (i + h) * kBkConsumers;   // chunk index within the slot
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            if (i + h < scw) {
-                const uint32_t base = slot_saddr + ci * chunk_bytes + lane_off;
-                if constexpr (RT > 0) {
-#pragma unroll
-                    for (int r = 0; r < RT; ++r) {
-                        uint32_t d0, d1, d2, d3;
-                        ldsm_x4_trans(base + r * 512u, d0, d1, d2, d3);
-                        mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
-                    }
-                } else {
-                    for (uint32_t r = 0; r < Rr; ++r) {
-                        uint32_t d0, d1, d2, d3;
-                        ldsm_x4_trans(base + r * 512u, d0, d1, d2, d3);
-                        mma_16816(acc, d0, d1, d2, d3, kOnesF16x2, kOnesF16x2);
-                    }
-                }
-            }
-            // thread (g, c): acc[0] = C_R[j = g], acc[2] = C_R[j = g + 8]  -> binary16 (:179-181)
-            const uint32_t pk = uint32_t(f32_to_h(acc[0])) | (uint32_t(f32_to_h(acc[2])) << 16);
-            const uint32_t vA = __shfl_sync(kFull, pk, 8 * c);       // (h_2c,   h_2c+8)
-            const uint32_t vB = __shfl_sync(kFull, pk, 8 * c + 4);   // (h_2c+1, h_2c+9)
-            a01[h] = prmt(vA, vB, 0x5410);                           // (h_2c,   h_2c+1)
-            a23[h] = prmt(vA, vB, 0x7632);                           // (h_2c+8, h_2c+9)
-        }
-        float fin[4] = {0.f, 0.f, 0.f, 0.f};
-        // finishing MMA (reduction.hpp:182): rows 0-7 chunk i, rows 8-15 chunk i+1
-        mma_16816(fin, a01[0], a01[1], a23[0], a23[1], kOnesF16x2, kOnesF16x2);
-        ovf |= !isfinite(fin[0]) || (i + 1 < scw && !isfinite(fin[2]));
-        if (lane == 0) {
-            chunks[chunk_base + cw + i * kBkConsumers] = fin[0];
-            if (i + 1 < scw) chunks[chunk_base + cw + (i + 1) * kBkConsumers] = fin[2];
-        }
+// unit u -> (group, pieces of that group, piece)
+struct Unit {
+    uint64_t gi;
+    uint32_t S, piece;
+};
+__device__ __forceinline__ Unit unit_of(const SpParams& p, uint64_t u) {
+    const uint64_t u_main = (p.tail_group - p.group_begin) * p.split;
+    Unit r;
+    if (u < u_main) {
+        r.S = p.split;
+        r.gi = p.group_begin + u / r.S;
+        r.piece = uint32_t(u % r.S);
+    } else {
+        r.S = p.split_tail;
+        r.gi = p.tail_group + (u - u_main) / r.S;
+        r.piece = uint32_t((u - u_main) % r.S);
     }
+    return r;
 }
 
-template <int RT>
-__global__ void __launch_bounds__(kBkThreads, 1)
-sp_bulk_kernel(const SpParams p, const uint32_t SC, const uint32_t ns, const uint64_t n_tiles) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    const uint32_t R = RT > 0 ? uint32_t(RT) : p.R;
-    const uint32_t slot_bytes = SC * R * 512u;
-    const BkLayout L = bk_layout(slot_bytes, ns);
-    unsigned char* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
-    uint64_t* empty = full + ns;
-    float* s_chunk = reinterpret_cast<float*>(smem + L.misc_off);          // [kBkTileBufs][256]
-    float* s_block = s_chunk + kBkTileBufs * kMaxChunksPerGroup;           // [kBkTileBufs][256]
-    float* s_scratch = s_block + kBkTileBufs * kMaxChunksPerGroup;
-    int* s_last = reinterpret_cast<int*>(s_scratch + 32);
-
+template <int RT, int NS, uint32_t kBkStage, bool IL, int XM = 0>
+__global__ void __launch_bounds__(kBkThreads) sp_bulk_kernel(const SpParams p) {
+    extern __shared__ __align__(1024) unsigned char s_ring_raw[];
+    __shared__ BkShared sh;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-    const uint32_t Cg = p.G * p.W;
-    const uint32_t slots_per_tile = Cg / SC;
+    const uint32_t G = p.G, Cg = G * p.W;
+    const uint64_t u_total = (p.tail_group - p.group_begin) * p.split + (p.group_end - p.tail_group) * p.split_tail;
+    const unsigned long long last_claim = u_total + uint64_t(kBkQD) * gridDim.x - 1;
 
-    if (warp == 0 && lane == 0) {
-        for (uint32_t i = 0; i < ns; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kBkConsumers);
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < kBkWarps; ++w)
+            for (int s = 0; s < NS; ++s) mbar_init(&sh.full[w][s], 1);
+        for (int i = 0; i < kBkQ; ++i) mbar_init(&sh.qfull[i], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sh.done[b], kBkWarps);
+            mbar_init(&sh.freed[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     bool ovf = false;
 
-    if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t policy = evict_first_policy();
-            const char* x = static_cast<const char*>(p.x);
-            uint32_t t = 0;
-            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-                const uint64_t tile_byte0 = tile * uint64_t(Cg) * R * 512u;
-                for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
-                    const uint32_t rs = t % ns, ph = (t / ns) & 1;
-                    mbar_wait(&empty[rs], ph ^ 1);
-                    mbar_expect_tx(&full[rs], slot_bytes);
-                    bulk_load_1d(ring + size_t(rs) * slot_bytes, x + tile_byte0 + uint64_t(s) * slot_bytes, slot_bytes,
-                                 &full[rs], policy);
-                }
+    if (warp < kBkWarps) {
+        // ------------------------------------------------------------------ streaming warp
+        const uint32_t ring = smem_u32(s_ring_raw) + warp * NS * kBkStage;
+        const char* x = static_cast<const char*>(p.x);
+        const uint64_t policy = evict_first_policy();
+        // issue cursor (warp-uniform): queue index, next fragment of the warp's share, fragments
+        // in the share, the share's first chunk
+        uint32_t ik = 0, ifr = 0, infr = 0;
+        uint64_t ic0 = 0;
+        bool idone = false;
+        uint32_t t_issue = 0;
+        constexpr uint32_t GR = bk_lcm(kBkStage / 512u, uint32_t(RT));   // granule: lcm(stage, chunk) fragments
+        constexpr uint32_t GC = GR / RT;                                   // chunks per granule
+        auto open_issue_unit = [&]() {   // the share of unit ik (waits for the claim)
+            mbar_wait(&sh.qfull[ik % kBkQ], (ik / kBkQ) & 1u);
+            const unsigned long long u = sh.q[ik % kBkQ];
+            if (u >= u_total) {
+                idone = true;
+                return;
             }
+            const Unit un = unit_of(p, u);
+            const uint32_t Cu = Cg / un.S, nc = Cu / kBkWarps;
+            ic0 = un.gi * Cg + uint64_t(un.piece) * Cu + (IL ? 0 : uint64_t(warp) * nc);
+            infr = nc * uint32_t(RT);
+            ifr = 0;
+        };
+        auto issue = [&]() {   // every lane: the next stage of the stream into slot t_issue % NS
+            if (idone) return;
+            if (ifr == infr) {
+                ++ik;
+                open_issue_unit();
+                if (idone) return;
+            }
+            constexpr uint32_t FPS = kBkStage / 512u;
+            const uint32_t nf = min(FPS, infr - ifr);
+            const uint32_t slot = t_issue % NS;
+            const uint32_t bar = smem_u32(&sh.full[warp][slot]);
+            if (lane == 0) mbar_expect_tx(&sh.full[warp][slot], nf * 512u);
+            // IL: the share is granules w, w + 8, w + 16, ... of GR = lcm(stage, R) fragments (whole
+            // chunks, whole stages) of the unit, so the CTA reads one compact region at a time
+            // with one copy per stage; else the contiguous w-th eighth of the unit
+            const uint64_t gfrag = IL ? ic0 * uint64_t(RT) + (uint64_t(warp) + uint64_t(kBkWarps) * (ifr / GR)) * GR + ifr % GR
+                                      : ic0 * uint64_t(RT) + ifr;
+            if (lane == 0) {
+                if constexpr (XM == 2)   // profiling: no L2 eviction hint
+                    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                     ring + slot * kBkStage),
+                                 "l"(reinterpret_cast<uint64_t>(x + gfrag * 512u)), "r"(nf * 512u), "r"(bar)
+                                 : "memory");
+                else
+                    asm volatile(
+                        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                        "[%3], %4;" ::"r"(ring + slot * kBkStage),
+                        "l"(reinterpret_cast<uint64_t>(x + gfrag * 512u)), "r"(nf * 512u), "r"(bar), "l"(policy)
+                        : "memory");
+            }
+            ifr += nf;
+            ++t_issue;
+        };
+        open_issue_unit();
+#pragma unroll 1
+        for (int s = 0; s < NS; ++s) issue();
+        // ldmatrix row address of this lane inside a fragment: matrix mi = lane>>3 supplies line
+        // (k = (lane&7) + 8*(mi>>1), half = mi&1): d0 = (k 0-7, j 0-7), d1 = (k 0-7, j 8-15),
+        // d2 = (k 8-15, j 0-7), d3 = (k 8-15, j 8-15)
+        const uint32_t mi = lane >> 3;
+        const uint32_t ld_off = 32u * ((lane & 7u) + 8u * (mi >> 1)) + 16u * (mi & 1u);
+        const unsigned g = lane >> 2, c = lane & 3u;
+        uint32_t t_cons = 0;
+#pragma unroll 1
+        for (uint32_t k = 0;; ++k) {
+            mbar_wait(&sh.qfull[k % kBkQ], (k / kBkQ) & 1u);
+            const unsigned long long u = sh.q[k % kBkQ];
+            if (u >= u_total) break;
+            const Unit un = unit_of(p, u);
+            const uint32_t Cu = Cg / un.S, nc = Cu / kBkWarps;
+            const uint32_t buf = k & 1u;
+            mbar_wait(&sh.freed[buf], ((k >> 1) & 1u) ^ 1u);   // the manager is done with this table
+            // chunk ci of the share is unit-local chunk (w + 8 (ci / GC)) GC + ci % GC (IL) or w nc + ci
+            float* out = sh.chunk[buf] + (IL ? warp * GC : warp * nc);
+            auto oidx = [&](uint32_t i) { return IL ? (i / GC) * (kBkWarps * GC) + i % GC : i; };
+            const uint32_t nfrag = nc * uint32_t(RT);
+            float lo[4] = {0.f, 0.f, 0.f, 0.f}, hi[4] = {0.f, 0.f, 0.f, 0.f};
+            uint32_t bb0 = 0, bb1 = 0;
+            uint32_t r = 0, ci = 0;
+#pragma unroll 1
+            constexpr uint32_t FPS = kBkStage / 512u;   // fragments per stage
+            for (uint32_t f0 = 0; f0 < nfrag; f0 += FPS) {
+                const uint32_t slot = t_cons % NS;
+                mbar_wait(&sh.full[warp][slot], (t_cons / NS) & 1u);
+                const uint32_t sb = ring + slot * kBkStage + ld_off;
+                const uint32_t nf = min(FPS, nfrag - f0);
+#pragma unroll
+                for (uint32_t q = 0; q < FPS; ++q) {
+                    if (XM != 1 && q < nf) {   // XM 1 (profiling): stream only, no MMA
+                        uint32_t d0, d1, d2, d3;
+                        ldsm_x4_trans(sb + q * 512u, d0, d1, d2, d3);
+                        // C_r = ones x M_r + C_{r-1} (reduction.hpp:177): columns 0-7 and 8-15
+                        mma_16816(lo, kOnesF16x2, kOnesF16x2, kOnesF16x2, kOnesF16x2, d0, d2);
+                        mma_16816(hi, kOnesF16x2, kOnesF16x2, kOnesF16x2, kOnesF16x2, d1, d3);
+                        if (++r == uint32_t(RT)) {
+                            r = 0;
+                            // C_R -> binary16 (:179-181), kept by the lanes of group g = ci mod 8
+                            const uint32_t b0 = pack_h2(lo[0], lo[1]), b1 = pack_h2(hi[0], hi[1]);
+                            const uint32_t kk = ci & 7u;
+                            if (g == kk) {
+                                bb0 = b0;
+                                bb1 = b1;
+                            }
+                            lo[0] = lo[1] = lo[2] = lo[3] = hi[0] = hi[1] = hi[2] = hi[3] = 0.f;
+                            if (kk == 7u || ci + 1 == nc) {
+                                // finishing MMA (:182) for chunks ci-kk .. ci (missing ones are zero)
+                                float fin[4] = {0.f, 0.f, 0.f, 0.f};
+                                mma_16816(fin, kOnesF16x2, kOnesF16x2, kOnesF16x2, kOnesF16x2, bb0, bb1);
+                                ovf |= !isfinite(fin[0]) || !isfinite(fin[1]);
+                                if (g == 0) {
+                                    if (2 * c <= kk) out[oidx(ci - kk + 2 * c)] = fin[0];
+                                    if (2 * c + 1 <= kk) out[oidx(ci - kk + 2 * c + 1)] = fin[1];
+                                }
+                                bb0 = bb1 = 0;
+                            }
+                            ++ci;
+                        }
+                    }
+                }
+                // the MMAs consumed this lane's fragments: order its generic reads of the slot
+                // before the async-proxy refill, then lane 0 refills it
+                fence_proxy_async();
+                __syncwarp();
+                issue();
+                ++t_cons;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.done[buf]);
         }
     } else {
-        const uint32_t cw = warp - 1;   // consumer index
-        // ldmatrix row address of this lane inside a fragment: matrix mi = lane>>3 supplies
-        // line (k = (lane&7) + 8*(mi>>1), half = mi&1)  -> byte 32k + 16*half
-        const uint32_t mi = lane >> 3;
-        const uint32_t lane_off = 32u * ((lane & 7u) + 8u * (mi >> 1)) + 16u * (mi & 1u);
-        const uint32_t scw = SC / kBkConsumers;  // chunks per consumer warp per slot
-        uint32_t t = 0, k = 0;
-        for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
-            const uint32_t buf = k % kBkTileBufs;
-            float* chunks = s_chunk + buf * kMaxChunksPerGroup;
-            for (uint32_t s = 0; s < slots_per_tile; ++s, ++t) {
-                const uint32_t rs = t % ns, ph = (t / ns) & 1;
-                mbar_wait(&full[rs], ph);
-                const uint32_t sa = smem_u32(ring + size_t(rs) * slot_bytes);
-                if (p.debug_mode != 1) bk_warp_chunks<RT>(sa, lane_off, R, scw, cw, chunks, s * SC, ovf);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[rs]);
+        // -------------------------------------------------------------------- manager warp
+        unsigned long long* ctr = p.work_counter;
+        if (lane == 0) {
+            for (int i = 0; i < kBkQD; ++i) {
+                const unsigned long long u = atomicAdd(ctr, 1ull);
+                if (u == last_claim) *ctr = 0ull;
+                sh.q[i] = u;
+                mbar_arrive(&sh.qfull[i]);
             }
-            named_bar(1, 32 * kBkConsumers);
-            float* blocks = s_block + buf * kMaxChunksPerGroup;
-            tile_trees_blocks(p, tile, chunks, blocks, cw, kBkConsumers);
-            named_bar(1, 32 * kBkConsumers);
-            if (cw == 0) tile_tree_group(p, tile, blocks);
         }
-        if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
+        __syncwarp();
+#pragma unroll 1
+        for (uint32_t k = 0;; ++k) {
+            const unsigned long long u = sh.q[k % kBkQ];   // written by this warp's lane 0
+            if (u >= u_total) break;
+            unsigned long long nxt = 0;
+            if (lane == 0) nxt = atomicAdd(ctr, 1ull);   // its latency hides behind this unit
+            const Unit un = unit_of(p, u);
+            const uint32_t Gu = G / un.S;
+            const uint64_t b0 = un.gi * G + uint64_t(un.piece) * Gu;
+            const uint32_t buf = k & 1u;
+            mbar_wait(&sh.done[buf], (k >> 1) & 1u);
+            range_trees_blocks(p, b0, Gu, sh.chunk[buf], sh.block, 0, 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.freed[buf]);
+            if (un.S == 1) {
+                tile_tree_group(p, un.gi, sh.block);
+            } else {
+                for (uint32_t b = lane; b < Gu; b += 32) p.block_scratch[b0 + b] = sh.block[b];
+                __syncwarp();
+                unsigned t = 0;
+                if (lane == 0)
+                    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(p.group_count + un.gi) : "memory");
+                t = __shfl_sync(kFull, t, 0);
+                __syncwarp();   // lane 0's acquire orders the other lanes' reads of the pieces
+                if (t == un.S - 1) {
+                    tile_tree_group<true>(p, un.gi, p.block_scratch + un.gi * G);
+                    if (lane == 0) p.group_count[un.gi] = 0u;
+                }
+            }
+            if (lane == 0) {
+                if (nxt == last_claim) *ctr = 0ull;
+                const uint32_t slot = (k + kBkQD) % kBkQ;
+                sh.q[slot] = nxt;
+                mbar_arrive(&sh.qfull[slot]);
+            }
+            __syncwarp();
+        }
     }
-    __threadfence();
+    if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __syncthreads();
-    finalize_last_cta(p, s_scratch, s_last, 512);
+    finalize_last_cta<true>(p, sh.scratch, &sh.last, 32 * kBkWarps);
+}
+
+using BkKernel = void (*)(SpParams);
+
+struct BkPick {
+    BkKernel fn;
+    uint32_t ring;   // dynamic shared memory: 8 warps x NS stages
+};
+
+template <int RT, int NS, uint32_t SB, bool IL = false, int XM = 0>
+constexpr BkPick bk_make() {
+    return {sp_bulk_kernel<RT, NS, SB, IL, XM>, uint32_t(kBkWarps) * NS * SB};
+}
+
+// Ring shape per chain length: NS stages of SB bytes per warp (default 4 x 2 KiB), each warp
+// streaming the contiguous eighth of a unit.  Profiling modes (debug_mode, R = 1; measured in
+// DESIGN.md section 3): 30 = 6 x 2 KiB, 31 = 3 x 4 KiB, 32 = 8 x 1 KiB, 33 / 37 = shares
+// interleaved in granules of lcm(stage, chunk), 34 / 36 / 38 = stream only (no MMA; timing),
+// 35 = no L2 eviction hint.
+BkPick bk_pick(uint32_t R, int mode = 0) {
+    if (R == 1 && mode == 30) return bk_make<1, 6, 2048>();
+    if (R == 1 && mode == 31) return bk_make<1, 3, 4096>();
+    if (R == 1 && mode == 32) return bk_make<1, 8, 1024>();
+    if (R == 1 && mode == 33) return bk_make<1, 4, 2048, true>();       // granule-interleaved shares
+    if (R == 1 && mode == 34) return bk_make<1, 4, 2048, false, 1>();   // stream only (timing)
+    if (R == 1 && mode == 35) return bk_make<1, 4, 2048, false, 2>();   // no L2 hint
+    if (R == 1 && mode == 36) return bk_make<1, 4, 2048, true, 1>();    // stream only, interleaved
+    if (R == 1 && mode == 37) return bk_make<1, 3, 4096, true>();       // 3 x 4 KiB interleaved
+    if (R == 1 && mode == 38) return bk_make<1, 3, 4096, true, 1>();    // the same, stream only
+    switch (R) {
+    case 1: return bk_make<1, 4, 2048>();
+    case 2: return bk_make<2, 4, 2048>();
+    case 3: return bk_make<3, 4, 2048>();
+    case 4: return bk_make<4, 4, 2048>();
+    case 5: return bk_make<5, 4, 2048>();
+    case 6: return bk_make<6, 4, 2048>();
+    case 7: return bk_make<7, 4, 2048>();
+    case 8: return bk_make<8, 4, 2048>();
+    default: return {nullptr, 0};
+    }
 }
 
 }  // namespace
 
-bool bulk_plan(const SpGeometry& g, uint32_t* SC_out, uint32_t* ns_out) {
-    if (g.m != 16) return false;
-    const uint64_t cg = uint64_t(g.G) * g.W;
-    // slot = SC chunks (a multiple of the consumer count), ~32 KB, dividing the tile
-    uint32_t SC = 0;
-    for (uint32_t cand = 256; cand >= uint32_t(kBkConsumers); cand -= kBkConsumers) {
-        if (cand % kBkConsumers == 0 && cg % cand == 0 && uint64_t(cand) * g.R * 512u <= 49152u) {
-            SC = cand;
-            break;
-        }
-    }
-    if (!SC) return false;
-    const uint32_t slot = SC * g.R * 512u;
-    uint32_t ns = kBkRingBytes / slot;
-    if (ns > 16) ns = 16;
-    if (ns < 3) return false;
-    if (bk_layout(slot, ns).total > 227u * 1024u) return false;
-    *SC_out = SC;
-    *ns_out = ns;
-    return true;
+// chunks per interleave granule (lcm(8, R) fragments: covers the 2 and 4 KiB stage shapes)
+static uint32_t bk_granule_chunks(uint32_t R) { return bk_lcm(8, R) / R; }
+
+bool bulk_supported(const SpGeometry& g) {
+    // R <= 8 (compile-time chain), the group a whole number of granules per warp, at least one
+    // full group
+    return g.m == 16 && g.R >= 1 && g.R <= 8 && (uint64_t(g.G) * g.W) % (kBkWarps * bk_granule_chunks(g.R)) == 0 &&
+           uint64_t(g.G) * g.W <= uint64_t(kMaxChunksPerGroup) && g.n / g.group_elems > 0;
 }
 
-cudaError_t launch_bulk(const SpParams& p, const SpGeometry& g, uint64_t n_tiles, int grid, cudaStream_t s) {
-    uint32_t SC, ns;
-    if (!bulk_plan(g, &SC, &ns)) return cudaErrorInvalidValue;
-    const BkLayout L = bk_layout(SC * g.R * 512u, ns);
+int bulk_max_grid(uint32_t R, int mode) {
     static PerDeviceOnce once;
-    const cudaError_t ea = once([] {
-        for (auto fn : {sp_bulk_kernel<0>, sp_bulk_kernel<1>, sp_bulk_kernel<2>, sp_bulk_kernel<3>,
-                        sp_bulk_kernel<4>, sp_bulk_kernel<5>}) {
-            const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            if (e != cudaSuccess) return e;
-        }
+    const cudaError_t e = once([] {
+        for (int md : {0, 30, 31, 32, 33, 34, 35, 36, 37, 38})
+            for (uint32_t r = 1; r <= 8; ++r) {
+                const BkPick k = bk_pick(r, md);
+                const cudaError_t a = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           int(k.ring));
+                if (a != cudaSuccess) return a;
+            }
         return cudaSuccess;
     });
-    if (ea != cudaSuccess) return ea;
-    switch (g.R) {
-    case 1: sp_bulk_kernel<1><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
-    case 2: sp_bulk_kernel<2><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
-    case 3: sp_bulk_kernel<3><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
-    case 4: sp_bulk_kernel<4><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
-    case 5: sp_bulk_kernel<5><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
-    default: sp_bulk_kernel<0><<<grid, kBkThreads, L.total, s>>>(p, SC, ns, n_tiles); break;
+    if (e != cudaSuccess) return 0;
+    const BkPick k = bk_pick(R, mode);
+    if (!k.fn) return 0;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.fn, kBkThreads, k.ring);
+    return std::max(1, std::min(per_sm, 2)) * sm_count();
+}
+
+void bulk_plan(const SpGeometry& g, SpParams* p, int grid) {
+    const uint64_t groups = p->group_end - p->group_begin;
+    const uint32_t Cg = g.G * g.W;
+    // pieces of S whole blocks, each warp share a whole number of chunks
+    auto ok = [&](uint32_t S) {
+        return S <= g.G && g.G % S == 0 && (Cg / S) % (kBkWarps * bk_granule_chunks(g.R)) == 0;
+    };
+    uint32_t S = 1;
+    while (double(groups) * S < 3.0 * grid && ok(S * 2)) S *= 2;
+    uint32_t St = S;
+    const uint64_t group_bytes = g.group_elems * 2;
+    while (group_bytes / St > kBkTailPieceBytes && ok(St * 2)) St *= 2;
+    p->split = S;
+    p->split_tail = St;
+    p->tail_group = p->group_end;
+    if (St > S) {
+        const uint64_t tail = std::min<uint64_t>(groups, (uint64_t(kBkTailUnitsPerCta) * grid + St - 1) / St);
+        p->tail_group = p->group_end - tail;
+        if (p->tail_group == p->group_begin) p->split = St;
     }
+}
+
+cudaError_t launch_bulk(const SpParams& p, int grid, cudaStream_t s) {
+    const BkPick k = bk_pick(p.R, p.debug_mode);
+    if (!k.fn || bulk_max_grid(p.R, p.debug_mode) == 0) return cudaErrorInvalidValue;
+    k.fn<<<grid, kBkThreads, k.ring, s>>>(p);
     return cudaGetLastError();
 }
 

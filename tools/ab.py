@@ -4,6 +4,7 @@
     python tools/ab.py [--n 1073741824] [--rounds 7] [--reps 10] SPEC [SPEC ...]
 
 SPEC = label:engine:R:B[:ENV=VAL,...]  e.g.  async:4:1:1024  tc05:2:1:1024:TCR_DEBUG_MODE=3
+(PROBE=1 in the ENV list times the streaming-read probe instead, e.g. tma:0:1:1:PROBE=1,TCR_PROBE=tma)
 (LIB=path in the ENV list times another build of libtcreduce_b200.so, e.g. a previous commit's;
 M=m sets the fragment side, default 16)
 Rounds alternate between the specs so clock / thermal drift hits all of them alike; the
@@ -62,8 +63,10 @@ def main():
         env = dict(kv.split("=") for kv in parts[4].split(",")) if len(parts) > 4 and parts[4] else {}
         lib_path = env.pop("LIB", None)
         m = int(env.pop("M", 16))
+        probe = env.pop("PROBE", None) is not None   # time the streaming-read probe instead
         cfg = T.ReductionConfig(m=m, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])))
-        specs.append((parts[0], cfg.to_c(), env, _capi.load() if lib_path is None else _load_other(lib_path)))
+        specs.append((parts[0], None if probe else cfg.to_c(), env,
+                      _capi.load() if lib_path is None else _load_other(lib_path)))
     times = {s[0]: [] for s in specs}
     vals = {}
     for rnd in range(a.rounds):
@@ -72,13 +75,18 @@ def main():
             os.environ.update(env)
             lib.tcr_enable_profiling_knobs.restype = C.c_int
             lib.tcr_enable_profiling_knobs()   # knobs are read only on this explicit call
+            def call():
+                if c is None:
+                    _capi.check(lib.tcr_read_probe_async(xp, 2 * a.n, sp))
+                else:
+                    _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))
             try:
                 for _ in range(3):
-                    _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))
+                    call()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
                 for _ in range(a.reps):
-                    _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))
+                    call()
                 e1.record(st)
                 e1.synchronize()
                 times[label].append(e0.elapsed_time(e1) / a.reps)
