@@ -30,6 +30,8 @@ import statistics
 import subprocess
 import sys
 import threading
+
+import numpy as np
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -171,6 +173,27 @@ class Clocks:
                 "timed_region_ms": (t1 - t0) * 1e3 if t0 is not None and t1 is not None else None}
 
 
+def cpu_model() -> str:
+    """The host CPU model (lscpu / /proc/cpuinfo) the CPU baseline ran on."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+CPU_SAMPLE = 1 << 26   # the bounded CPU sample of the 2^30 workload (both CPU legs)
+
+
 def cpu_reference_rate(n_sample: int, reps: int = 1):
     """Reference CPU path on all host threads: (Gelem/s, kind, cores, value)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -195,7 +218,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n_sample = 1 << 22
+    n_sample = CPU_SAMPLE
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     cores = os.cpu_count() or 1
@@ -220,8 +243,10 @@ def run_reference(args):
             "impl": "reference",
             "config": {"workload": "single_pass m=%d R=%d B=%d uniform[0,1) seed 0" % (args.m, args.R, args.B),
                        "n_per_step": n_sample, "n_target": args.n, "parallelism": "host threads"},
-            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind,
-                             "sample": f"n={n_sample} per step (bounded sample of the n=2^30 workload)"},
+            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                             "sample": f"uniform[0,1) seed 0, n=2^{n_sample.bit_length() - 1} per step (bounded "
+                                       f"sample of the n=2^30 workload; the same sample as the GPU arm's "
+                                       f"cpu_baseline)"},
             "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -519,7 +544,17 @@ def main():
         xf.copy_(T.generate("uniform", 0, n, device=dev, dtype="float32", first=rank * n).cpu())
         torch.cuda.empty_cache()
         e32, v32 = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xf.data_ptr()))
+        # the reference's real caller: std::span<const float> over a PAGEABLE std::vector
+        # (reduction.hpp:344) -- plain malloc'd host memory, staged through the library's pinned ring
+        xpg = np.empty(n, dtype=np.float32)
+        xpg[:] = xf.numpy()
         del xf
+        e32p, v32p = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xpg.ctypes.data))
+        xpg16 = np.empty(n, dtype=np.uint16)
+        xpg16[:] = x.cpu().view(torch.int16).numpy().view(np.uint16)
+        del xpg
+        e16p, v16p = time_host(lib.tcr_reduce_f16_host, C.c_void_p(xpg16.ctypes.data))
+        del xpg16
         e2e = {"value": world * n / e16 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": world * 2 * n,
                "d2h_bytes_per_step": world * 8, "ms_per_step": e16 * 1e3,
                "path": "tcr_reduce_f16_host (pinned binary16 host input, pipelined H2D + reduce)",
@@ -528,7 +563,18 @@ def main():
                               "d2h_bytes_per_step": world * 8, "ms_per_step": e32 * 1e3,
                               "path": "tcr_reduce_f32_host = reduce(std::span<const float>) drop-in (pinned fp32 "
                                       "host input, pipelined H2D + fused convert/reduce)",
-                              "same_value_as_f16_host": v32 == v16}}
+                              "same_value_as_f16_host": v32 == v16},
+               "f32_dropin_pageable": {"value": world * n / e32p / 1e9, "unit": "Gelem/s",
+                                       "h2d_bytes_per_step": world * 4 * n, "d2h_bytes_per_step": world * 8,
+                                       "ms_per_step": e32p * 1e3,
+                                       "path": "tcr_reduce_f32_host on pageable host memory (the reference caller's "
+                                               "std::vector): parallel host copies into a pinned staging ring, "
+                                               "pipelined H2D + fused convert/reduce",
+                                       "same_value_as_pinned": v32p == v32},
+               "f16_pageable": {"value": world * n / e16p / 1e9, "unit": "Gelem/s",
+                                "h2d_bytes_per_step": world * 2 * n, "d2h_bytes_per_step": world * 8,
+                                "ms_per_step": e16p * 1e3, "path": "tcr_reduce_f16_host on pageable host memory",
+                                "same_value_as_pinned": v16p == v16}}
       except Exception as exc:
         e2e = {"error": repr(exc)}
 
@@ -547,8 +593,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
       try:
-        v, kind, cores, val, times = cpu_reference_rate(1 << 26)
-        cpu = {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind,
+        v, kind, cores, val, times = cpu_reference_rate(CPU_SAMPLE)
+        cpu = {"value": v, "unit": "Gelem/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
                "sample": "uniform[0,1) seed 0, n=2^26 (bounded sample of the 2^30 workload), m=16 R=1 B=1024",
                "seconds": times[0]}
       except Exception as exc:

@@ -19,6 +19,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 
 #include "tcr_kernels.h"
@@ -120,6 +121,11 @@ struct Workspace {
     size_t ring_cap = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    // pageable host input: a pinned staging ring filled by parallel host copies (kStageSlots
+    // slots of kStageBytes), each slot's H2D tracked by an event
+    void* pin_stage = nullptr;
+    cudaEvent_t pin_free[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t pin_seq = 0;
     // split variant: the shuffle32 share on an auxiliary stream
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -135,6 +141,10 @@ struct Workspace {
         f(work_counter); f(ord_ws); f(stage); f(unaligned); f(ring[0]); f(ring[1]); f(ring16[0]); f(ring16[1]);
         if (host_pinned) cudaFreeHost(host_pinned);
         host_pinned = nullptr;
+        if (pin_stage) cudaFreeHost(pin_stage);
+        pin_stage = nullptr;
+        for (cudaEvent_t* e : {&pin_free[0], &pin_free[1], &pin_free[2], &pin_free[3]})
+            if (*e) cudaEventDestroy(*e), *e = nullptr;
         for (cudaEvent_t* e : {&copied[0], &copied[1], &consumed[0], &consumed[1], &fork, &join})
             if (*e) cudaEventDestroy(*e), *e = nullptr;
         for (cudaStream_t* st : {&copy_stream, &aux_stream})
@@ -1165,8 +1175,61 @@ int host_stream(cudaStream_t* out) {
     return TCR_OK;
 }
 
+// H2D of a pageable host range (the reference's caller passes a std::vector, reduction.hpp:344):
+// through the workspace's pinned staging ring, each slot filled by parallel host copies while
+// the previous slots' DMAs run on the copy stream.  Pinned (or registered) sources go straight.
+constexpr size_t kStageBytes = 16u << 20;
+constexpr int kStageSlots = 4;
+
+bool is_pageable(const void* x) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, x) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return pa.type == cudaMemoryTypeUnregistered;
+}
+
+void parallel_copy(char* dst, const char* src, size_t bytes) {
+    static const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = unsigned(std::min<size_t>(std::min(16u, hw), std::max<size_t>(1, bytes >> 20)));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t per = (bytes / nt + 63) & ~size_t(63);
+    for (unsigned t = 1; t < nt; ++t) {
+        const size_t b0 = std::min(bytes, per * t), b1 = std::min(bytes, per * (t + 1));
+        if (b1 > b0) pool.emplace_back([=] { std::memcpy(dst + b0, src + b0, b1 - b0); });
+    }
+    std::memcpy(dst, src, std::min(bytes, per));
+    for (auto& th : pool) th.join();
+}
+
+int h2d(void* dst, const char* src, size_t bytes, bool pageable, Workspace* w) {
+    if (!pageable) {
+        TCR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, w->copy_stream));
+        return TCR_OK;
+    }
+    if (!w->pin_stage) {
+        TCR_CUDA(cudaMallocHost(&w->pin_stage, kStageBytes * kStageSlots));
+        for (auto& e : w->pin_free) TCR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (size_t off = 0; off < bytes; off += kStageBytes) {
+        const int slot = int(w->pin_seq++ % kStageSlots);
+        char* pin = static_cast<char*>(w->pin_stage) + size_t(slot) * kStageBytes;
+        TCR_CUDA(cudaEventSynchronize(w->pin_free[slot]));   // its previous DMA is done
+        const size_t b = std::min(kStageBytes, bytes - off);
+        parallel_copy(pin, src + off, b);
+        TCR_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin, b, cudaMemcpyHostToDevice, w->copy_stream));
+        TCR_CUDA(cudaEventRecord(w->pin_free[slot], w->copy_stream));
+    }
+    return TCR_OK;
+}
+
 // Host-input reduce(): pipelined H2D of group-aligned chunks on a copy stream (2-slot ring,
-// pinned or pageable source), reduce kernel per chunk on the compute stream, one finaliser.
+// pinned source, or pageable through the pinned staging ring), reduce kernel per chunk on the compute stream, one finaliser.
 // f32: fp32 values converted to binary16 on the device (fused into the m = 16 kernel);
 // otherwise binary16 bit patterns (half the bytes over PCIe).
 int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outcome* out) {
@@ -1234,6 +1297,7 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
     TCR_CUDA(cudaMemsetAsync(w->overflow(), 0, 4, s));
     const char* xb = static_cast<const char*>(x);
     const bool f32_direct = f32 && cc.m != 16 && tcr::genm_f32_supported(g);
+    const bool pageable = n * esz >= (1u << 20) && is_pageable(x);
     for (uint64_t k = 0; k < n_chunks; ++k) {
         const int slot = int(k & 1);
         const uint64_t e0 = k * chunk_elems;
@@ -1242,7 +1306,8 @@ int reduce_host(const void* x, bool f32, size_t n, const tcr_config* c, tcr_outc
         const uint64_t g1 = std::min<uint64_t>(g.n_groups, g0 + groups_per_chunk);
         void* dst = f32 ? static_cast<void*>(w->ring[slot]) : static_cast<void*>(w->ring16[slot]);
         if (k >= 2) TCR_CUDA(cudaStreamWaitEvent(w->copy_stream, w->consumed[slot], 0));
-        TCR_CUDA(cudaMemcpyAsync(dst, xb + e0 * esz, (e1 - e0) * esz, cudaMemcpyHostToDevice, w->copy_stream));
+        rc = h2d(dst, xb + e0 * esz, (e1 - e0) * esz, pageable, w);
+        if (rc) return rc;
         TCR_CUDA(cudaEventRecord(w->copied[slot], w->copy_stream));
         TCR_CUDA(cudaStreamWaitEvent(s, w->copied[slot], 0));
         const bool last = (k + 1 == n_chunks);
