@@ -201,10 +201,10 @@ const char* tcr_version(void);
  * the defaults.  Not thread-safe against concurrent reductions. */
 int tcr_enable_profiling_knobs(void);
 void tcr_reset_profiling_knobs(void);
-/* Profiling: counters of the last ascending ORDERED walk (CTA composites applied, group records
- * applied, groups added block by block, of which with an invalid / unsafe record), then the
- * %globaltimer stamps (ns) of its phases: first CTA start, last look-back end, last record end,
- * walk start, walk end.  host: 9 values.  Re-arms the stamps. */
+/* Profiling: counters of the last ORDERED walk (tree nodes applied, CTA runs applied, segment
+ * records applied, 32-block segments added block by block), then the %globaltimer stamps (ns) of
+ * its phases: first CTA start, last look-back end, last record end, walk start, walk end.
+ * host: 9 values.  Re-arms the stamps. */
 int tcr_ordered_stats(unsigned long long* host9);
 /* Profiling: per-CTA %globaltimer stamps of the last TCR_DEBUG_MODE=20 launch. */
 int tcr_debug_timestamps(unsigned long long* host, size_t count);

@@ -494,7 +494,8 @@ int ensure_order(Workspace* w, uint64_t nb, uint64_t seed, cudaStream_t s) {
     return TCR_OK;
 }
 
-// ORDERED finalise: the serial chain over the published block results (tcr_ordered.cu).
+// ORDERED finalise: the reference's serial fp32 chain over the published block results, in
+// ascending or seeded-permutation order, evaluated in parallel and bit for bit (tcr_ordered.cu).
 int enqueue_ordered(uint64_t n, const tcr_config* c, const float* blocks, float* d_result, Workspace* w, cudaStream_t s) {
     const tcr::SpGeometry g = tcr::make_geometry(n, c->m, c->R, c->B);
     const uint32_t* order = nullptr;
@@ -502,17 +503,16 @@ int enqueue_ordered(uint64_t n, const tcr_config* c, const float* blocks, float*
         int rc = ensure_order(w, g.n_blocks, c->atomic_seed, s);
         if (rc) return rc;
         order = w->order;
-    } else if (tcr::knobs().debug_mode != 40) {   // 40: profiling only, the serial chain
-        // ascending: the parallel exact evaluation over the group partials' binades
-        const size_t bytes = tcr::ordered_ws_bytes(g.n_groups, tcr::ordered_grid(g.n_groups));
-        int rc = ensure_zero(&w->ord_ws, &w->ord_cap, (bytes + 3) / 4, s);   // look-back flags start at 0
-        if (rc) return rc;
-        TCR_CUDA(tcr::launch_ordered_ascending(blocks, w->group_partials, g.n_blocks, g.n_groups, g.G, w->ord_ws,
-                                               w->ticket(), d_result, s));
+    }
+    if (tcr::knobs().debug_mode == 40) {   // profiling only: the literal serial chain
+        TCR_CUDA(tcr::launch_ordered(blocks, order, g.n_blocks, d_result, s));
         ++g_launches;
         return TCR_OK;
     }
-    TCR_CUDA(tcr::launch_ordered(blocks, order, g.n_blocks, d_result, s));
+    const size_t bytes = tcr::ordered_ws_bytes(g.n_blocks);
+    int rc = ensure_zero(&w->ord_ws, &w->ord_cap, (bytes + 3) / 4, s);   // look-back flags start at 0
+    if (rc) return rc;
+    TCR_CUDA(tcr::launch_ordered_parallel(blocks, order, g.n_blocks, w->ord_ws, w->ticket(), d_result, s));
     ++g_launches;
     return TCR_OK;
 }

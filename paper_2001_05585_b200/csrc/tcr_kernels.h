@@ -106,14 +106,15 @@ bool async_plan(const SpGeometry& g, SpParams* p, int grid);
 // ORDERED finaliser (tcr_ordered.cu): serial binary32 sum of blocks[order[k]] (order null:
 // ascending), the reference's accumulation (reduction.hpp:257-268).
 cudaError_t launch_ordered(const float* blocks, const uint32_t* order, uint64_t nb, float* result, cudaStream_t s);
-// Ascending order in parallel, bit-identical to the serial chain (tcr_ordered.cu): per-group
-// records of the binade-local integer arithmetic, composed into runs, walked by one warp.
-// ws: >= ordered_ws_bytes(n_groups, ordered_grid(n_groups)); ticket zero on entry and exit.
-size_t ordered_ws_bytes(uint64_t n_groups, int grid);
-int ordered_stats(unsigned long long* host);   // profiling: counters of the last walk
-int ordered_grid(uint64_t n_groups);
-cudaError_t launch_ordered_ascending(const float* blocks, const float* group_partials, uint64_t nb, uint64_t n_groups,
-                                     uint32_t G, void* ws, uint32_t* ticket, float* result, cudaStream_t s);
+// Any order in parallel, bit-identical to the serial chain (tcr_ordered.cu): per-segment
+// records of the binade-local integer arithmetic, composed into runs and a tree, walked by one
+// warp.  order: position -> block, or null (ascending).  ws: >= ordered_ws_bytes(nb), zero on
+// first use (look-back flags return to zero); ticket zero on entry and exit.
+size_t ordered_ws_bytes(uint64_t nb);
+int ordered_stats(unsigned long long* host);   // profiling: counters and phase stamps of the last walk
+int ordered_grid(uint64_t nb);
+cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, uint64_t nb, void* ws, uint32_t* ticket,
+                                    float* result, cudaStream_t s);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.
 bool genm_supported(const SpGeometry& g);

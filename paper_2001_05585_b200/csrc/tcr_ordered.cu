@@ -62,48 +62,67 @@ __global__ void __launch_bounds__(kOrdThreads) ordered_serial_kernel(const float
     if (tid == 0) *result = acc;
 }
 
-// ------------------------------------------------------------------ ascending order, in parallel
+// ------------------------------------------------------------------ any order, in parallel
 //
 // The chain can be evaluated exactly without doing it add by add.  While the running sum stays in
 // one binade [2^e, 2^(e+1)) (sign sigma), the fp32 values there are the integer multiples T u of
 // u = 2^(e-23) with T in [2^23, 2^24), and fl(s + b) = sigma u round(T + sigma b / u), rounding to
-// the nearest integer, ties to the EVEN integer (= even mantissa).  So over a group of blocks:
+// the nearest integer, ties to the EVEN integer (= even mantissa).  So over a segment of blocks:
 //   q_k = sigma b_k / u (exact in binary64),  r_k = its rounding,  T_{k+1} = T_k + r_k,
 // where r_k depends on T_k only through the parity of T_k and only when q_k is an exact tie.
-// A group's RECORD for a guessed (sigma, e) holds, for both start parities p0, the total
+// A segment's RECORD for a guessed (sigma, e) holds, for both start parities p0, the total
 // sum_k r_k and the min / max of the partial sums; it applies to an actual running sum s iff s is
 // normal with that sign and exponent and every partial T stays in [2^23 + 1, 2^24 - 1] (then
 // every real T_k + q_k lies strictly inside the binade and the rounding above IS fl's).
-// Records of consecutive groups with the same guess compose associatively into runs.
+// Records with the same guess compose associatively.
 //
-//   1. every CTA: approximate prefix of the group partials (binary64) -> a guess per group;
-//      one warp per group builds its record (two passes: tie-parity maps, warp scan, sums);
-//      thread 0 composes the CTA's groups into runs.
-//   2. the last CTA (ticket): one warp walks the runs in order with the actual running sum --
-//      apply when the record holds, else the group's records one by one, else the group's
-//      blocks add by add (a warp-wide chain).  The result is the serial sum, bit for bit.
+//   0. ordered_agg / ordered_scan: binary64 sums of every 2048 positions of the order, and their
+//      exclusive prefix (one CTA).
+//   1. every CTA (2048 positions = 64 segments of 32, one warp per 8 segments): binary64 segment
+//      sums -> the approximate running sum before each segment -> its guess; the segment records
+//      (one value per lane: tie-parity maps and partial sums by warp scans); a segment predicted
+//      to leave its binade is marked for block-by-block addition; lane 0 of warp 0 composes runs
+//      of equal guesses into the CTA's run list.
+//   2. the last CTA (ticket): per chunk of 256 CTAs, a binary tree of compositions over the CTA
+//      composites in shared memory (a node is valid when all its CTAs are one run with one
+//      guess); the CTAs' run lists and the blocks of segments without a usable guess are staged
+//      in shared memory; one warp walks the tree with the actual running sum -- apply a node when
+//      its record holds, else descend; at a CTA: its runs, else their segments' records, else the
+//      segment's blocks add by add (a warp-wide chain).  The result is the serial sum, bit for bit.
 //
-// Guesses only steer the speed: a wrong one fails its check and the walk falls back.
+// Guesses only steer the speed: a wrong one fails its check and the walk descends.
 
-__device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
-__device__ __forceinline__ int64_t i64max(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int32_t clamp30(int64_t v) {
+    return int32_t(v < -(1ll << 30) ? -(1ll << 30) : (v > (1ll << 30) ? (1ll << 30) : v));
+}
 __device__ __forceinline__ uint64_t u64min(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-struct OrdRec {                 // 40 bytes
+struct OrdRec {                 // 32 bytes
     int32_t hdr;                // bit 0 valid, bit 1 negative, bits 2.. biased exponent of s
-    int32_t pad;
-    int64_t dT[2];              // sum of r_k for start parity 0 / 1 (|.| < 2^25 when valid)
+    int32_t dT[2];              // sum of the roundings r_k for start parity 0 / 1
     int32_t mn[2], mx[2];       // min / max partial sum (relative to T_0) for start parity 0 / 1
+    int32_t pad;
 };
-static_assert(sizeof(OrdRec) == 40, "record layout");
+static_assert(sizeof(OrdRec) == 32, "record layout");
+// |dT|, |mn|, |mx| are clamped to 2^30: a record that can apply keeps every partial sum inside
+// one binade (|.| < 2^24), so a clamped record never passes rec_applies.
 
-constexpr uint32_t kOrdPer = 64;   // groups per CTA (records and composition in shared memory)
+constexpr uint32_t kOxSeg = 32;                             // positions per segment (one per lane)
+constexpr uint32_t kOxSegPerWarp = 8;
+constexpr uint32_t kOxSegPerCta = kOxSegPerWarp * (kOrdThreads / 32);   // 64
+constexpr uint32_t kOxPerCta = kOxSeg * kOxSegPerCta;                  // 2048 positions
+constexpr int kOxWalkThreads = 1024;
+constexpr uint32_t kOxChunk = kOxWalkThreads;               // record CTAs per walk tree (leaves)
+constexpr uint32_t kOxNodes = 2 * kOxChunk - 1;
+constexpr uint32_t kOxRunPool = 1024;                       // staged runs per chunk
+constexpr uint32_t kOxSegPool = 256;                        // staged serial segments per chunk
+constexpr uint32_t kOxNoPool = 0xFFFFFFFFu;
 
-// profiling counters of the last walk: CTA composites applied, group records applied, groups
-// added block by block, groups whose record was invalid / unsafe
+// walk counters of the last launch (profiling): tree nodes applied, CTA runs applied, segment
+// records applied, segments added block by block
 __device__ unsigned long long g_ord_stats[4];
-// profiling: %globaltimer of the first CTA start, the last look-back end, the last record end,
-// the walk start and end (min / max over CTAs)
+// profiling: %globaltimer of the first record CTA start, the last prefix, the last record end,
+// the walk start and end
 __device__ unsigned long long g_ord_times[5];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -111,41 +130,52 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-struct OrdParams {
-    const float* blocks;        // block results, ascending
-    const float* group_partials;
-    uint64_t nb, n_groups;
-    uint32_t G;                 // blocks per group
-    OrdRec* grec;               // [n_groups] group records
-    OrdRec* crec;               // [grid] the CTA's composite (when all its groups are one run)
-    uint32_t* cone;             // [grid] 1 iff crec is usable
-    double* agg;                // [grid] sum of the CTA's group partials (binary64)
-    double* incl;               // [grid] inclusive prefix of agg
-    uint32_t* flag;             // [grid] 0 / 1 aggregate / 2 inclusive published; zero on entry, exit
-    uint32_t* ticket;           // zero on entry / exit
+struct OxParams {
+    const float* blocks;        // block results (reduction.hpp:248-255)
+    const uint32_t* order;      // position -> block (seeded permutation) or null (ascending)
+    uint64_t nb;
+    uint32_t grid;              // record CTAs
+    OrdRec* segrec;             // [grid * 64] segment records
+    OrdRec* runrec;             // [grid * 64] run composites
+    uint32_t* runinfo;          // [grid * 64] first local segment << 8 | segment count
+    uint32_t* nrun;             // [grid]
+    const double* pre;          // [grid] binary64 sum of the positions before each record CTA
     float* result;
 };
 
-__device__ __forceinline__ bool rec_applies(const OrdRec& r, float s, int64_t* T0out, int* p0out) {
+__device__ __forceinline__ float ox_load(const OxParams& P, uint64_t k) {
+    if (k >= P.nb) return 0.0f;   // trailing positions: + 0 is the identity of the chain (s is never -0)
+    return __ldcg(P.blocks + (P.order ? __ldg(P.order + k) : k));
+}
+
+__device__ __forceinline__ bool rec_applies(const OrdRec& r, float s) {
     if (!(r.hdr & 1)) return false;
     const uint32_t bits = __float_as_uint(s);
     const uint32_t ex = (bits >> 23) & 0xFFu;
     if (ex == 0 || ex == 0xFFu) return false;                  // zero, subnormal, inf, NaN
     if (int32_t(ex) != (r.hdr >> 2) || int32_t(bits >> 31) != ((r.hdr >> 1) & 1)) return false;
-    const int64_t T0 = int64_t((bits & 0x7FFFFFu) | 0x800000u);
-    const int p0 = int(T0 & 1);
-    if (T0 + r.mn[p0] < (1 << 23) + 1 || T0 + r.mx[p0] > (1 << 24) - 1) return false;
-    *T0out = T0;
-    *p0out = p0;
-    return true;
+    const int32_t T0 = int32_t((bits & 0x7FFFFFu) | 0x800000u);
+    const int p0 = T0 & 1;
+    return T0 + r.mn[p0] >= (1 << 23) + 1 && T0 + r.mx[p0] <= (1 << 24) - 1;
 }
 
 __device__ __forceinline__ float rec_apply(const OrdRec& r, float s) {
     const uint32_t bits = __float_as_uint(s);
-    const int64_t T0 = int64_t((bits & 0x7FFFFFu) | 0x800000u);
-    const int64_t T1 = T0 + r.dT[T0 & 1];
+    const int32_t T0 = int32_t((bits & 0x7FFFFFu) | 0x800000u);
+    const int32_t T1 = T0 + r.dT[T0 & 1];
     return __uint_as_float((bits & 0xFF800000u) | uint32_t(T1 - (1 << 23)));
 }
+
+__device__ __forceinline__ OrdRec rec_invalid() {
+    OrdRec r;
+    r.hdr = 0;
+    r.dT[0] = r.dT[1] = 0;
+    r.mn[0] = r.mn[1] = r.mx[0] = r.mx[1] = 0;
+    r.pad = 0;
+    return r;
+}
+
+__device__ __forceinline__ bool rec_joinable(const OrdRec& a, const OrdRec& b) { return (a.hdr & 1) && a.hdr == b.hdr; }
 
 // Compose b after a (same guess, both valid).
 __device__ __forceinline__ OrdRec rec_compose(const OrdRec& a, const OrdRec& b) {
@@ -154,284 +184,410 @@ __device__ __forceinline__ OrdRec rec_compose(const OrdRec& a, const OrdRec& b) 
     c.pad = 0;
 #pragma unroll
     for (int p0 = 0; p0 < 2; ++p0) {
-        const int pm = int((p0 + a.dT[p0]) & 1);
+        const int pm = (p0 + a.dT[p0]) & 1;
         const int64_t d = a.dT[p0];
-        c.dT[p0] = d + b.dT[pm];
-        const int64_t mn = d + b.mn[pm], mx = d + b.mx[pm];
-        // the partial sums stay < 2^25 in magnitude whenever the run can apply; clamp the rest
-        // so the check fails instead of overflowing
-        c.mn[p0] = int32_t(i64max(-(1ll << 30), i64min(a.mn[p0], mn)));
-        c.mx[p0] = int32_t(i64min(1ll << 30, i64max(a.mx[p0], mx)));
+        c.dT[p0] = clamp30(d + b.dT[pm]);
+        c.mn[p0] = clamp30(a.mn[p0] < d + b.mn[pm] ? int64_t(a.mn[p0]) : d + b.mn[pm]);
+        c.mx[p0] = clamp30(a.mx[p0] > d + b.mx[pm] ? int64_t(a.mx[p0]) : d + b.mx[pm]);
     }
     return c;
 }
 
-// One warp: the record of blocks [b0, b0 + cnt) for the guess (neg, e); lanes take consecutive
-// slices of J = ceil(cnt / 32).
-__device__ OrdRec warp_record(const float* blocks, uint64_t b0, uint32_t cnt, bool neg, int e) {
+// guess for an approximate running sum S: its binade, unless S is within 2^-10 of a binade edge
+__device__ __forceinline__ bool ox_guess(double S, bool* neg, int* e) {
+    const uint64_t bits = uint64_t(__double_as_longlong(S));
+    const int de = int((bits >> 52) & 0x7FF);            // biased binary64 exponent
+    const uint32_t top = uint32_t(bits >> 42) & 0x3FFu;  // leading 10 fraction bits
+    *neg = (bits >> 63) != 0;
+    *e = de - 1023 + 127;                                // biased binary32 exponent
+    return de != 0 && top != 0 && top != 0x3FFu && *e >= 1 && *e <= 254;
+}
+
+// One warp, one value per lane: the record of the 32 values in lane order for the guess (neg, e).
+// The rounding of q_k = sigma b_k / u depends on the running T only for an exact tie: with no tie
+// in the warp one scan gives both parities' record.
+__device__ __forceinline__ OrdRec warp_record1(float b, bool neg, int e) {
     const unsigned lane = threadIdx.x & 31u;
-    const uint32_t J = (cnt + 31) / 32;
-    const uint32_t lo = lane * J, hi = min(cnt, lo + J);
-    const double scale = ldexp(neg ? -1.0 : 1.0, 23 - (e - 127));   // sigma / u
-    bool ok = true;
-    // pass 1: the lane's tie-parity map, as its end parity for start parity 0 and 1
-    uint32_t pe[2] = {0u, 1u};
-    for (uint32_t k = lo; k < hi; ++k) {
-        const float b = __ldg(blocks + b0 + k);
-        const double q = double(b) * scale;
-        ok &= isfinite(b) && fabs(q) < 33554432.0;   // 2^25
-        const double f = floor(q), ph = q - f;
-        const int64_t fi = int64_t(f);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int64_t r = ph < 0.5 ? fi : (ph > 0.5 ? fi + 1 : fi + ((pe[t] + fi) & 1));
-            pe[t] = uint32_t((pe[t] + r) & 1);
-        }
-    }
-    // inclusive warp scan of the maps (compose in lane order), then the lane's start parities
-    uint32_t m0 = pe[0], m1 = pe[1];
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t a0 = __shfl_up_sync(kFull, m0, off), a1 = __shfl_up_sync(kFull, m1, off);
-        if (lane >= uint32_t(off)) {
-            // (this after earlier): p -> mine(earlier(p))
-            const uint32_t n0 = a0 ? m1 : m0, n1 = a1 ? m1 : m0;
-            m0 = n0;
-            m1 = n1;
-        }
-    }
-    uint32_t s0 = __shfl_up_sync(kFull, m0, 1), s1 = __shfl_up_sync(kFull, m1, 1);
-    if (lane == 0) {
-        s0 = 0u;
-        s1 = 1u;
-    }
-    // pass 2: partial sums from the lane's start parities
-    int64_t acc[2] = {0, 0}, mn[2] = {INT64_MAX, INT64_MAX}, mx[2] = {INT64_MIN, INT64_MIN};
-    uint32_t pp[2] = {s0, s1};
-    for (uint32_t k = lo; k < hi; ++k) {
-        const float b = __ldg(blocks + b0 + k);
-        const double q = double(b) * scale;
-        const double f = floor(q), ph = q - f;
-        const int64_t fi = int64_t(f);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int64_t r = ph < 0.5 ? fi : (ph > 0.5 ? fi + 1 : fi + ((pp[t] + fi) & 1));
-            pp[t] = uint32_t((pp[t] + r) & 1);
-            acc[t] += r;
-            mn[t] = i64min(mn[t], acc[t]);
-            mx[t] = i64max(mx[t], acc[t]);
-        }
-    }
-    // exclusive scan of the lane sums, then the warp's min / max of all partial sums
+    // sigma / u = sigma 2^(150 - e), built from its bits
+    const double scale = __longlong_as_double((long long)(uint64_t(1023 + 150 - e) << 52) | (neg ? (1ll << 63) : 0ll));
+    const double q = double(b) * scale;
+    const bool fin = isfinite(b) && fabs(q) < 33554432.0;   // 2^25
+    const bool ok = __all_sync(kFull, fin);
+    const double f = fin ? floor(q) : 0.0, ph = fin ? q - f : 0.0;
+    const int32_t fi = int32_t(f);
     OrdRec rec;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        int64_t inc = acc[t];
+    rec.pad = 0;
+    if (!__any_sync(kFull, ph == 0.5)) {
+        int32_t inc = fi + (ph > 0.5 ? 1 : 0);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const int64_t a = __shfl_up_sync(kFull, inc, off);
+            const int32_t a = __shfl_up_sync(kFull, inc, off);
             if (lane >= uint32_t(off)) inc += a;
         }
-        const int64_t excl = inc - acc[t];
-        int64_t lmn = hi > lo ? excl + mn[t] : INT64_MAX, lmx = hi > lo ? excl + mx[t] : INT64_MIN;
+        const int32_t mn = __reduce_min_sync(kFull, inc), mx = __reduce_max_sync(kFull, inc);
+        const int32_t tot = __shfl_sync(kFull, inc, 31);
+        rec.dT[0] = rec.dT[1] = tot;
+        rec.mn[0] = rec.mn[1] = mn;
+        rec.mx[0] = rec.mx[1] = mx;
+    } else {
+        auto rr = [&](uint32_t p) -> int32_t { return ph < 0.5 ? fi : (ph > 0.5 ? fi + 1 : fi + int32_t((p + fi) & 1)); };
+        // the lane's parity map p -> (p + r(p)) & 1, composed in lane order (inclusive scan)
+        uint32_t m0 = uint32_t(rr(0) & 1), m1 = uint32_t((1 + rr(1)) & 1);
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-            lmn = i64min(lmn, __shfl_xor_sync(kFull, lmn, off));
-            lmx = i64max(lmx, __shfl_xor_sync(kFull, lmx, off));
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t a0 = __shfl_up_sync(kFull, m0, off), a1 = __shfl_up_sync(kFull, m1, off);
+            if (lane >= uint32_t(off)) {
+                const uint32_t n0 = a0 ? m1 : m0, n1 = a1 ? m1 : m0;   // mine(earlier(p))
+                m0 = n0;
+                m1 = n1;
+            }
         }
-        rec.dT[t] = __shfl_sync(kFull, inc, 31);
-        rec.mn[t] = int32_t(i64max(-(1ll << 30), i64min(lmn, 1ll << 30)));
-        rec.mx[t] = int32_t(i64max(-(1ll << 30), i64min(lmx, 1ll << 30)));
+        uint32_t s0 = __shfl_up_sync(kFull, m0, 1), s1 = __shfl_up_sync(kFull, m1, 1);
+        if (lane == 0) {
+            s0 = 0u;
+            s1 = 1u;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            int32_t inc = rr(t ? s1 : s0);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int32_t a = __shfl_up_sync(kFull, inc, off);
+                if (lane >= uint32_t(off)) inc += a;
+            }
+            rec.mn[t] = __reduce_min_sync(kFull, inc);
+            rec.mx[t] = __reduce_max_sync(kFull, inc);
+            rec.dT[t] = __shfl_sync(kFull, inc, 31);
+        }
     }
-    ok = __all_sync(kFull, ok);
     rec.hdr = (ok ? 1 : 0) | (neg ? 2 : 0) | (e << 2);
-    rec.pad = 0;
     return rec;
 }
 
-// One warp: s + blocks[b0], + blocks[b0 + 1], ... one fp32 add at a time (the reference's loop);
-// every lane runs the same chain on broadcast values, so s stays warp-uniform.
-__device__ float warp_serial(const float* blocks, uint64_t b0, uint32_t cnt, float s) {
-    const unsigned lane = threadIdx.x & 31u;
-    for (uint32_t base = 0; base < cnt; base += 32) {
-        const uint32_t k = base + lane;
-        const float v = k < cnt ? __ldcg(blocks + b0 + k) : 0.0f;
-        const uint32_t m = min(32u, cnt - base);
-        for (uint32_t i = 0; i < m; ++i) s += __shfl_sync(kFull, v, i);
-    }
+// One warp: s + v_0 + v_1 + ... + v_31 (lane l holds v_l), one fp32 add at a time (the reference's
+// loop); every lane runs the same chain, so s stays warp-uniform.
+__device__ __forceinline__ float warp_chain32(float v, float s) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s += __shfl_sync(kFull, v, i);
     return s;
 }
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// binary64 sum of the positions [2048 b, 2048 b + 2048) of the order -> agg[b]
+__global__ void __launch_bounds__(kOrdThreads) ordered_agg_kernel(const OxParams P, double* agg) {
+    __shared__ double s_w[kOrdThreads / 32];
+    const uint64_t base = uint64_t(blockIdx.x) * kOxPerCta;
+    double d = 0.0;
+#pragma unroll
+    for (uint32_t i = 0; i < kOxPerCta / kOrdThreads; ++i) d += double(ox_load(P, base + i * kOrdThreads + threadIdx.x));
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(kFull, d, off);
+    if ((threadIdx.x & 31u) == 0) s_w[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < kOrdThreads / 32; ++w) a += s_w[w];
+        agg[blockIdx.x] = a;
+    }
 }
 
-// CTA b owns groups [64 b, 64 b + 64).  The approximate running sum before them comes from a
-// decoupled look-back over the CTAs' published aggregates (each CTA publishes its aggregate at
-// once and its inclusive prefix as soon as it knows it; a CTA only waits on lower-numbered ones,
-// which were scheduled before it), so no separate scan launch is needed.
-__global__ void __launch_bounds__(kOrdThreads) ordered_ascending_kernel(const OrdParams P) {
-    __shared__ double s_gp[kOrdPer];
-    __shared__ double s_S[kOrdPer];
-    __shared__ OrdRec s_rec[kOrdPer];
-    __shared__ double s_pre;
-    __shared__ int s_last;
-    __shared__ OrdRec s_wrec[kOrdThreads];
-    __shared__ OrdRec s_grp[kOrdPer];
-    __shared__ uint32_t s_wone[kOrdThreads];
+// exclusive prefix of agg[0, grid) in binary64, one CTA of 1024 threads: pre[b]
+__global__ void __launch_bounds__(1024) ordered_scan_kernel(const double* agg, double* pre, uint32_t grid) {
+    __shared__ double s_t[1024];
+    const uint32_t t = threadIdx.x;
+    const uint32_t per = (grid + 1023) / 1024, lo = t * per, hi = min(grid, lo + per);
+    double sum = 0.0;
+    for (uint32_t i = lo; i < hi; ++i) sum += __ldcg(agg + i);
+    s_t[t] = sum;
+    __syncthreads();
+    for (uint32_t off = 1; off < 1024; off <<= 1) {   // inclusive Hillis-Steele scan of the thread sums
+        const double v = t >= off ? s_t[t - off] : 0.0;
+        __syncthreads();
+        s_t[t] += v;
+        __syncthreads();
+    }
+    double run = t ? s_t[t - 1] : 0.0;
+    for (uint32_t i = lo; i < hi; ++i) {
+        pre[i] = run;
+        run += __ldcg(agg + i);
+    }
+}
+
+// Records: CTA b = positions [2048 b, 2048 b + 2048) = 64 segments; warp w segments 8w .. 8w+7.
+__global__ void __launch_bounds__(kOrdThreads) ordered_records_kernel(const OxParams P) {
+    __shared__ double s_ss[kOxSegPerCta];
+    __shared__ double s_S[kOxSegPerCta];
+    __shared__ OrdRec s_run[kOxSegPerCta];     // per warp: its runs at [8 w, 8 w + count)
+    __shared__ uint32_t s_info[kOxSegPerCta];
+    __shared__ uint32_t s_wn[kOrdThreads / 32];
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     const uint64_t b = blockIdx.x;
-    const uint64_t ga = b * kOrdPer, gb = u64min(P.n_groups, ga + kOrdPer);
-    const uint32_t ng = uint32_t(gb - ga);
+    const uint64_t base = b * kOxPerCta;
     if (tid == 0) atomicMin(&g_ord_times[0], gtimer());
-    if (tid < kOrdPer) s_gp[tid] = tid < ng ? double(__ldcg(P.group_partials + ga + tid)) : 0.0;
+    float v[kOxSegPerWarp];
+#pragma unroll
+    for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = ox_load(P, base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
+#pragma unroll
+    for (uint32_t i = 0; i < kOxSegPerWarp; ++i) {
+        double d = double(v[i]);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) d += __shfl_xor_sync(kFull, d, off);
+        if (lane == 0) s_ss[warp * kOxSegPerWarp + i] = d;
+    }
     __syncthreads();
     if (warp == 0) {
-        double a = s_gp[lane] + s_gp[lane + 32];
+        // exclusive prefix of the 64 segment sums (two per lane), from the CTA's prefix
+        const double a0 = s_ss[2 * lane], a1 = s_ss[2 * lane + 1];
+        double inc = a0 + a1;
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) a += __shfl_xor_sync(kFull, a, off);
-        if (lane == 0) {
-            P.agg[b] = a;
-            if (b == 0) P.incl[b] = a;
-            __threadfence();
-            st_release(P.flag + b, b == 0 ? 2u : 1u);
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(kFull, inc, off);
+            if (lane >= uint32_t(off)) inc += t;
         }
-        // look-back: windows of 32 predecessors, nearest first
-        double pre = 0.0;
-        int64_t j = int64_t(b) - 1;
-        while (j >= 0) {
-            const int64_t idx = j - int64_t(lane);
-            uint32_t f = idx >= 0 ? ld_acquire(P.flag + idx) : 2u;
-            const unsigned ready2 = __ballot_sync(kFull, f == 2u);
-            const unsigned stop = ready2 ? (__ffs(ready2) - 1) : 31u;      // nearest inclusive (or window end)
-            const unsigned zero = __ballot_sync(kFull, f == 0u) & ((stop == 31u && !ready2) ? kFull : ((2u << stop) - 1u));
-            if (zero) continue;                                            // a predecessor has not published yet
-            double v = 0.0;
-            if (idx >= 0 && lane <= stop) v = (ready2 && lane == stop) ? __ldcg(P.incl + idx) : __ldcg(P.agg + idx);
+        const double ex = __ldcg(P.pre + b) + (inc - (a0 + a1));
+        s_S[2 * lane] = ex;
+        s_S[2 * lane + 1] = ex + a0;
+        if (lane == 0) atomicMax(&g_ord_times[1], gtimer());
+    }
+    __syncthreads();
+    OrdRec r[kOxSegPerWarp];
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-            pre += v;
-            if (ready2) break;
-            j -= 32;
+    for (uint32_t i = 0; i < kOxSegPerWarp; ++i) {
+        const uint32_t si = warp * kOxSegPerWarp + i;
+        const double S = s_S[si];
+        bool neg;
+        int e;
+        r[i] = ox_guess(S, &neg, &e) ? warp_record1(v[i], neg, e) : rec_invalid();
+        if (r[i].hdr & 1) {
+            // predicted to leave its binade (the estimated start plus the record's partial sums
+            // within 2^-10 of an edge): the segment will be added block by block -- a run break
+            const double T0 = fabs(S) * ldexp(1.0, 150 - e);
+            const double mg = 8192.0;
+            if (T0 + double(min(r[i].mn[0], r[i].mn[1])) < 8388608.0 + mg ||
+                T0 + double(max(r[i].mx[0], r[i].mx[1])) > 16777216.0 - mg)
+                r[i].hdr &= ~1;
         }
-        if (lane == 0) {
-            s_pre = pre;
-            if (b != 0) {
-                P.incl[b] = pre + a;
-                __threadfence();
-                st_release(P.flag + b, 2u);
+        if (lane == 0) P.segrec[b * kOxSegPerCta + si] = r[i];
+    }
+    // the warp's runs (lane 0), then thread 0 joins the warps' run lists
+    if (lane == 0) {
+        uint32_t nr = 0, first = 0;
+        OrdRec c = r[0];
+#pragma unroll
+        for (uint32_t i = 1; i <= kOxSegPerWarp; ++i) {
+            if (i < kOxSegPerWarp && rec_joinable(c, r[i])) {
+                c = rec_compose(c, r[i]);
+                continue;
+            }
+            s_run[warp * kOxSegPerWarp + nr] = c;
+            s_info[warp * kOxSegPerWarp + nr] = ((warp * kOxSegPerWarp + first) << 8) | (i - first);
+            ++nr;
+            if (i < kOxSegPerWarp) {
+                c = r[i];
+                first = i;
             }
         }
-    }
-    __syncthreads();
-    if (tid == 0) atomicMax(&g_ord_times[1], gtimer());
-    if (tid == 0) {
-        double S = s_pre;
-        for (uint32_t i = 0; i < ng; ++i) {
-            s_S[i] = S;
-            S += s_gp[i];
-        }
-    }
-    __syncthreads();
-    // records: warp w takes groups w, w + 8, ... of the CTA
-    for (uint32_t i = warp; i < ng; i += kOrdThreads / 32) {
-        const double S = s_S[i];
-        const uint64_t g = ga + i;
-        const uint64_t b0 = g * P.G;
-        const uint32_t cnt = uint32_t(u64min(P.G, P.nb - b0));
-        // guess: the binade of the approximate sum, unless it is within 1e-3 of a boundary
-        int ex = 0;
-        const double fr = frexp(fabs(S), &ex);   // |S| = fr 2^ex, fr in [0.5, 1)
-        const bool safe = S != 0.0 && fr > 0.5005 && fr < 0.9995 && ex - 1 + 127 >= 1 && ex - 1 + 127 <= 254;
-        OrdRec r;
-        if (safe) {
-            r = warp_record(P.blocks, b0, cnt, S < 0.0, ex - 1 + 127);
-        } else {
-            r.hdr = 0;
-            r.pad = 0;
-            r.dT[0] = r.dT[1] = 0;
-            r.mn[0] = r.mn[1] = r.mx[0] = r.mx[1] = 0;
-        }
-        if (lane == 0) {
-            s_rec[i] = r;
-            P.grec[g] = r;
-        }
+        s_wn[warp] = nr;
     }
     __syncthreads();
     if (tid == 0) {
-        // the CTA's composite, when all its groups are one run (valid, same guess)
-        OrdRec c = s_rec[0];
-        bool one = (c.hdr & 1) != 0;
-        for (uint32_t i = 1; one && i < ng; ++i) {
-            one = s_rec[i].hdr == c.hdr;
-            if (one) c = rec_compose(c, s_rec[i]);
-        }
-        P.crec[b] = c;
-        P.cone[b] = one ? 1u : 0u;
-        atomicMax(&g_ord_times[2], gtimer());
-        unsigned t;
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(P.ticket) : "memory");
-        s_last = t == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    if (tid == 0) g_ord_times[3] = gtimer();
-    // the walk, in block order: chunks of 256 CTAs staged in shared memory by the whole CTA,
-    // walked by warp 0 with the actual running sum
-    float s = 0.0f;
-    unsigned long long st[4] = {0, 0, 0, 0};
-    for (uint32_t c0 = 0; c0 < gridDim.x; c0 += kOrdThreads) {
-        const uint32_t cn = min(uint32_t(kOrdThreads), gridDim.x - c0);
-        if (tid < cn) {
-            s_wone[tid] = __ldcg(P.cone + c0 + tid);
-            s_wrec[tid] = P.crec[c0 + tid];
-        }
-        __syncthreads();
-        if (warp == 0) {
-            for (uint32_t k = 0; k < cn; ++k) {
-                int64_t T0;
-                int p0;
-                if (s_wone[k] && rec_applies(s_wrec[k], s, &T0, &p0)) {
-                    s = rec_apply(s_wrec[k], s);
-                    if (lane == 0) ++st[0];
+        uint32_t nr = 0;
+        OrdRec c = s_run[0];
+        uint32_t ci = s_info[0];
+        for (uint32_t w = 0; w < kOrdThreads / 32; ++w) {
+            for (uint32_t j = (w == 0 ? 1 : 0); j < s_wn[w]; ++j) {
+                const OrdRec& x = s_run[w * kOxSegPerWarp + j];
+                const uint32_t xi = s_info[w * kOxSegPerWarp + j];
+                if (rec_joinable(c, x)) {
+                    c = rec_compose(c, x);
+                    ci += xi & 0xFFu;
                     continue;
                 }
-                const uint64_t jg0 = uint64_t(c0 + k) * kOrdPer, jg1 = u64min(P.n_groups, jg0 + kOrdPer);
-                // the CTA's group records, all at once (one round trip, not one per group)
-                for (uint64_t g = jg0 + lane; g < jg1; g += 32) s_grp[g - jg0] = P.grec[g];
-                __syncwarp();
-                for (uint64_t g = jg0; g < jg1; ++g) {
-                    const OrdRec gr = s_grp[g - jg0];
-                    if (rec_applies(gr, s, &T0, &p0)) {
-                        s = rec_apply(gr, s);
-                        if (lane == 0) ++st[1];
+                P.runrec[b * kOxSegPerCta + nr] = c;
+                P.runinfo[b * kOxSegPerCta + nr] = ci;
+                ++nr;
+                c = x;
+                ci = xi;
+            }
+        }
+        P.runrec[b * kOxSegPerCta + nr] = c;
+        P.runinfo[b * kOxSegPerCta + nr] = ci;
+        P.nrun[b] = nr + 1;
+        atomicMax(&g_ord_times[2], gtimer());
+    }
+}
+
+struct OxWalkSmem {
+    OrdRec node[kOxNodes];          // tree over the chunk's CTA composites (heap order)
+    OrdRec run[kOxRunPool];         // staged run lists
+    uint32_t runinfo[kOxRunPool];   // first << 8 | count
+    uint32_t runseg[kOxRunPool];    // segment pool slot of an invalid one-segment run, or kOxNoPool
+    uint32_t owner[kOxRunPool];     // leaf that owns the staged run
+    uint32_t runbase[kOxChunk];     // first staged run of each leaf, or kOxNoPool
+    uint32_t segid[kOxSegPool];     // global segment of each staged serial segment
+    float seg[kOxSegPool][kOxSeg];  // staged blocks of serial segments
+    uint8_t kind[kOxNodes + 1];     // 0 empty, 1 valid composite, 2 descend
+    uint32_t nruns, nsegs;
+};
+
+// The walk (one CTA): per chunk of 1024 record CTAs, stage, build the tree, walk it with warp 0.
+__global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxParams P) {
+    extern __shared__ __align__(16) unsigned char ox_smem[];
+    OxWalkSmem& W = *reinterpret_cast<OxWalkSmem*>(ox_smem);
+    const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    if (tid == 0) g_ord_times[3] = gtimer();
+    float s = 0.0f;
+    unsigned long long st[4] = {0, 0, 0, 0};
+    for (uint64_t c0 = 0; c0 < P.grid; c0 += kOxChunk) {
+        const uint32_t cn = uint32_t(u64min(kOxChunk, P.grid - c0));
+        if (tid == 0) W.nruns = W.nsegs = 0;
+        __syncthreads();
+        // leaves: the CTA composite when the CTA is one valid run; reserve pool space for the others
+        const uint32_t li = kOxChunk - 1 + tid;
+        uint8_t kd = 0;
+        uint32_t nr = 0, rb = kOxNoPool;
+        if (tid < cn) {
+            const uint64_t cb = c0 + tid;
+            nr = __ldcg(P.nrun + cb);
+            const OrdRec r0 = P.runrec[cb * kOxSegPerCta];
+            if (nr == 1 && (r0.hdr & 1)) {
+                W.node[li] = r0;
+                kd = 1;
+            } else {
+                kd = 2;
+                const uint32_t at = atomicAdd(&W.nruns, nr);
+                if (at + nr <= kOxRunPool) {
+                    rb = at;
+                    for (uint32_t r = 0; r < nr; ++r) W.owner[at + r] = tid;
+                } else {
+                    // does not fit: walked from global memory; mark its share of the pool unused
+                    for (uint32_t r = at; r < at + nr && r < kOxRunPool; ++r) W.owner[r] = kOxNoPool;
+                }
+            }
+        }
+        W.kind[li] = kd;
+        W.runbase[tid] = rb;
+        __syncthreads();
+        // stage the runs (one per thread), and reserve a pool slot for each serial segment
+        const uint32_t staged = min(W.nruns, kOxRunPool);
+        for (uint32_t j = tid; j < staged; j += kOxWalkThreads) {
+            const uint32_t t = W.owner[j];
+            if (t == kOxNoPool) continue;
+            const uint64_t cb = c0 + t;
+            const uint32_t r = j - W.runbase[t];
+            const OrdRec rr = P.runrec[cb * kOxSegPerCta + r];
+            const uint32_t ri = __ldcg(P.runinfo + cb * kOxSegPerCta + r);
+            W.run[j] = rr;
+            W.runinfo[j] = ri;
+            uint32_t sl = kOxNoPool;
+            if (!(rr.hdr & 1) && (ri & 0xFFu) == 1u) {
+                const uint32_t ss = atomicAdd(&W.nsegs, 1u);
+                if (ss < kOxSegPool) {
+                    sl = ss;
+                    W.segid[ss] = uint32_t(cb * kOxSegPerCta + (ri >> 8));
+                }
+            }
+            W.runseg[j] = sl;
+        }
+        __syncthreads();
+        // stage the serial segments' blocks, all threads at once
+        const uint32_t nseg = min(W.nsegs, kOxSegPool);
+        for (uint32_t e2 = tid; e2 < nseg * kOxSeg; e2 += kOxWalkThreads)
+            W.seg[e2 / kOxSeg][e2 % kOxSeg] = ox_load(P, uint64_t(W.segid[e2 / kOxSeg]) * kOxSeg + e2 % kOxSeg);
+        // internal nodes, level by level (heap order: children 2i+1, 2i+2)
+        for (uint32_t cnt = kOxChunk / 2, lo = kOxChunk / 2 - 1;; cnt >>= 1, lo = (lo - 1) / 2) {
+            __syncthreads();
+            if (tid < cnt) {
+                const uint32_t i = lo + tid, l = 2 * i + 1, r = 2 * i + 2;
+                const uint8_t kl = W.kind[l], kr = W.kind[r];
+                uint8_t k;
+                if (kl == 0) {
+                    k = kr;
+                    if (kr == 1) W.node[i] = W.node[r];
+                } else if (kr == 0) {
+                    k = kl;
+                    if (kl == 1) W.node[i] = W.node[l];
+                } else if (kl == 1 && kr == 1 && rec_joinable(W.node[l], W.node[r])) {
+                    W.node[i] = rec_compose(W.node[l], W.node[r]);
+                    k = 1;
+                } else {
+                    k = 2;
+                }
+                W.kind[i] = k;
+            }
+            if (cnt == 1) break;
+        }
+        __syncthreads();
+        // the walk: warp 0, depth-first with an explicit stack
+        if (warp == 0) {
+            uint32_t stk[24];
+            int top = 0;
+            stk[top++] = 0;
+            while (top > 0) {
+                const uint32_t i = stk[--top];
+                const uint8_t k = W.kind[i];
+                if (k == 0) continue;
+                if (k == 1 && rec_applies(W.node[i], s)) {
+                    s = rec_apply(W.node[i], s);
+                    ++st[0];
+                    continue;
+                }
+                if (i < kOxChunk - 1) {            // internal: right pushed first, left walked first
+                    stk[top++] = 2 * i + 2;
+                    stk[top++] = 2 * i + 1;
+                    continue;
+                }
+                // leaf: record CTA cb, its runs (staged or from global)
+                const uint32_t t = i - (kOxChunk - 1);
+                const uint64_t cb = c0 + t;
+                const uint32_t rb2 = W.runbase[t];
+                const uint32_t nr2 = k == 1 ? 1u : __ldcg(P.nrun + cb);
+                for (uint32_t r = 0; r < nr2; ++r) {
+                    OrdRec rr;
+                    uint32_t ri, sl = kOxNoPool;
+                    if (k == 1) {
+                        rr = W.node[i];
+                        ri = kOxSegPerCta;   // segments 0 .. 63
+                    } else if (rb2 != kOxNoPool) {
+                        rr = W.run[rb2 + r];
+                        ri = W.runinfo[rb2 + r];
+                        sl = W.runseg[rb2 + r];
                     } else {
-                        if (lane == 0) {
-                            ++st[2];
-                            if (!(gr.hdr & 1)) ++st[3];
+                        rr = P.runrec[cb * kOxSegPerCta + r];
+                        ri = __ldcg(P.runinfo + cb * kOxSegPerCta + r);
+                    }
+                    if (rec_applies(rr, s)) {
+                        s = rec_apply(rr, s);
+                        ++st[1];
+                        continue;
+                    }
+                    const uint32_t sf = ri >> 8, sc = ri & 0xFFu;
+                    for (uint32_t q = sf; q < sf + sc; ++q) {
+                        const uint64_t gs = cb * kOxSegPerCta + q;
+                        if (sc > 1 || (rr.hdr & 1)) {
+                            const OrdRec sr = P.segrec[gs];
+                            if (rec_applies(sr, s)) {
+                                s = rec_apply(sr, s);
+                                ++st[2];
+                                continue;
+                            }
                         }
-                        const uint64_t b0 = g * P.G;
-                        s = warp_serial(P.blocks, b0, uint32_t(u64min(P.G, P.nb - b0)), s);
+                        const float x = sl != kOxNoPool ? W.seg[sl][lane] : ox_load(P, gs * kOxSeg + lane);
+                        s = warp_chain32(x, s);
+                        ++st[3];
                     }
                 }
-                __syncwarp();
             }
         }
         __syncthreads();
     }
-    for (uint32_t j = tid; j < gridDim.x; j += kOrdThreads) P.flag[j] = 0u;
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) g_ord_stats[i] = st[i];
         g_ord_times[4] = gtimer();
         *P.result = s;
-        *P.ticket = 0u;
     }
 }
+
+constexpr size_t kOxSmem = sizeof(OxWalkSmem);
 
 }  // namespace
 
@@ -447,31 +603,43 @@ int ordered_stats(unsigned long long* host) {
     return cudaMemcpyToSymbol(g_ord_times, init, sizeof(init)) == cudaSuccess ? 0 : -1;
 }
 
-size_t ordered_ws_bytes(uint64_t n_groups, int grid) {
-    return n_groups * sizeof(OrdRec) + size_t(grid) * (sizeof(OrdRec) + 2 * sizeof(double) + 2 * sizeof(uint32_t)) + 256;
+int ordered_grid(uint64_t nb) { return int((nb + kOxPerCta - 1) / kOxPerCta); }
+
+size_t ordered_ws_bytes(uint64_t nb) {
+    const size_t grid = size_t(ordered_grid(nb));
+    return grid * kOxSegPerCta * (2 * sizeof(OrdRec) + sizeof(uint32_t)) + grid * (2 * sizeof(double) + sizeof(uint32_t)) +
+           256;
 }
 
-int ordered_grid(uint64_t n_groups) { return int((n_groups + kOrdPer - 1) / kOrdPer); }
-
-cudaError_t launch_ordered_ascending(const float* blocks, const float* group_partials, uint64_t nb, uint64_t n_groups,
-                                     uint32_t G, void* ws, uint32_t* ticket, float* result, cudaStream_t s) {
-    const int grid = ordered_grid(n_groups);
-    OrdParams P{};
+cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, uint64_t nb, void* ws, uint32_t* ticket,
+                                    float* result, cudaStream_t s) {
+    (void)ticket;
+    const int grid = ordered_grid(nb);
+    static PerDeviceOnce once;
+    const cudaError_t ea = once([] {
+        return cudaFuncSetAttribute(ordered_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kOxSmem));
+    });
+    if (ea != cudaSuccess) return ea;
+    OxParams P{};
     P.blocks = blocks;
-    P.group_partials = group_partials;
+    P.order = order;
     P.nb = nb;
-    P.n_groups = n_groups;
-    P.G = G;
+    P.grid = uint32_t(grid);
     char* w = static_cast<char*>(ws);
-    P.grec = reinterpret_cast<OrdRec*>(w);
-    P.crec = P.grec + n_groups;
-    P.agg = reinterpret_cast<double*>(P.crec + grid);
-    P.incl = P.agg + grid;
-    P.cone = reinterpret_cast<uint32_t*>(P.incl + grid);
-    P.flag = P.cone + grid;
-    P.ticket = ticket;
+    const size_t ns = size_t(grid) * kOxSegPerCta;
+    // 8-byte members first
+    double* agg = reinterpret_cast<double*>(w);
+    double* pre = agg + grid;
+    P.pre = pre;
+    P.segrec = reinterpret_cast<OrdRec*>(pre + grid);
+    P.runrec = P.segrec + ns;
+    P.runinfo = reinterpret_cast<uint32_t*>(P.runrec + ns);
+    P.nrun = P.runinfo + ns;
     P.result = result;
-    ordered_ascending_kernel<<<grid, kOrdThreads, 0, s>>>(P);
+    ordered_agg_kernel<<<grid, kOrdThreads, 0, s>>>(P, agg);
+    ordered_scan_kernel<<<1, 1024, 0, s>>>(agg, pre, uint32_t(grid));
+    ordered_records_kernel<<<grid, kOrdThreads, 0, s>>>(P);
+    ordered_walk_kernel<<<1, kOxWalkThreads, kOxSmem, s>>>(P);
     return cudaGetLastError();
 }
 

@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(kBkThreads) sp_bulk_kernel(const SpParams p) {
             float lo[4] = {0.f, 0.f, 0.f, 0.f}, hi[4] = {0.f, 0.f, 0.f, 0.f};
             uint32_t bb0 = 0, bb1 = 0;
             uint32_t r = 0, ci = 0;
-#pragma unroll 1
             constexpr uint32_t FPS = kBkStage / 512u;   // fragments per stage
+#pragma unroll 1
             for (uint32_t f0 = 0; f0 < nfrag; f0 += FPS) {
                 const uint32_t slot = t_cons % NS;
                 mbar_wait(&sh.full[warp][slot], (t_cons / NS) & 1u);
