@@ -65,6 +65,11 @@ __device__ __forceinline__ bool h_overflowed(uint16_t h) { return (h & 0x7C00u) 
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: let a successor launched with programmatic stream serialization
+// (the ORDERED finaliser chain) be scheduled now; it waits for this grid in-kernel
+// (griddepcontrol.wait).  A no-op for ordinary successors.
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // SplitMix64 k-th draw, k >= 1 (rng.hpp:13-18 with the state jumped ahead by k*gamma).
 __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
     uint64_t z = seed + k * 0x9E3779B97F4A7C15ull;

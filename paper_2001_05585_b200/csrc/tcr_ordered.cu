@@ -8,6 +8,7 @@
 // waits on an L2 load.  (The order itself is computed once on the host per (blocks, seed) and
 // cached in the workspace -- tcr_capi.cpp.)
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "tcr_device.cuh"
@@ -117,6 +118,7 @@ constexpr uint32_t kOxNodes = 2 * kOxChunk - 1;
 constexpr uint32_t kOxRunPool = 1024;                       // staged runs per chunk
 constexpr uint32_t kOxSegPool = 256;                        // staged serial segments per chunk
 constexpr uint32_t kOxNoPool = 0xFFFFFFFFu;
+constexpr double kOxMargin = 512.0;                         // units of the binade's ulp
 
 // walk counters of the last launch (profiling): tree nodes applied, CTA runs applied, segment
 // records applied, segments added block by block
@@ -141,6 +143,7 @@ struct OxParams {
     uint32_t* nrun;             // [grid]
     const double* pre;          // [grid] binary64 sum of the positions before each record CTA
     float* result;
+    int dbg;                    // profiling (debug_mode 41): per-chunk phase times via printf
 };
 
 __device__ __forceinline__ float ox_load(const OxParams& P, uint64_t k) {
@@ -193,14 +196,13 @@ __device__ __forceinline__ OrdRec rec_compose(const OrdRec& a, const OrdRec& b) 
     return c;
 }
 
-// guess for an approximate running sum S: its binade, unless S is within 2^-10 of a binade edge
+// guess for an approximate running sum S: its binade (normal binary32 range only)
 __device__ __forceinline__ bool ox_guess(double S, bool* neg, int* e) {
     const uint64_t bits = uint64_t(__double_as_longlong(S));
     const int de = int((bits >> 52) & 0x7FF);            // biased binary64 exponent
-    const uint32_t top = uint32_t(bits >> 42) & 0x3FFu;  // leading 10 fraction bits
     *neg = (bits >> 63) != 0;
     *e = de - 1023 + 127;                                // biased binary32 exponent
-    return de != 0 && top != 0 && top != 0x3FFu && *e >= 1 && *e <= 254;
+    return de != 0 && *e >= 1 && *e <= 254;
 }
 
 // One warp, one value per lane: the record of the 32 values in lane order for the guess (neg, e).
@@ -272,9 +274,17 @@ __device__ __forceinline__ float warp_chain32(float v, float s) {
     return s;
 }
 
+// Programmatic dependent launch: each kernel of the chain lets the next one launch at once and
+// waits for its predecessor's results (griddepcontrol; no-ops without the launch attribute).
+__device__ __forceinline__ void pdl_wait_and_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // binary64 sum of the positions [2048 b, 2048 b + 2048) of the order -> agg[b]
 __global__ void __launch_bounds__(kOrdThreads) ordered_agg_kernel(const OxParams P, double* agg) {
     __shared__ double s_w[kOrdThreads / 32];
+    pdl_wait_and_release();
     const uint64_t base = uint64_t(blockIdx.x) * kOxPerCta;
     double d = 0.0;
 #pragma unroll
@@ -293,6 +303,7 @@ __global__ void __launch_bounds__(kOrdThreads) ordered_agg_kernel(const OxParams
 // exclusive prefix of agg[0, grid) in binary64, one CTA of 1024 threads: pre[b]
 __global__ void __launch_bounds__(1024) ordered_scan_kernel(const double* agg, double* pre, uint32_t grid) {
     __shared__ double s_t[1024];
+    pdl_wait_and_release();
     const uint32_t t = threadIdx.x;
     const uint32_t per = (grid + 1023) / 1024, lo = t * per, hi = min(grid, lo + per);
     double sum = 0.0;
@@ -313,7 +324,7 @@ __global__ void __launch_bounds__(1024) ordered_scan_kernel(const double* agg, d
 }
 
 // Records: CTA b = positions [2048 b, 2048 b + 2048) = 64 segments; warp w segments 8w .. 8w+7.
-__global__ void __launch_bounds__(kOrdThreads) ordered_records_kernel(const OxParams P) {
+__global__ void __launch_bounds__(kOrdThreads, 4) ordered_records_kernel(const OxParams P) {
     __shared__ double s_ss[kOxSegPerCta];
     __shared__ double s_S[kOxSegPerCta];
     __shared__ OrdRec s_run[kOxSegPerCta];     // per warp: its runs at [8 w, 8 w + count)
@@ -322,6 +333,7 @@ __global__ void __launch_bounds__(kOrdThreads) ordered_records_kernel(const OxPa
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     const uint64_t b = blockIdx.x;
     const uint64_t base = b * kOxPerCta;
+    pdl_wait_and_release();
     if (tid == 0) atomicMin(&g_ord_times[0], gtimer());
     float v[kOxSegPerWarp];
 #pragma unroll
@@ -359,9 +371,12 @@ __global__ void __launch_bounds__(kOrdThreads) ordered_records_kernel(const OxPa
         r[i] = ox_guess(S, &neg, &e) ? warp_record1(v[i], neg, e) : rec_invalid();
         if (r[i].hdr & 1) {
             // predicted to leave its binade (the estimated start plus the record's partial sums
-            // within 2^-10 of an edge): the segment will be added block by block -- a run break
-            const double T0 = fabs(S) * ldexp(1.0, 150 - e);
-            const double mg = 8192.0;
+            // within kOxMargin units of an edge): the segment will be added block by block -- a
+            // run break.  The margin covers the distance between the binary64 prefix and the
+            // actual binary32 chain (measured <= 84 units at 2^30 uniform, m = 4); a wrong
+            // prediction only costs speed (the walk descends)
+            const double T0 = fabs(S) * __longlong_as_double((long long)(uint64_t(1023 + 150 - e) << 52));
+            const double mg = kOxMargin;
             if (T0 + double(min(r[i].mn[0], r[i].mn[1])) < 8388608.0 + mg ||
                 T0 + double(max(r[i].mx[0], r[i].mx[1])) > 16777216.0 - mg)
                 r[i].hdr &= ~1;
@@ -423,6 +438,7 @@ struct OxWalkSmem {
     uint32_t runseg[kOxRunPool];    // segment pool slot of an invalid one-segment run, or kOxNoPool
     uint32_t owner[kOxRunPool];     // leaf that owns the staged run
     uint32_t runbase[kOxChunk];     // first staged run of each leaf, or kOxNoPool
+    uint32_t leafnr[kOxChunk];      // runs of each leaf
     uint32_t segid[kOxSegPool];     // global segment of each staged serial segment
     float seg[kOxSegPool][kOxSeg];  // staged blocks of serial segments
     uint8_t kind[kOxNodes + 1];     // 0 empty, 1 valid composite, 2 descend
@@ -434,15 +450,19 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
     extern __shared__ __align__(16) unsigned char ox_smem[];
     OxWalkSmem& W = *reinterpret_cast<OxWalkSmem*>(ox_smem);
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    pdl_wait_and_release();
     if (tid == 0) g_ord_times[3] = gtimer();
     float s = 0.0f;
     unsigned long long st[4] = {0, 0, 0, 0};
     for (uint64_t c0 = 0; c0 < P.grid; c0 += kOxChunk) {
+        const unsigned long long tc0 = gtimer();
         const uint32_t cn = uint32_t(u64min(kOxChunk, P.grid - c0));
+        uint32_t L = 2;   // leaves of this chunk's tree: a power of two >= cn (shallow trees for small grids)
+        while (L < cn) L <<= 1;
         if (tid == 0) W.nruns = W.nsegs = 0;
         __syncthreads();
         // leaves: the CTA composite when the CTA is one valid run; reserve pool space for the others
-        const uint32_t li = kOxChunk - 1 + tid;
+        const uint32_t li = L - 1 + tid;
         uint8_t kd = 0;
         uint32_t nr = 0, rb = kOxNoPool;
         if (tid < cn) {
@@ -464,9 +484,11 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
                 }
             }
         }
-        W.kind[li] = kd;
+        if (tid < L) W.kind[li] = kd;
         W.runbase[tid] = rb;
+        W.leafnr[tid] = nr;
         __syncthreads();
+        const unsigned long long tc1 = gtimer();
         // stage the runs (one per thread), and reserve a pool slot for each serial segment
         const uint32_t staged = min(W.nruns, kOxRunPool);
         for (uint32_t j = tid; j < staged; j += kOxWalkThreads) {
@@ -489,12 +511,13 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
             W.runseg[j] = sl;
         }
         __syncthreads();
+        const unsigned long long tc2 = gtimer();
         // stage the serial segments' blocks, all threads at once
         const uint32_t nseg = min(W.nsegs, kOxSegPool);
         for (uint32_t e2 = tid; e2 < nseg * kOxSeg; e2 += kOxWalkThreads)
             W.seg[e2 / kOxSeg][e2 % kOxSeg] = ox_load(P, uint64_t(W.segid[e2 / kOxSeg]) * kOxSeg + e2 % kOxSeg);
         // internal nodes, level by level (heap order: children 2i+1, 2i+2)
-        for (uint32_t cnt = kOxChunk / 2, lo = kOxChunk / 2 - 1;; cnt >>= 1, lo = (lo - 1) / 2) {
+        for (uint32_t cnt = L / 2, lo = L / 2 - 1;; cnt >>= 1, lo = (lo - 1) / 2) {
             __syncthreads();
             if (tid < cnt) {
                 const uint32_t i = lo + tid, l = 2 * i + 1, r = 2 * i + 2;
@@ -517,6 +540,7 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
             if (cnt == 1) break;
         }
         __syncthreads();
+        const unsigned long long tc3 = gtimer();
         // the walk: warp 0, depth-first with an explicit stack
         if (warp == 0) {
             uint32_t stk[24];
@@ -531,16 +555,16 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
                     ++st[0];
                     continue;
                 }
-                if (i < kOxChunk - 1) {            // internal: right pushed first, left walked first
+                if (i < L - 1) {                   // internal: right pushed first, left walked first
                     stk[top++] = 2 * i + 2;
                     stk[top++] = 2 * i + 1;
                     continue;
                 }
                 // leaf: record CTA cb, its runs (staged or from global)
-                const uint32_t t = i - (kOxChunk - 1);
+                const uint32_t t = i - (L - 1);
                 const uint64_t cb = c0 + t;
                 const uint32_t rb2 = W.runbase[t];
-                const uint32_t nr2 = k == 1 ? 1u : __ldcg(P.nrun + cb);
+                const uint32_t nr2 = k == 1 ? 1u : W.leafnr[t];
                 for (uint32_t r = 0; r < nr2; ++r) {
                     OrdRec rr;
                     uint32_t ri, sl = kOxNoPool;
@@ -578,6 +602,10 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
                 }
             }
         }
+        if (P.dbg && tid == 0)
+            printf("ordered walk chunk %llu: leaves %.2f us, runs staged %.2f us (%u), segments staged + tree %.2f us (%u), "
+                   "walk %.2f us\n", (unsigned long long)c0, (tc1 - tc0) * 1e-3, (tc2 - tc1) * 1e-3, W.nruns,
+                   (tc3 - tc2) * 1e-3, W.nsegs, (gtimer() - tc3) * 1e-3);
         __syncthreads();
     }
     if (tid == 0) {
@@ -614,6 +642,7 @@ size_t ordered_ws_bytes(uint64_t nb) {
 cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, uint64_t nb, void* ws, uint32_t* ticket,
                                     float* result, cudaStream_t s) {
     (void)ticket;
+    const int dbg = knobs().debug_mode == 41;
     const int grid = ordered_grid(nb);
     static PerDeviceOnce once;
     const cudaError_t ea = once([] {
@@ -636,11 +665,27 @@ cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, 
     P.runinfo = reinterpret_cast<uint32_t*>(P.runrec + ns);
     P.nrun = P.runinfo + ns;
     P.result = result;
-    ordered_agg_kernel<<<grid, kOrdThreads, 0, s>>>(P, agg);
-    ordered_scan_kernel<<<1, 1024, 0, s>>>(agg, pre, uint32_t(grid));
-    ordered_records_kernel<<<grid, kOrdThreads, 0, s>>>(P);
-    ordered_walk_kernel<<<1, kOxWalkThreads, kOxSmem, s>>>(P);
-    return cudaGetLastError();
+    P.dbg = dbg;
+    // four stream-ordered launches with programmatic dependent launch: each grid is scheduled while
+    // its predecessor runs and waits on it in-kernel (the launch latencies overlap)
+    auto pdl = [&](auto kernel, unsigned g, unsigned t, size_t smem, auto... args) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(g);
+        cfg.blockDim = dim3(t);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kernel, args...);
+    };
+    cudaError_t e = pdl(ordered_agg_kernel, unsigned(grid), unsigned(kOrdThreads), 0, P, agg);
+    if (e == cudaSuccess) e = pdl(ordered_scan_kernel, 1u, 1024u, 0, static_cast<const double*>(agg), pre, uint32_t(grid));
+    if (e == cudaSuccess) e = pdl(ordered_records_kernel, unsigned(grid), unsigned(kOrdThreads), 0, P);
+    if (e == cudaSuccess) e = pdl(ordered_walk_kernel, 1u, unsigned(kOxWalkThreads), kOxSmem, P);
+    return e;
 }
 
 }  // namespace tcr

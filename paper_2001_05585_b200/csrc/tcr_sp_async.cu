@@ -291,6 +291,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
+    pdl_release();
     extern __shared__ __align__(128) unsigned char s_ring[];
     __shared__ __align__(16) float s_chunk[kMaxChunksPerGroup];
     __shared__ __align__(16) float s_block[kMaxChunksPerGroup];

@@ -196,6 +196,7 @@ __device__ __forceinline__ void sts_pred(uint32_t addr, float v, bool on) {
 // register-capped variants measured 1-10 % slower here.)
 template <int M, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, const NatShape S) {
+    pdl_release();
     constexpr int ND = 2;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ float s_scratch[32];
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
 // unchanged.  4 bytes per element from HBM, no conversion pass.
 template <int M, int RBC, int UPS, int ND, bool REPAIR, bool XG = true, bool F32 = false>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams p, const NatShape S) {
+    pdl_release();
     constexpr uint32_t ESZ = F32 ? 4u : 2u;                            // bytes per input element
     constexpr uint32_t EP = 16u / ESZ;                                 // elements per 16-byte piece
     constexpr uint32_t UNIT_EL = 256u * RBC;
@@ -563,6 +565,7 @@ struct TrStage {
 
 template <int MM, int SI, int KC, bool REPAIR>   // MM = 8, 32, 64, 128
 __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, const TrShape S) {
+    pdl_release();
     // stages of T tiles: m >= 32 items are K = R (m/16)^2 (a multiple of 4) contiguous tiles, so a
     // 2 KiB stage of 4 tiles stays inside one item (one issue / wait / sync per 4 tiles); m = 8
     // with one-tile items (K = 1: R = 1, 2, 4) is dealt to the warps in runs of SI = 4 adjacent
@@ -756,6 +759,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_tr_kernel(const SpParams p, con
 // ascending-j finishing sum (:182, fragment.hpp:89-92), carried across the m / 256 slabs.
 template <bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, const uint32_t m) {
+    pdl_release();
     // 2 KiB stages: tiles of 4 consecutive rows of one slab (R m rows, a multiple of 4)
     constexpr uint32_t T = 4;
     constexpr int D = kGmTrDepth / int(T);
@@ -870,6 +874,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_kernel(const SpParams p, c
 // similar magnitude add exactly in fp32, so the order rarely matters).
 template <int SL, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams p, const uint32_t m) {
+    pdl_release();
     // 2 KiB stages of 4 consecutive tiles of the warp's stream (rows / 8 * SL tiles per chunk,
     // a multiple of 4): one issue / wait / sync per 4 tiles
     constexpr uint32_t T = 4;
@@ -1003,6 +1008,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_wide_cta_kernel(const SpParams 
 // only 256 chunks at m = 1024: one CTA per chunk left most SMs idle.
 template <int SL, bool REPAIR>
 __global__ void __launch_bounds__(kGmThreads) gm_wide_cluster_kernel(const SpParams p, const uint32_t m) {
+    pdl_release();
     constexpr uint32_t T = 4;                                    // tiles per stage (as gm_wide_cta_kernel)
     constexpr int D = kGmTrDepth / int(T);
     constexpr uint32_t QS = SL > 4 ? uint32_t(SL) : 4u;
