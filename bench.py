@@ -380,7 +380,7 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     lib = _capi.load()
     n = args.n
-    cfg = T.ReductionConfig(m=args.m, R=args.R, B=args.B, engine=T.Engine(args.engine))
+    cfg = T.ReductionConfig(m=args.m, R=args.R, B=args.B, engine=T.Engine(args.engine), finalize=T.Finalize.tree)
     c_cfg = cfg.to_c()
     stream = torch.cuda.current_stream(dev)
     sp = C.c_void_p(stream.cuda_stream)

@@ -89,7 +89,7 @@ struct ReductionConfig {
     double f = 0.5;           // tensor fraction, split variant only
     AtomicOrder atomic_order = AtomicOrder::ascending;
     std::uint64_t atomic_seed = 0;
-    Finalize finalize = Finalize::tree;
+    Finalize finalize = Finalize::ordered;   // the reference's serial combine (reduction.hpp:257-268)
     Engine engine = Engine::automatic;
 
     unsigned warps_per_block() const { return B / 32; }

@@ -45,18 +45,22 @@ typedef enum {
 /* AtomicOrder -- reduction.hpp:25. */
 typedef enum { TCR_ASCENDING = 0, TCR_SEEDED_PERMUTATION = 1 } tcr_atomic_order;
 
-/* How block results are combined on the device (no reference counterpart: the
- * reference serialises its simulated atomics, reduction.hpp:257-268).
- *   TREE    -- deterministic pairwise tree over block results (default; bit-reproducible,
- *              independent of launch geometry, more accurate than a serial sum)
- *   ORDERED -- exactly the reference order: serial fp32 sum, ascending or seeded permutation
+/* How block results are combined on the device (the reference serialises its simulated
+ * atomics, reduction.hpp:257-268).
+ *   ORDERED -- exactly the reference order: serial fp32 sum, ascending or seeded permutation,
+ *              evaluated in parallel bit for bit (default of tcr_config_init and of the C++ /
+ *              Python drop-ins: the reference's value wherever the block results are its)
+ *   TREE    -- deterministic pairwise tree over block results (bit-reproducible, independent of
+ *              launch geometry, more accurate than a serial sum, and the fastest: the measured
+ *              hot path)
  *   ATOMIC  -- the paper's one atomicAdd per block (order unspecified)
  * TREE has no order to permute: a config with atomic_order = SEEDED_PERMUTATION and
  * finalize = TREE runs ORDERED (the seed is never silently ignored). */
 typedef enum { TCR_FINALIZE_TREE = 0, TCR_FINALIZE_ORDERED = 1, TCR_FINALIZE_ATOMIC = 2 } tcr_finalize;
 
 /* Kernel family (chosen by measurement; AUTO picks the fastest available for the config).
- *   MMA_SYNC      -- 1-D TMA bulk copies into a smem ring, ldmatrix.trans + HMMA.16816 chain
+ *   MMA_SYNC      -- TMA-fed: per-warp rings refilled by 1-D bulk copies (cp.async.bulk), a
+ *                    manager warp claiming work ahead, ldmatrix.trans + HMMA.16816 chain
  *   TCGEN05       -- tensor-map TMA (SWIZZLE_32B) ring, single-thread tcgen05.mma into TMEM
  *   MMA_SYNC_REGS -- streaming 128-bit loads straight into registers, MOVM + HMMA (also the
  *                    fp32 convert-on-load path and the ragged tail of the TMA engines)
@@ -138,7 +142,8 @@ int tcr_single_pass_f32_async(const float* d_x, size_t n, const tcr_config* cfg,
  * (communicators are created once per device list and cached).  Every shard but the last must
  * hold a multiple of tcr_group_elems(cfg) elements (so the global block partition is the
  * single-GPU one); out gets the combined value, the OR of the overflow flags and the reference
- * counters of the total length. */
+ * counters of the total length.  Each shard combines its blocks with the TREE (an ORDERED config
+ * runs TREE per shard: the cross-shard sum is one collective, not the serial chain). */
 int tcr_reduce_f16_sharded(const uint16_t* const* d_x, const size_t* n, const int32_t* devices, int32_t ngpu,
                            const tcr_config* cfg, tcr_outcome* out);
 

@@ -904,7 +904,7 @@ void tcr_config_init(tcr_config* c) {
     c->f = 0.5;
     c->atomic_order = TCR_ASCENDING;
     c->atomic_seed = 0;
-    c->finalize = TCR_FINALIZE_TREE;
+    c->finalize = TCR_FINALIZE_ORDERED;   // the reference's combine: drop-in callers get its value
     c->engine = TCR_ENGINE_AUTO;
 }
 

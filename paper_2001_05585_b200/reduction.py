@@ -68,7 +68,7 @@ class ReductionConfig:
     f: float = 0.5
     atomic_order: AtomicOrder = AtomicOrder.ascending
     atomic_seed: int = 0
-    finalize: Finalize = Finalize.tree
+    finalize: Finalize = Finalize.ordered   # the reference's serial combine (reduction.hpp:257-268)
     engine: Engine = Engine.auto
 
     def warps_per_block(self) -> int:

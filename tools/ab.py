@@ -64,7 +64,8 @@ def main():
         lib_path = env.pop("LIB", None)
         m = int(env.pop("M", 16))
         probe = env.pop("PROBE", None) is not None   # time the streaming-read probe instead
-        cfg = T.ReductionConfig(m=m, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])))
+        cfg = T.ReductionConfig(m=m, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])),
+                                finalize=T.Finalize[env.pop("FIN", "tree")])
         specs.append((parts[0], None if probe else cfg.to_c(), env,
                       _capi.load() if lib_path is None else _load_other(lib_path)))
     times = {s[0]: [] for s in specs}

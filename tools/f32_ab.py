@@ -25,7 +25,7 @@ def main():
         res = torch.zeros(2, dtype=torch.float32, device=dev)
         ovf = torch.zeros(1, dtype=torch.int32, device=dev)
         for R, B in ((1, 1024), (4, 128)):
-            cfg = T.ReductionConfig(m=16, R=R, B=B).to_c()
+            cfg = T.ReductionConfig(m=16, R=R, B=B, finalize=T.Finalize.tree).to_c()
             t = {k: [] for k in libs}
             for _ in range(5):
                 for name, lib in libs.items():

@@ -23,7 +23,7 @@ for n in (1 << 28, 1 << 30):
     for m, env in ((16, None), (4, None)):
         if env:
             os.environ[env] = "1"
-        cfg = T.ReductionConfig(m=m, R=1, B=1024 if m == 16 else 128).to_c()
+        cfg = T.ReductionConfig(m=m, R=1, B=1024 if m == 16 else 128, finalize=T.Finalize.tree).to_c()
         fn = lambda: _capi.check(lib.tcr_single_pass_f32_async(C.c_void_p(xf.data_ptr()), n, C.byref(cfg),  # noqa: E731
                                                                C.c_void_p(res.data_ptr()), C.c_void_p(ovf.data_ptr()), sp))
         for _ in range(3):

@@ -28,7 +28,7 @@ def main():
     x = T.generate("uniform", 0, a.n, dtype="float32" if a.f32 else "float16")
     res = torch.zeros(2, dtype=torch.float32, device="cuda")
     ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
-    cfg = T.ReductionConfig(m=a.m, R=a.R, B=a.B, engine=T.Engine(a.engine)).to_c()
+    cfg = T.ReductionConfig(m=a.m, R=a.R, B=a.B, engine=T.Engine(a.engine), finalize=T.Finalize.tree).to_c()
     fn = lib.tcr_single_pass_f32_async if a.f32 else lib.tcr_single_pass_f16_async
     for _ in range(a.reps):
         _capi.check(fn(C.c_void_p(x.data_ptr()), a.n, C.byref(cfg), C.c_void_p(res.data_ptr()),

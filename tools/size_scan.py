@@ -26,7 +26,7 @@ def main():
     res = torch.zeros(2, dtype=torch.float32, device=dev)
     ovf = torch.zeros(1, dtype=torch.int32, device=dev)
     xp, rp, op = C.c_void_p(x.data_ptr()), C.c_void_p(res.data_ptr()), C.c_void_p(ovf.data_ptr())
-    cfg = T.ReductionConfig(m=16, R=1, B=1024).to_c()
+    cfg = T.ReductionConfig(m=16, R=1, B=1024, finalize=T.Finalize.tree).to_c()
 
     def timed(fn, reps=20):
         for _ in range(3):

@@ -30,6 +30,15 @@ KEYS = [
 ]
 
 
+# the workload of each named capture (the default is the bench config)
+CAPTURE_CONFIG = {
+    "genm_m2": "single_pass_m2_R1_B128_n268435456",
+    "genm_m4": "single_pass_m4_R1_B128_n268435456",
+    "genm_m4_r2": "single_pass_m4_R1_B128_n268435456",
+    "ordered": "ordered_walk_m16_R1_B1024_n1073741824",
+}
+
+
 def ncu_raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -92,7 +101,7 @@ def main():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
         try:
             tb = float(rd) * scale.get(ur, 1) + float(wr) * scale.get(uw, 1)
-            traffic[f"{name}_single_pass_m16_R1_B1024_n1073741824"] = tb
+            traffic[f"{name}_{CAPTURE_CONFIG.get(name, 'single_pass_m16_R1_B1024_n1073741824')}"] = tb
             if name == "async":
                 traffic["single_pass_m16_R1_B1024_n1073741824"] = tb
         except (TypeError, ValueError):

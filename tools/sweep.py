@@ -80,7 +80,7 @@ def main():
         for engine in (T.Engine.mma_sync_async, T.Engine.tcgen05, T.Engine.mma_sync, T.Engine.mma_sync_regs):
             for B in (32, 128, 256, 512, 1024):
                 for R in (1, 2, 3, 4, 5):
-                    cfg = T.ReductionConfig(m=16, R=R, B=B, engine=engine)
+                    cfg = T.ReductionConfig(m=16, R=R, B=B, engine=engine, finalize=T.Finalize.tree)
                     c = cfg.to_c()
                     med, best = time_fn(lambda: _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(c), rp, op, sp)),
                                         args.reps)
@@ -95,7 +95,7 @@ def main():
         mpts = []
         for (m, R, B) in ((4, 1, 128), (4, 4, 128), (2, 1, 128), (8, 1, 128), (8, 4, 128), (32, 1, 128), (64, 1, 128),
                           (128, 1, 128)):
-            cfg = T.ReductionConfig(m=m, R=R, B=B)
+            cfg = T.ReductionConfig(m=m, R=R, B=B, finalize=T.Finalize.tree)
             c = cfg.to_c()
             med, best = time_fn(lambda: _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(c), rp, op, sp)),
                                 args.reps)

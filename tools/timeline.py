@@ -30,7 +30,7 @@ def main():
     x = T.generate("uniform", 0, a.n, device=dev)
     res = torch.zeros(2, dtype=torch.float32, device=dev)
     ovf = torch.zeros(1, dtype=torch.int32, device=dev)
-    cfg = T.ReductionConfig(m=16, R=a.R, B=a.B).to_c()
+    cfg = T.ReductionConfig(m=16, R=a.R, B=a.B, finalize=T.Finalize.tree).to_c()
     runs = []
     for rep in range(6):
         _capi.check(lib.tcr_single_pass_f16_async(C.c_void_p(x.data_ptr()), a.n, C.byref(cfg),
