@@ -98,7 +98,7 @@ __device__ __forceinline__ int32_t clamp30(int64_t v) {
 }
 __device__ __forceinline__ uint64_t u64min(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-struct OrdRec {                 // 32 bytes
+struct __align__(16) OrdRec {   // 32 bytes, two 16-byte accesses
     int32_t hdr;                // bit 0 valid, bit 1 negative, bits 2.. biased exponent of s
     int32_t dT[2];              // sum of the roundings r_k for start parity 0 / 1
     int32_t mn[2], mx[2];       // min / max partial sum (relative to T_0) for start parity 0 / 1
@@ -151,6 +151,8 @@ __device__ __forceinline__ float ox_load(const OxParams& P, uint64_t k) {
     return __ldcg(P.blocks + (P.order ? __ldg(P.order + k) : k));
 }
 
+// (parity-indexed fields are selected, never indexed: a runtime index would put the record in
+// local memory)
 __device__ __forceinline__ bool rec_applies(const OrdRec& r, float s) {
     if (!(r.hdr & 1)) return false;
     const uint32_t bits = __float_as_uint(s);
@@ -158,14 +160,15 @@ __device__ __forceinline__ bool rec_applies(const OrdRec& r, float s) {
     if (ex == 0 || ex == 0xFFu) return false;                  // zero, subnormal, inf, NaN
     if (int32_t(ex) != (r.hdr >> 2) || int32_t(bits >> 31) != ((r.hdr >> 1) & 1)) return false;
     const int32_t T0 = int32_t((bits & 0x7FFFFFu) | 0x800000u);
-    const int p0 = T0 & 1;
-    return T0 + r.mn[p0] >= (1 << 23) + 1 && T0 + r.mx[p0] <= (1 << 24) - 1;
+    const bool p1 = T0 & 1;
+    const int32_t mn = p1 ? r.mn[1] : r.mn[0], mx = p1 ? r.mx[1] : r.mx[0];
+    return T0 + mn >= (1 << 23) + 1 && T0 + mx <= (1 << 24) - 1;
 }
 
 __device__ __forceinline__ float rec_apply(const OrdRec& r, float s) {
     const uint32_t bits = __float_as_uint(s);
     const int32_t T0 = int32_t((bits & 0x7FFFFFu) | 0x800000u);
-    const int32_t T1 = T0 + r.dT[T0 & 1];
+    const int32_t T1 = T0 + ((T0 & 1) ? r.dT[1] : r.dT[0]);
     return __uint_as_float((bits & 0xFF800000u) | uint32_t(T1 - (1 << 23)));
 }
 
@@ -187,11 +190,12 @@ __device__ __forceinline__ OrdRec rec_compose(const OrdRec& a, const OrdRec& b) 
     c.pad = 0;
 #pragma unroll
     for (int p0 = 0; p0 < 2; ++p0) {
-        const int pm = (p0 + a.dT[p0]) & 1;
         const int64_t d = a.dT[p0];
-        c.dT[p0] = clamp30(d + b.dT[pm]);
-        c.mn[p0] = clamp30(a.mn[p0] < d + b.mn[pm] ? int64_t(a.mn[p0]) : d + b.mn[pm]);
-        c.mx[p0] = clamp30(a.mx[p0] > d + b.mx[pm] ? int64_t(a.mx[p0]) : d + b.mx[pm]);
+        const bool pm = (p0 + a.dT[p0]) & 1;
+        const int64_t bdT = pm ? b.dT[1] : b.dT[0], bmn = pm ? b.mn[1] : b.mn[0], bmx = pm ? b.mx[1] : b.mx[0];
+        c.dT[p0] = clamp30(d + bdT);
+        c.mn[p0] = clamp30(a.mn[p0] < d + bmn ? int64_t(a.mn[p0]) : d + bmn);
+        c.mx[p0] = clamp30(a.mx[p0] > d + bmx ? int64_t(a.mx[p0]) : d + bmx);
     }
     return c;
 }
@@ -267,10 +271,29 @@ __device__ __forceinline__ OrdRec warp_record1(float b, bool neg, int e) {
 }
 
 // One warp: s + v_0 + v_1 + ... + v_31 (lane l holds v_l), one fp32 add at a time (the reference's
-// loop); every lane runs the same chain, so s stays warp-uniform.
+// loop); every lane runs the same chain, so s stays warp-uniform.  All 32 shuffles are issued
+// before the dependent adds, so the chain costs the adds' latency, not the shuffles'.
 __device__ __forceinline__ float warp_chain32(float v, float s) {
+    float a[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) s += __shfl_sync(kFull, v, i);
+    for (int i = 0; i < 32; ++i) a[i] = __shfl_sync(kFull, v, i);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s += a[i];
+    return s;
+}
+
+// The same chain over 32 values staged in shared memory (16-byte aligned): broadcast vector loads.
+__device__ __forceinline__ float smem_chain32(const float* v, float s) {
+    float4 a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = reinterpret_cast<const float4*>(v)[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        s += a[i].x;
+        s += a[i].y;
+        s += a[i].z;
+        s += a[i].w;
+    }
     return s;
 }
 
@@ -440,9 +463,12 @@ struct OxWalkSmem {
     uint32_t runbase[kOxChunk];     // first staged run of each leaf, or kOxNoPool
     uint32_t leafnr[kOxChunk];      // runs of each leaf
     uint32_t segid[kOxSegPool];     // global segment of each staged serial segment
-    float seg[kOxSegPool][kOxSeg];  // staged blocks of serial segments
+    __align__(16) float seg[kOxSegPool][kOxSeg];  // staged blocks of serial segments
     uint8_t kind[kOxNodes + 1];     // 0 empty, 1 valid composite, 2 descend
-    uint32_t nruns, nsegs;
+    uint8_t pred[kOxNodes + 1];     // the node's composite is predicted to apply (estimated start)
+    uint32_t items[kOxChunk];       // the walk plan: topmost predicted nodes and uncovered leaves
+    uint32_t wsum[kOxWalkThreads / 32];
+    uint32_t nruns, nsegs, nitems;
 };
 
 // The walk (one CTA): per chunk of 1024 record CTAs, stage, build the tree, walk it with warp 0.
@@ -541,11 +567,68 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         }
         __syncthreads();
         const unsigned long long tc3 = gtimer();
-        // the walk: warp 0, depth-first with an explicit stack
+        // the plan: a node's composite is predicted to apply at the binary64 prefix before its
+        // first record CTA; the walk visits the topmost predicted nodes and the uncovered leaves
+        // in order, and descends only where a prediction fails
+        for (uint32_t i = tid; i < 2 * L - 1; i += kOxWalkThreads) {
+            uint32_t f = i;
+            while (f < L - 1) f = 2 * f + 1;   // leftmost leaf
+            const uint32_t t = f - (L - 1);
+            bool pr = false;
+            if (W.kind[i] == 1 && t < cn) pr = rec_applies(W.node[i], float(__ldcg(P.pre + c0 + t)));
+            W.pred[i] = pr ? 1 : 0;
+        }
+        __syncthreads();
+        uint32_t item = 0, emit = 0;
+        if (tid < cn && W.kind[L - 1 + tid] != 0) {
+            uint32_t i = L - 1 + tid, cover = W.pred[i] ? i : kOxNoPool;
+            while (i > 0) {
+                i = (i - 1) / 2;
+                if (W.pred[i]) cover = i;
+            }
+            if (cover == kOxNoPool) {
+                item = L - 1 + tid;
+                emit = 1;
+            } else {
+                uint32_t f = cover;
+                while (f < L - 1) f = 2 * f + 1;
+                item = cover;
+                emit = f == L - 1 + tid;
+            }
+        }
+        // block-wide exclusive scan of the emit flags -> the plan in leaf order
+        const unsigned bal = __ballot_sync(kFull, emit);
+        if (lane == 0) W.wsum[warp] = __popc(bal);
+        __syncthreads();
         if (warp == 0) {
+            const uint32_t v = W.wsum[lane];
+            uint32_t inc = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t2 = __shfl_up_sync(kFull, inc, off);
+                if (lane >= uint32_t(off)) inc += t2;
+            }
+            W.wsum[lane] = inc - v;
+            if (lane == 31) W.nitems = inc;
+        }
+        __syncthreads();
+        if (emit) W.items[W.wsum[warp] + __popc(bal & ((1u << lane) - 1u))] = item;
+        __syncthreads();
+        const unsigned long long tc4 = gtimer();
+        // the walk: warp 0 -- each plan item applied when its record holds, else depth-first
+        // below it with an explicit stack
+        if (warp == 0) {
+            const uint32_t nit = W.nitems;
+            for (uint32_t j = 0; j < nit; ++j) {
+            const uint32_t root = W.items[j];
+            if (W.pred[root] && rec_applies(W.node[root], s)) {
+                s = rec_apply(W.node[root], s);
+                ++st[0];
+                continue;
+            }
             uint32_t stk[24];
             int top = 0;
-            stk[top++] = 0;
+            stk[top++] = root;
             while (top > 0) {
                 const uint32_t i = stk[--top];
                 const uint8_t k = W.kind[i];
@@ -595,17 +678,18 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
                                 continue;
                             }
                         }
-                        const float x = sl != kOxNoPool ? W.seg[sl][lane] : ox_load(P, gs * kOxSeg + lane);
-                        s = warp_chain32(x, s);
+                        if (sl != kOxNoPool) s = smem_chain32(W.seg[sl], s);
+                        else s = warp_chain32(ox_load(P, gs * kOxSeg + lane), s);
                         ++st[3];
                     }
                 }
             }
+            }
         }
         if (P.dbg && tid == 0)
             printf("ordered walk chunk %llu: leaves %.2f us, runs staged %.2f us (%u), segments staged + tree %.2f us (%u), "
-                   "walk %.2f us\n", (unsigned long long)c0, (tc1 - tc0) * 1e-3, (tc2 - tc1) * 1e-3, W.nruns,
-                   (tc3 - tc2) * 1e-3, W.nsegs, (gtimer() - tc3) * 1e-3);
+                   "plan %.2f us (%u items), walk %.2f us\n", (unsigned long long)c0, (tc1 - tc0) * 1e-3, (tc2 - tc1) * 1e-3,
+                   W.nruns, (tc3 - tc2) * 1e-3, W.nsegs, (tc4 - tc3) * 1e-3, W.nitems, (gtimer() - tc4) * 1e-3);
         __syncthreads();
     }
     if (tid == 0) {
