@@ -493,7 +493,15 @@ def main():
         t_cf = timeit(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 0, cp, sp)))
         t_ch = timeit(lambda: _capi.check(lib.tcr_cub_sum_f16_async(xp, n, 1, cp, sp)))
         t_rd = timeit(lambda: _capi.check(lib.tcr_read_probe_async(xp, 2 * n, sp)))
+        # the drop-in default combine (ORDERED: the reference's serial order, bit for bit) on the
+        # same launch path, beside the TREE headline
+        c_ord = T.ReductionConfig(m=args.m, R=args.R, B=args.B, engine=T.Engine(args.engine),
+                                  finalize=T.Finalize.ordered).to_c()
+        t_or = timeit(lambda: _capi.check(lib.tcr_single_pass_f16_async(xp, n, C.byref(c_ord), cp, op, sp)))
         comparators = {
+            "finalize_ordered": {"gelem_s": n / t_or / 1e6, "ms": t_or, "vs_tree_kernel": kms / t_or,
+                                 "what": "single_pass with finalize=ORDERED (drop-in default): streaming kernel + "
+                                         "the parallel serial-order finaliser chain, 10 back-to-back launches"},
             "unit": "Gelem/s",
             "warp_shuffle_fp32": n / t_sh / 1e6,
             "cub_half_in_float_acc": n / t_cf / 1e6,
@@ -545,16 +553,21 @@ def main():
         torch.cuda.empty_cache()
         e32, v32 = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xf.data_ptr()))
         # the reference's real caller: std::span<const float> over a PAGEABLE std::vector
-        # (reduction.hpp:344) -- plain malloc'd host memory, staged through the library's pinned ring
-        xpg = np.empty(n, dtype=np.float32)
-        xpg[:] = xf.numpy()
-        del xf
-        e32p, v32p = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xpg.ctypes.data))
-        xpg16 = np.empty(n, dtype=np.uint16)
-        xpg16[:] = x.cpu().view(torch.int16).numpy().view(np.uint16)
-        del xpg
-        e16p, v16p = time_host(lib.tcr_reduce_f16_host, C.c_void_p(xpg16.ctypes.data))
-        del xpg16
+        # (reduction.hpp:344) -- plain malloc'd host memory, staged through the library's pinned
+        # ring.  One GPU only (N ranks would each hold 6 GiB more host memory)
+        pageable = world == 1
+        if pageable:
+            xpg = np.empty(n, dtype=np.float32)
+            xpg[:] = xf.numpy()
+            del xf
+            e32p, v32p = time_host(lib.tcr_reduce_f32_host, C.c_void_p(xpg.ctypes.data))
+            xpg16 = np.empty(n, dtype=np.uint16)
+            xpg16[:] = x.cpu().view(torch.int16).numpy().view(np.uint16)
+            del xpg
+            e16p, v16p = time_host(lib.tcr_reduce_f16_host, C.c_void_p(xpg16.ctypes.data))
+            del xpg16
+        else:
+            del xf
         e2e = {"value": world * n / e16 / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": world * 2 * n,
                "d2h_bytes_per_step": world * 8, "ms_per_step": e16 * 1e3,
                "path": "tcr_reduce_f16_host (pinned binary16 host input, pipelined H2D + reduce)",
@@ -563,7 +576,9 @@ def main():
                               "d2h_bytes_per_step": world * 8, "ms_per_step": e32 * 1e3,
                               "path": "tcr_reduce_f32_host = reduce(std::span<const float>) drop-in (pinned fp32 "
                                       "host input, pipelined H2D + fused convert/reduce)",
-                              "same_value_as_f16_host": v32 == v16},
+                              "same_value_as_f16_host": v32 == v16}}
+        if pageable:
+            e2e.update({
                "f32_dropin_pageable": {"value": world * n / e32p / 1e9, "unit": "Gelem/s",
                                        "h2d_bytes_per_step": world * 4 * n, "d2h_bytes_per_step": world * 8,
                                        "ms_per_step": e32p * 1e3,
@@ -574,7 +589,7 @@ def main():
                "f16_pageable": {"value": world * n / e16p / 1e9, "unit": "Gelem/s",
                                 "h2d_bytes_per_step": world * 2 * n, "d2h_bytes_per_step": world * 8,
                                 "ms_per_step": e16p * 1e3, "path": "tcr_reduce_f16_host on pageable host memory",
-                                "same_value_as_pinned": v16p == v16}}
+                                "same_value_as_pinned": v16p == v16}})
       except Exception as exc:
         e2e = {"error": repr(exc)}
 
