@@ -642,14 +642,16 @@ int run_tree(const void* d_x, bool f32, uint64_t n, bool half, tcr_outcome* out,
     return TCR_OK;
 }
 
-// oracle64 (:106-110): binary64 sum on the device.
+// oracle64 (:106-110): the reference's left-to-right binary64 sum, bit for bit -- the serial
+// chain evaluated in parallel (tcr_ordered.cu, binary64 records).
 int run_oracle64(const void* d_x, bool f32, uint64_t n, tcr_outcome* out, Workspace* w, cudaStream_t s) {
     out->value = 0.0;
     if (n == 0) return TCR_OK;   // the reference's oracle64 of an empty span is 0
-    int rc = ensure(&w->dpart, &w->dpart_cap, size_t(tcr::sm_count()) * 4, s);
+    const size_t bytes = tcr::ordered_ws_bytes(n, true);
+    int rc = ensure_zero(&w->ord_ws, &w->ord_cap, (bytes + 3) / 4, s);
     if (rc) return rc;
-    TCR_CUDA(tcr::launch_dsum(d_x, f32, n, w->dpart, w->var_ticket(), w->dsum_out(), s));
-    ++g_launches;
+    TCR_CUDA(tcr::launch_serial_sum64(d_x, f32, n, w->ord_ws, w->dsum_out(), s));
+    g_launches += 4;
     return sync_read(&out->value, w->dsum_out(), 8, w, s);
 }
 

@@ -110,11 +110,15 @@ cudaError_t launch_ordered(const float* blocks, const uint32_t* order, uint64_t 
 // records of the binade-local integer arithmetic, composed into runs and a tree, walked by one
 // warp.  order: position -> block, or null (ascending).  ws: >= ordered_ws_bytes(nb), zero on
 // first use (look-back flags return to zero); ticket zero on entry and exit.
-size_t ordered_ws_bytes(uint64_t nb);
+size_t ordered_ws_bytes(uint64_t nb, bool binary64 = false);
 int ordered_stats(unsigned long long* host);   // profiling: counters and phase stamps of the last walk
 int ordered_grid(uint64_t nb);
 cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, uint64_t nb, void* ws, uint32_t* ticket,
                                     float* result, cudaStream_t s);
+// oracle64 (reduction.hpp:106-110): the reference's serial binary64 sum of n fp32 (f32) or
+// binary16 values, by the same parallel evaluation in binary64 -- bit for bit the left-to-right
+// loop.  ws: >= ordered_ws_bytes(n, true).
+cudaError_t launch_serial_sum64(const void* x, bool f32, uint64_t n, void* ws, double* result, cudaStream_t s);
 
 // Fragment sides m != 16 (tcr_sp_genm.cu): binary16 input, any group range.
 bool genm_supported(const SpGeometry& g);
@@ -124,14 +128,12 @@ bool genm_supported(const SpGeometry& g);
 bool genm_f32_supported(const SpGeometry& g);
 cudaError_t launch_genm(const SpParams& p, const SpGeometry& g, cudaStream_t s, bool repair, bool f32 = false);
 
-// Variants (tcr_variants.cu): bit-exact strided pairwise trees (shuffle32 / half_tree), binary64
-// sum (oracle64), and the recurrence level rounding.
+// Variants (tcr_variants.cu): bit-exact strided pairwise trees (shuffle32 / half_tree) and the
+// recurrence level rounding (oracle64 is the binary64 serial chain of tcr_ordered.cu).
 uint64_t tree_cols_needed(uint64_t n);
 int tree_launches(uint64_t n);
 cudaError_t launch_pairwise_tree(const void* x, bool f32, uint64_t n, bool half, float* cols, float* out,
                                  uint32_t* ovf, cudaStream_t s);
-cudaError_t launch_dsum(const void* x, bool f32, uint64_t n, double* partials, uint32_t* ticket, double* out,
-                        cudaStream_t s);
 cudaError_t launch_round_level(const float* in, uint16_t* out, uint64_t count, uint32_t* ovf, cudaStream_t s);
 
 // fp32 -> binary16 (RNE, from_single) conversion of count elements.

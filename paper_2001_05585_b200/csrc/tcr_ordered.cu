@@ -93,32 +93,60 @@ __global__ void __launch_bounds__(kOrdThreads) ordered_serial_kernel(const float
 //
 // Guesses only steer the speed: a wrong one fails its check and the walk descends.
 
-__device__ __forceinline__ int32_t clamp30(int64_t v) {
-    return int32_t(v < -(1ll << 30) ? -(1ll << 30) : (v > (1ll << 30) ? (1ll << 30) : v));
-}
 __device__ __forceinline__ uint64_t u64min(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-struct __align__(16) OrdRec {   // 32 bytes, two 16-byte accesses
-    int32_t hdr;                // bit 0 valid, bit 1 negative, bits 2.. biased exponent of s
-    int32_t dT[2];              // sum of the roundings r_k for start parity 0 / 1
-    int32_t mn[2], mx[2];       // min / max partial sum (relative to T_0) for start parity 0 / 1
-    int32_t pad;
+// The two serial chains evaluated this way: binary32 (the reference's combine of block results,
+// reduction.hpp:264-268) and binary64 (oracle64, reduction.hpp:106-110).  In a binade the values
+// are T u with T in [2^MANT, 2^(MANT+1)).
+template <typename A> struct OxFmt;
+template <> struct OxFmt<float> {
+    using I = int32_t;
+    using U = uint32_t;
+    static constexpr int kMant = 23, kBias = 127, kEmax = 254;
+    static constexpr U kExpMask = 0xFFu;
+    static constexpr double kQMax = 33554432.0;            // 2^25: 32 roundings stay below 2^30
+    static constexpr int64_t kClamp = 1ll << 30;
+    static constexpr double kMargin = 512.0;               // ulps (the binary64 prefix vs the chain)
+    __device__ static U bits(float s) { return __float_as_uint(s); }
+    __device__ static float from(U b) { return __uint_as_float(b); }
 };
-static_assert(sizeof(OrdRec) == 32, "record layout");
-// |dT|, |mn|, |mx| are clamped to 2^30: a record that can apply keeps every partial sum inside
-// one binade (|.| < 2^24), so a clamped record never passes rec_applies.
+template <> struct OxFmt<double> {
+    using I = int64_t;
+    using U = uint64_t;
+    static constexpr int kMant = 52, kBias = 1023, kEmax = 2046;
+    static constexpr U kExpMask = 0x7FFu;
+    static constexpr double kQMax = 144115188075855872.0;  // 2^57: 32 roundings stay below 2^62
+    static constexpr int64_t kClamp = 1ll << 60;
+    static constexpr double kMargin = 1048576.0;           // 2^20 ulps
+    __device__ static U bits(double s) { return uint64_t(__double_as_longlong(s)); }
+    __device__ static double from(U b) { return __longlong_as_double((long long)b); }
+};
+
+template <typename A>
+struct __align__(16) OxRec {    // binary32: 32 bytes; binary64: 64
+    int32_t hdr;                // bit 0 valid, bit 1 negative, bits 2.. biased exponent of s
+    int32_t pad;
+    typename OxFmt<A>::I dT[2];  // sum of the roundings r_k for start parity 0 / 1
+    typename OxFmt<A>::I mn[2];  // min / max partial sum (relative to T_0) for start parity 0 / 1
+    typename OxFmt<A>::I mx[2];
+};
+static_assert(sizeof(OxRec<float>) == 32, "record layout");
+// |dT|, |mn|, |mx| are clamped to kClamp: a record that can apply keeps every partial sum inside
+// one binade (|.| < 2^(MANT+1)), so a clamped record never passes rec_applies.
+template <typename A>
+__device__ __forceinline__ typename OxFmt<A>::I ox_clamp(int64_t v) {
+    constexpr int64_t C = OxFmt<A>::kClamp;
+    return typename OxFmt<A>::I(v < -C ? -C : (v > C ? C : v));
+}
 
 constexpr uint32_t kOxSeg = 32;                             // positions per segment (one per lane)
 constexpr uint32_t kOxSegPerWarp = 8;
 constexpr uint32_t kOxSegPerCta = kOxSegPerWarp * (kOrdThreads / 32);   // 64
 constexpr uint32_t kOxPerCta = kOxSeg * kOxSegPerCta;                  // 2048 positions
-constexpr int kOxWalkThreads = 1024;
-constexpr uint32_t kOxChunk = kOxWalkThreads;               // record CTAs per walk tree (leaves)
-constexpr uint32_t kOxNodes = 2 * kOxChunk - 1;
-constexpr uint32_t kOxRunPool = 1024;                       // staged runs per chunk
 constexpr uint32_t kOxSegPool = 256;                        // staged serial segments per chunk
 constexpr uint32_t kOxNoPool = 0xFFFFFFFFu;
-constexpr double kOxMargin = 512.0;                         // units of the binade's ulp
+// walk CTA = record CTAs per walk tree (leaves) = staged runs per chunk
+template <typename A> struct OxWalk { static constexpr int kThreads = sizeof(A) == 4 ? 1024 : 512; };
 
 // walk counters of the last launch (profiling): tree nodes applied, CTA runs applied, segment
 // records applied, segments added block by block
@@ -133,59 +161,73 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 struct OxParams {
-    const float* blocks;        // block results (reduction.hpp:248-255)
-    const uint32_t* order;      // position -> block (seeded permutation) or null (ascending)
+    const float* blocks;        // the sequence (block results, reduction.hpp:248-255; or fp32 input)
+    const uint16_t* halves;     // ... or binary16 input (oracle64 over binary16), when non-null
+    const uint32_t* order;      // position -> index (seeded permutation) or null (ascending)
     uint64_t nb;
     uint32_t grid;              // record CTAs
-    OrdRec* segrec;             // [grid * 64] segment records
-    OrdRec* runrec;             // [grid * 64] run composites
+    void* segrec;               // [grid * 64] OxRec<A> segment records
+    void* runrec;               // [grid * 64] OxRec<A> run composites
     uint32_t* runinfo;          // [grid * 64] first local segment << 8 | segment count
     uint32_t* nrun;             // [grid]
     const double* pre;          // [grid] binary64 sum of the positions before each record CTA
-    float* result;
+    void* result;               // A
     int dbg;                    // profiling (debug_mode 41): per-chunk phase times via printf
 };
 
 __device__ __forceinline__ float ox_load(const OxParams& P, uint64_t k) {
     if (k >= P.nb) return 0.0f;   // trailing positions: + 0 is the identity of the chain (s is never -0)
-    return __ldcg(P.blocks + (P.order ? __ldg(P.order + k) : k));
+    const uint64_t i = P.order ? __ldg(P.order + k) : k;
+    return P.halves ? h_to_f32(__ldg(P.halves + i)) : __ldcg(P.blocks + i);
 }
 
 // (parity-indexed fields are selected, never indexed: a runtime index would put the record in
 // local memory)
-__device__ __forceinline__ bool rec_applies(const OrdRec& r, float s) {
+template <typename A>
+__device__ __forceinline__ bool rec_applies(const OxRec<A>& r, A s) {
+    using F = OxFmt<A>;
+    using I = typename F::I;
     if (!(r.hdr & 1)) return false;
-    const uint32_t bits = __float_as_uint(s);
-    const uint32_t ex = (bits >> 23) & 0xFFu;
-    if (ex == 0 || ex == 0xFFu) return false;                  // zero, subnormal, inf, NaN
-    if (int32_t(ex) != (r.hdr >> 2) || int32_t(bits >> 31) != ((r.hdr >> 1) & 1)) return false;
-    const int32_t T0 = int32_t((bits & 0x7FFFFFu) | 0x800000u);
+    const typename F::U bits = F::bits(s);
+    const int ex = int((bits >> F::kMant) & F::kExpMask);
+    if (ex == 0 || ex == int(F::kExpMask)) return false;       // zero, subnormal, inf, NaN
+    if (ex != (r.hdr >> 2) || int(bits >> (8 * sizeof(A) - 1)) != ((r.hdr >> 1) & 1)) return false;
+    const I T0 = I((bits & ((typename F::U(1) << F::kMant) - 1)) | (typename F::U(1) << F::kMant));
     const bool p1 = T0 & 1;
-    const int32_t mn = p1 ? r.mn[1] : r.mn[0], mx = p1 ? r.mx[1] : r.mx[0];
-    return T0 + mn >= (1 << 23) + 1 && T0 + mx <= (1 << 24) - 1;
+    const I mn = p1 ? r.mn[1] : r.mn[0], mx = p1 ? r.mx[1] : r.mx[0];
+    return T0 + mn >= (I(1) << F::kMant) + 1 && T0 + mx <= (I(1) << (F::kMant + 1)) - 1;
 }
 
-__device__ __forceinline__ float rec_apply(const OrdRec& r, float s) {
-    const uint32_t bits = __float_as_uint(s);
-    const int32_t T0 = int32_t((bits & 0x7FFFFFu) | 0x800000u);
-    const int32_t T1 = T0 + ((T0 & 1) ? r.dT[1] : r.dT[0]);
-    return __uint_as_float((bits & 0xFF800000u) | uint32_t(T1 - (1 << 23)));
+template <typename A>
+__device__ __forceinline__ A rec_apply(const OxRec<A>& r, A s) {
+    using F = OxFmt<A>;
+    using I = typename F::I;
+    const typename F::U bits = F::bits(s);
+    constexpr typename F::U kM = (typename F::U(1) << F::kMant) - 1;
+    const I T0 = I((bits & kM) | (typename F::U(1) << F::kMant));
+    const I T1 = T0 + ((T0 & 1) ? r.dT[1] : r.dT[0]);
+    return F::from((bits & ~kM) | typename F::U(T1 - (I(1) << F::kMant)));
 }
 
-__device__ __forceinline__ OrdRec rec_invalid() {
-    OrdRec r;
+template <typename A>
+__device__ __forceinline__ OxRec<A> rec_invalid() {
+    OxRec<A> r;
     r.hdr = 0;
+    r.pad = 0;
     r.dT[0] = r.dT[1] = 0;
     r.mn[0] = r.mn[1] = r.mx[0] = r.mx[1] = 0;
-    r.pad = 0;
     return r;
 }
 
-__device__ __forceinline__ bool rec_joinable(const OrdRec& a, const OrdRec& b) { return (a.hdr & 1) && a.hdr == b.hdr; }
+template <typename A>
+__device__ __forceinline__ bool rec_joinable(const OxRec<A>& a, const OxRec<A>& b) {
+    return (a.hdr & 1) && a.hdr == b.hdr;
+}
 
 // Compose b after a (same guess, both valid).
-__device__ __forceinline__ OrdRec rec_compose(const OrdRec& a, const OrdRec& b) {
-    OrdRec c;
+template <typename A>
+__device__ __forceinline__ OxRec<A> rec_compose(const OxRec<A>& a, const OxRec<A>& b) {
+    OxRec<A> c;
     c.hdr = a.hdr;
     c.pad = 0;
 #pragma unroll
@@ -193,50 +235,84 @@ __device__ __forceinline__ OrdRec rec_compose(const OrdRec& a, const OrdRec& b) 
         const int64_t d = a.dT[p0];
         const bool pm = (p0 + a.dT[p0]) & 1;
         const int64_t bdT = pm ? b.dT[1] : b.dT[0], bmn = pm ? b.mn[1] : b.mn[0], bmx = pm ? b.mx[1] : b.mx[0];
-        c.dT[p0] = clamp30(d + bdT);
-        c.mn[p0] = clamp30(a.mn[p0] < d + bmn ? int64_t(a.mn[p0]) : d + bmn);
-        c.mx[p0] = clamp30(a.mx[p0] > d + bmx ? int64_t(a.mx[p0]) : d + bmx);
+        c.dT[p0] = ox_clamp<A>(d + bdT);
+        c.mn[p0] = ox_clamp<A>(a.mn[p0] < d + bmn ? int64_t(a.mn[p0]) : d + bmn);
+        c.mx[p0] = ox_clamp<A>(a.mx[p0] > d + bmx ? int64_t(a.mx[p0]) : d + bmx);
     }
     return c;
 }
 
-// guess for an approximate running sum S: its binade (normal binary32 range only)
+// guess for an approximate running sum S: its binade in A (normal range only)
+template <typename A>
 __device__ __forceinline__ bool ox_guess(double S, bool* neg, int* e) {
     const uint64_t bits = uint64_t(__double_as_longlong(S));
     const int de = int((bits >> 52) & 0x7FF);            // biased binary64 exponent
     *neg = (bits >> 63) != 0;
-    *e = de - 1023 + 127;                                // biased binary32 exponent
-    return de != 0 && *e >= 1 && *e <= 254;
+    *e = de - 1023 + OxFmt<A>::kBias;                    // biased exponent in A
+    return de != 0 && *e >= 1 && *e <= OxFmt<A>::kEmax;
+}
+
+// 2^k as a binary64 built from its bits (k in the normal range)
+__device__ __forceinline__ double pow2d(int k) { return __longlong_as_double((long long)(uint64_t(1023 + k) << 52)); }
+
+template <typename I>
+__device__ __forceinline__ I warp_min(I v) {
+    if constexpr (sizeof(I) == 4) {
+        return __reduce_min_sync(kFull, v);
+    } else {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const I o = __shfl_xor_sync(kFull, v, off);
+            v = o < v ? o : v;
+        }
+        return v;
+    }
+}
+template <typename I>
+__device__ __forceinline__ I warp_max(I v) {
+    if constexpr (sizeof(I) == 4) {
+        return __reduce_max_sync(kFull, v);
+    } else {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const I o = __shfl_xor_sync(kFull, v, off);
+            v = o > v ? o : v;
+        }
+        return v;
+    }
 }
 
 // One warp, one value per lane: the record of the 32 values in lane order for the guess (neg, e).
 // The rounding of q_k = sigma b_k / u depends on the running T only for an exact tie: with no tie
 // in the warp one scan gives both parities' record.
-__device__ __forceinline__ OrdRec warp_record1(float b, bool neg, int e) {
+template <typename A>
+__device__ __forceinline__ OxRec<A> warp_record1(float b, bool neg, int e) {
+    using F = OxFmt<A>;
+    using I = typename F::I;
     const unsigned lane = threadIdx.x & 31u;
-    // sigma / u = sigma 2^(150 - e), built from its bits
-    const double scale = __longlong_as_double((long long)(uint64_t(1023 + 150 - e) << 52) | (neg ? (1ll << 63) : 0ll));
-    const double q = double(b) * scale;
-    const bool fin = isfinite(b) && fabs(q) < 33554432.0;   // 2^25
+    const int sh = F::kBias + F::kMant - e;              // sigma / u = sigma 2^sh
+    if (sh > 1023 || sh < -1022) return rec_invalid<A>();   // warp-uniform: the guess is
+    const double q = double(b) * (neg ? -pow2d(sh) : pow2d(sh));
+    const bool fin = isfinite(b) && fabs(q) < F::kQMax;
     const bool ok = __all_sync(kFull, fin);
     const double f = fin ? floor(q) : 0.0, ph = fin ? q - f : 0.0;
-    const int32_t fi = int32_t(f);
-    OrdRec rec;
+    const I fi = I(f);
+    OxRec<A> rec;
     rec.pad = 0;
     if (!__any_sync(kFull, ph == 0.5)) {
-        int32_t inc = fi + (ph > 0.5 ? 1 : 0);
+        I inc = fi + (ph > 0.5 ? 1 : 0);
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const int32_t a = __shfl_up_sync(kFull, inc, off);
+            const I a = __shfl_up_sync(kFull, inc, off);
             if (lane >= uint32_t(off)) inc += a;
         }
-        const int32_t mn = __reduce_min_sync(kFull, inc), mx = __reduce_max_sync(kFull, inc);
-        const int32_t tot = __shfl_sync(kFull, inc, 31);
+        const I mn = ox_clamp<A>(warp_min(inc)), mx = ox_clamp<A>(warp_max(inc));
+        const I tot = ox_clamp<A>(__shfl_sync(kFull, inc, 31));
         rec.dT[0] = rec.dT[1] = tot;
         rec.mn[0] = rec.mn[1] = mn;
         rec.mx[0] = rec.mx[1] = mx;
     } else {
-        auto rr = [&](uint32_t p) -> int32_t { return ph < 0.5 ? fi : (ph > 0.5 ? fi + 1 : fi + int32_t((p + fi) & 1)); };
+        auto rr = [&](uint32_t p) -> I { return ph < 0.5 ? fi : (ph > 0.5 ? fi + 1 : fi + I((p + fi) & 1)); };
         // the lane's parity map p -> (p + r(p)) & 1, composed in lane order (inclusive scan)
         uint32_t m0 = uint32_t(rr(0) & 1), m1 = uint32_t((1 + rr(1)) & 1);
 #pragma unroll
@@ -255,44 +331,46 @@ __device__ __forceinline__ OrdRec warp_record1(float b, bool neg, int e) {
         }
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-            int32_t inc = rr(t ? s1 : s0);
+            I inc = rr(t ? s1 : s0);
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-                const int32_t a = __shfl_up_sync(kFull, inc, off);
+                const I a = __shfl_up_sync(kFull, inc, off);
                 if (lane >= uint32_t(off)) inc += a;
             }
-            rec.mn[t] = __reduce_min_sync(kFull, inc);
-            rec.mx[t] = __reduce_max_sync(kFull, inc);
-            rec.dT[t] = __shfl_sync(kFull, inc, 31);
+            rec.mn[t] = ox_clamp<A>(warp_min(inc));
+            rec.mx[t] = ox_clamp<A>(warp_max(inc));
+            rec.dT[t] = ox_clamp<A>(__shfl_sync(kFull, inc, 31));
         }
     }
     rec.hdr = (ok ? 1 : 0) | (neg ? 2 : 0) | (e << 2);
     return rec;
 }
 
-// One warp: s + v_0 + v_1 + ... + v_31 (lane l holds v_l), one fp32 add at a time (the reference's
+// One warp: s + v_0 + v_1 + ... + v_31 (lane l holds v_l), one add at a time in A (the reference's
 // loop); every lane runs the same chain, so s stays warp-uniform.  All 32 shuffles are issued
 // before the dependent adds, so the chain costs the adds' latency, not the shuffles'.
-__device__ __forceinline__ float warp_chain32(float v, float s) {
+template <typename A>
+__device__ __forceinline__ A warp_chain32(float v, A s) {
     float a[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) a[i] = __shfl_sync(kFull, v, i);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) s += a[i];
+    for (int i = 0; i < 32; ++i) s += A(a[i]);
     return s;
 }
 
 // The same chain over 32 values staged in shared memory (16-byte aligned): broadcast vector loads.
-__device__ __forceinline__ float smem_chain32(const float* v, float s) {
+template <typename A>
+__device__ __forceinline__ A smem_chain32(const float* v, A s) {
     float4 a[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) a[i] = reinterpret_cast<const float4*>(v)[i];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        s += a[i].x;
-        s += a[i].y;
-        s += a[i].z;
-        s += a[i].w;
+        s += A(a[i].x);
+        s += A(a[i].y);
+        s += A(a[i].z);
+        s += A(a[i].w);
     }
     return s;
 }
@@ -347,12 +425,17 @@ __global__ void __launch_bounds__(1024) ordered_scan_kernel(const double* agg, d
 }
 
 // Records: CTA b = positions [2048 b, 2048 b + 2048) = 64 segments; warp w segments 8w .. 8w+7.
+template <typename A>
 __global__ void __launch_bounds__(kOrdThreads, 4) ordered_records_kernel(const OxParams P) {
+    using F = OxFmt<A>;
+    using Rec = OxRec<A>;
     __shared__ double s_ss[kOxSegPerCta];
     __shared__ double s_S[kOxSegPerCta];
-    __shared__ OrdRec s_run[kOxSegPerCta];     // per warp: its runs at [8 w, 8 w + count)
+    __shared__ Rec s_run[kOxSegPerCta];        // per warp: its runs at [8 w, 8 w + count)
     __shared__ uint32_t s_info[kOxSegPerCta];
     __shared__ uint32_t s_wn[kOrdThreads / 32];
+    Rec* segrec = static_cast<Rec*>(P.segrec);
+    Rec* runrec = static_cast<Rec*>(P.runrec);
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     const uint64_t b = blockIdx.x;
     const uint64_t base = b * kOxPerCta;
@@ -384,32 +467,31 @@ __global__ void __launch_bounds__(kOrdThreads, 4) ordered_records_kernel(const O
         if (lane == 0) atomicMax(&g_ord_times[1], gtimer());
     }
     __syncthreads();
-    OrdRec r[kOxSegPerWarp];
+    Rec r[kOxSegPerWarp];
 #pragma unroll
     for (uint32_t i = 0; i < kOxSegPerWarp; ++i) {
         const uint32_t si = warp * kOxSegPerWarp + i;
         const double S = s_S[si];
         bool neg;
         int e;
-        r[i] = ox_guess(S, &neg, &e) ? warp_record1(v[i], neg, e) : rec_invalid();
+        r[i] = ox_guess<A>(S, &neg, &e) ? warp_record1<A>(v[i], neg, e) : rec_invalid<A>();
         if (r[i].hdr & 1) {
             // predicted to leave its binade (the estimated start plus the record's partial sums
-            // within kOxMargin units of an edge): the segment will be added block by block -- a
-            // run break.  The margin covers the distance between the binary64 prefix and the
-            // actual binary32 chain (measured <= 84 units at 2^30 uniform, m = 4); a wrong
-            // prediction only costs speed (the walk descends)
-            const double T0 = fabs(S) * __longlong_as_double((long long)(uint64_t(1023 + 150 - e) << 52));
-            const double mg = kOxMargin;
-            if (T0 + double(min(r[i].mn[0], r[i].mn[1])) < 8388608.0 + mg ||
-                T0 + double(max(r[i].mx[0], r[i].mx[1])) > 16777216.0 - mg)
+            // within kMargin ulps of an edge): the segment will be added block by block -- a run
+            // break.  The margin covers the distance between the binary64 prefix and the actual
+            // chain (binary32: measured <= 84 ulps at 2^30 uniform, m = 4); a wrong prediction
+            // only costs speed (the walk descends)
+            const double T0 = fabs(S) * pow2d(F::kBias + F::kMant - e);
+            const double lo = pow2d(F::kMant) + F::kMargin, hi = pow2d(F::kMant + 1) - F::kMargin;
+            if (T0 + double(min(r[i].mn[0], r[i].mn[1])) < lo || T0 + double(max(r[i].mx[0], r[i].mx[1])) > hi)
                 r[i].hdr &= ~1;
         }
-        if (lane == 0) P.segrec[b * kOxSegPerCta + si] = r[i];
+        if (lane == 0) segrec[b * kOxSegPerCta + si] = r[i];
     }
     // the warp's runs (lane 0), then thread 0 joins the warps' run lists
     if (lane == 0) {
         uint32_t nr = 0, first = 0;
-        OrdRec c = r[0];
+        Rec c = r[0];
 #pragma unroll
         for (uint32_t i = 1; i <= kOxSegPerWarp; ++i) {
             if (i < kOxSegPerWarp && rec_joinable(c, r[i])) {
@@ -429,60 +511,67 @@ __global__ void __launch_bounds__(kOrdThreads, 4) ordered_records_kernel(const O
     __syncthreads();
     if (tid == 0) {
         uint32_t nr = 0;
-        OrdRec c = s_run[0];
+        Rec c = s_run[0];
         uint32_t ci = s_info[0];
         for (uint32_t w = 0; w < kOrdThreads / 32; ++w) {
             for (uint32_t j = (w == 0 ? 1 : 0); j < s_wn[w]; ++j) {
-                const OrdRec& x = s_run[w * kOxSegPerWarp + j];
+                const Rec& x = s_run[w * kOxSegPerWarp + j];
                 const uint32_t xi = s_info[w * kOxSegPerWarp + j];
                 if (rec_joinable(c, x)) {
                     c = rec_compose(c, x);
                     ci += xi & 0xFFu;
                     continue;
                 }
-                P.runrec[b * kOxSegPerCta + nr] = c;
+                runrec[b * kOxSegPerCta + nr] = c;
                 P.runinfo[b * kOxSegPerCta + nr] = ci;
                 ++nr;
                 c = x;
                 ci = xi;
             }
         }
-        P.runrec[b * kOxSegPerCta + nr] = c;
+        runrec[b * kOxSegPerCta + nr] = c;
         P.runinfo[b * kOxSegPerCta + nr] = ci;
         P.nrun[b] = nr + 1;
         atomicMax(&g_ord_times[2], gtimer());
     }
 }
 
+template <typename A>
 struct OxWalkSmem {
-    OrdRec node[kOxNodes];          // tree over the chunk's CTA composites (heap order)
-    OrdRec run[kOxRunPool];         // staged run lists
-    uint32_t runinfo[kOxRunPool];   // first << 8 | count
-    uint32_t runseg[kOxRunPool];    // segment pool slot of an invalid one-segment run, or kOxNoPool
-    uint32_t owner[kOxRunPool];     // leaf that owns the staged run
-    uint32_t runbase[kOxChunk];     // first staged run of each leaf, or kOxNoPool
-    uint32_t leafnr[kOxChunk];      // runs of each leaf
+    static constexpr uint32_t CH = OxWalk<A>::kThreads;    // leaves per chunk = staged runs
+    OxRec<A> node[2 * CH - 1];      // tree over the chunk's CTA composites (heap order)
+    OxRec<A> run[CH];               // staged run lists
+    uint32_t runinfo[CH];           // first << 8 | count
+    uint32_t runseg[CH];            // segment pool slot of an invalid one-segment run, or kOxNoPool
+    uint32_t owner[CH];             // leaf that owns the staged run
+    uint32_t runbase[CH];           // first staged run of each leaf, or kOxNoPool
+    uint32_t leafnr[CH];            // runs of each leaf
     uint32_t segid[kOxSegPool];     // global segment of each staged serial segment
-    __align__(16) float seg[kOxSegPool][kOxSeg];  // staged blocks of serial segments
-    uint8_t kind[kOxNodes + 1];     // 0 empty, 1 valid composite, 2 descend
-    uint8_t pred[kOxNodes + 1];     // the node's composite is predicted to apply (estimated start)
-    uint32_t items[kOxChunk];       // the walk plan: topmost predicted nodes and uncovered leaves
-    uint32_t wsum[kOxWalkThreads / 32];
+    __align__(16) float seg[kOxSegPool][kOxSeg];  // staged values of serial segments
+    uint8_t kind[2 * CH];           // 0 empty, 1 valid composite, 2 descend
+    uint8_t pred[2 * CH];           // the node's composite is predicted to apply (estimated start)
+    uint32_t items[CH];             // the walk plan: topmost predicted nodes and uncovered leaves
+    uint32_t wsum[CH / 32];
     uint32_t nruns, nsegs, nitems;
 };
 
-// The walk (one CTA): per chunk of 1024 record CTAs, stage, build the tree, walk it with warp 0.
-__global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxParams P) {
+// The walk (one CTA): per chunk of CH record CTAs, stage, build the tree, walk it with warp 0.
+template <typename A>
+__global__ void __launch_bounds__(OxWalk<A>::kThreads) ordered_walk_kernel(const OxParams P) {
+    using Rec = OxRec<A>;
+    constexpr uint32_t CH = OxWalk<A>::kThreads;
     extern __shared__ __align__(16) unsigned char ox_smem[];
-    OxWalkSmem& W = *reinterpret_cast<OxWalkSmem*>(ox_smem);
+    OxWalkSmem<A>& W = *reinterpret_cast<OxWalkSmem<A>*>(ox_smem);
+    const Rec* segrec = static_cast<const Rec*>(P.segrec);
+    const Rec* runrec = static_cast<const Rec*>(P.runrec);
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     pdl_wait_and_release();
     if (tid == 0) g_ord_times[3] = gtimer();
-    float s = 0.0f;
+    A s = A(0);
     unsigned long long st[4] = {0, 0, 0, 0};
-    for (uint64_t c0 = 0; c0 < P.grid; c0 += kOxChunk) {
+    for (uint64_t c0 = 0; c0 < P.grid; c0 += CH) {
         const unsigned long long tc0 = gtimer();
-        const uint32_t cn = uint32_t(u64min(kOxChunk, P.grid - c0));
+        const uint32_t cn = uint32_t(u64min(CH, P.grid - c0));
         uint32_t L = 2;   // leaves of this chunk's tree: a power of two >= cn (shallow trees for small grids)
         while (L < cn) L <<= 1;
         if (tid == 0) W.nruns = W.nsegs = 0;
@@ -494,19 +583,19 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         if (tid < cn) {
             const uint64_t cb = c0 + tid;
             nr = __ldcg(P.nrun + cb);
-            const OrdRec r0 = P.runrec[cb * kOxSegPerCta];
+            const Rec r0 = runrec[cb * kOxSegPerCta];
             if (nr == 1 && (r0.hdr & 1)) {
                 W.node[li] = r0;
                 kd = 1;
             } else {
                 kd = 2;
                 const uint32_t at = atomicAdd(&W.nruns, nr);
-                if (at + nr <= kOxRunPool) {
+                if (at + nr <= CH) {
                     rb = at;
                     for (uint32_t r = 0; r < nr; ++r) W.owner[at + r] = tid;
                 } else {
                     // does not fit: walked from global memory; mark its share of the pool unused
-                    for (uint32_t r = at; r < at + nr && r < kOxRunPool; ++r) W.owner[r] = kOxNoPool;
+                    for (uint32_t r = at; r < at + nr && r < CH; ++r) W.owner[r] = kOxNoPool;
                 }
             }
         }
@@ -516,13 +605,13 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         __syncthreads();
         const unsigned long long tc1 = gtimer();
         // stage the runs (one per thread), and reserve a pool slot for each serial segment
-        const uint32_t staged = min(W.nruns, kOxRunPool);
-        for (uint32_t j = tid; j < staged; j += kOxWalkThreads) {
+        const uint32_t staged = min(W.nruns, CH);
+        for (uint32_t j = tid; j < staged; j += CH) {
             const uint32_t t = W.owner[j];
             if (t == kOxNoPool) continue;
             const uint64_t cb = c0 + t;
             const uint32_t r = j - W.runbase[t];
-            const OrdRec rr = P.runrec[cb * kOxSegPerCta + r];
+            const Rec rr = runrec[cb * kOxSegPerCta + r];
             const uint32_t ri = __ldcg(P.runinfo + cb * kOxSegPerCta + r);
             W.run[j] = rr;
             W.runinfo[j] = ri;
@@ -538,9 +627,9 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         }
         __syncthreads();
         const unsigned long long tc2 = gtimer();
-        // stage the serial segments' blocks, all threads at once
+        // stage the serial segments' values, all threads at once
         const uint32_t nseg = min(W.nsegs, kOxSegPool);
-        for (uint32_t e2 = tid; e2 < nseg * kOxSeg; e2 += kOxWalkThreads)
+        for (uint32_t e2 = tid; e2 < nseg * kOxSeg; e2 += CH)
             W.seg[e2 / kOxSeg][e2 % kOxSeg] = ox_load(P, uint64_t(W.segid[e2 / kOxSeg]) * kOxSeg + e2 % kOxSeg);
         // internal nodes, level by level (heap order: children 2i+1, 2i+2)
         for (uint32_t cnt = L / 2, lo = L / 2 - 1;; cnt >>= 1, lo = (lo - 1) / 2) {
@@ -570,12 +659,12 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         // the plan: a node's composite is predicted to apply at the binary64 prefix before its
         // first record CTA; the walk visits the topmost predicted nodes and the uncovered leaves
         // in order, and descends only where a prediction fails
-        for (uint32_t i = tid; i < 2 * L - 1; i += kOxWalkThreads) {
+        for (uint32_t i = tid; i < 2 * L - 1; i += CH) {
             uint32_t f = i;
             while (f < L - 1) f = 2 * f + 1;   // leftmost leaf
             const uint32_t t = f - (L - 1);
             bool pr = false;
-            if (W.kind[i] == 1 && t < cn) pr = rec_applies(W.node[i], float(__ldcg(P.pre + c0 + t)));
+            if (W.kind[i] == 1 && t < cn) pr = rec_applies(W.node[i], A(__ldcg(P.pre + c0 + t)));
             W.pred[i] = pr ? 1 : 0;
         }
         __syncthreads();
@@ -601,14 +690,14 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         if (lane == 0) W.wsum[warp] = __popc(bal);
         __syncthreads();
         if (warp == 0) {
-            const uint32_t v = W.wsum[lane];
+            const uint32_t v = lane < CH / 32 ? W.wsum[lane] : 0u;
             uint32_t inc = v;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const uint32_t t2 = __shfl_up_sync(kFull, inc, off);
                 if (lane >= uint32_t(off)) inc += t2;
             }
-            W.wsum[lane] = inc - v;
+            if (lane < CH / 32) W.wsum[lane] = inc - v;
             if (lane == 31) W.nitems = inc;
         }
         __syncthreads();
@@ -620,70 +709,70 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
         if (warp == 0) {
             const uint32_t nit = W.nitems;
             for (uint32_t j = 0; j < nit; ++j) {
-            const uint32_t root = W.items[j];
-            if (W.pred[root] && rec_applies(W.node[root], s)) {
-                s = rec_apply(W.node[root], s);
-                ++st[0];
-                continue;
-            }
-            uint32_t stk[24];
-            int top = 0;
-            stk[top++] = root;
-            while (top > 0) {
-                const uint32_t i = stk[--top];
-                const uint8_t k = W.kind[i];
-                if (k == 0) continue;
-                if (k == 1 && rec_applies(W.node[i], s)) {
-                    s = rec_apply(W.node[i], s);
+                const uint32_t root = W.items[j];
+                if (W.pred[root] && rec_applies(W.node[root], s)) {
+                    s = rec_apply(W.node[root], s);
                     ++st[0];
                     continue;
                 }
-                if (i < L - 1) {                   // internal: right pushed first, left walked first
-                    stk[top++] = 2 * i + 2;
-                    stk[top++] = 2 * i + 1;
-                    continue;
-                }
-                // leaf: record CTA cb, its runs (staged or from global)
-                const uint32_t t = i - (L - 1);
-                const uint64_t cb = c0 + t;
-                const uint32_t rb2 = W.runbase[t];
-                const uint32_t nr2 = k == 1 ? 1u : W.leafnr[t];
-                for (uint32_t r = 0; r < nr2; ++r) {
-                    OrdRec rr;
-                    uint32_t ri, sl = kOxNoPool;
-                    if (k == 1) {
-                        rr = W.node[i];
-                        ri = kOxSegPerCta;   // segments 0 .. 63
-                    } else if (rb2 != kOxNoPool) {
-                        rr = W.run[rb2 + r];
-                        ri = W.runinfo[rb2 + r];
-                        sl = W.runseg[rb2 + r];
-                    } else {
-                        rr = P.runrec[cb * kOxSegPerCta + r];
-                        ri = __ldcg(P.runinfo + cb * kOxSegPerCta + r);
-                    }
-                    if (rec_applies(rr, s)) {
-                        s = rec_apply(rr, s);
-                        ++st[1];
+                uint32_t stk[24];
+                int top = 0;
+                stk[top++] = root;
+                while (top > 0) {
+                    const uint32_t i = stk[--top];
+                    const uint8_t k = W.kind[i];
+                    if (k == 0) continue;
+                    if (k == 1 && rec_applies(W.node[i], s)) {
+                        s = rec_apply(W.node[i], s);
+                        ++st[0];
                         continue;
                     }
-                    const uint32_t sf = ri >> 8, sc = ri & 0xFFu;
-                    for (uint32_t q = sf; q < sf + sc; ++q) {
-                        const uint64_t gs = cb * kOxSegPerCta + q;
-                        if (sc > 1 || (rr.hdr & 1)) {
-                            const OrdRec sr = P.segrec[gs];
-                            if (rec_applies(sr, s)) {
-                                s = rec_apply(sr, s);
-                                ++st[2];
-                                continue;
-                            }
+                    if (i < L - 1) {                   // internal: right pushed first, left walked first
+                        stk[top++] = 2 * i + 2;
+                        stk[top++] = 2 * i + 1;
+                        continue;
+                    }
+                    // leaf: record CTA cb, its runs (staged or from global)
+                    const uint32_t t = i - (L - 1);
+                    const uint64_t cb = c0 + t;
+                    const uint32_t rb2 = W.runbase[t];
+                    const uint32_t nr2 = k == 1 ? 1u : W.leafnr[t];
+                    for (uint32_t r = 0; r < nr2; ++r) {
+                        Rec rr;
+                        uint32_t ri, sl = kOxNoPool;
+                        if (k == 1) {
+                            rr = W.node[i];
+                            ri = kOxSegPerCta;   // segments 0 .. 63
+                        } else if (rb2 != kOxNoPool) {
+                            rr = W.run[rb2 + r];
+                            ri = W.runinfo[rb2 + r];
+                            sl = W.runseg[rb2 + r];
+                        } else {
+                            rr = runrec[cb * kOxSegPerCta + r];
+                            ri = __ldcg(P.runinfo + cb * kOxSegPerCta + r);
                         }
-                        if (sl != kOxNoPool) s = smem_chain32(W.seg[sl], s);
-                        else s = warp_chain32(ox_load(P, gs * kOxSeg + lane), s);
-                        ++st[3];
+                        if (rec_applies(rr, s)) {
+                            s = rec_apply(rr, s);
+                            ++st[1];
+                            continue;
+                        }
+                        const uint32_t sf = ri >> 8, sc = ri & 0xFFu;
+                        for (uint32_t q = sf; q < sf + sc; ++q) {
+                            const uint64_t gs = cb * kOxSegPerCta + q;
+                            if (sc > 1 || (rr.hdr & 1)) {
+                                const Rec sr = segrec[gs];
+                                if (rec_applies(sr, s)) {
+                                    s = rec_apply(sr, s);
+                                    ++st[2];
+                                    continue;
+                                }
+                            }
+                            if (sl != kOxNoPool) s = smem_chain32<A>(W.seg[sl], s);
+                            else s = warp_chain32<A>(ox_load(P, gs * kOxSeg + lane), s);
+                            ++st[3];
+                        }
                     }
                 }
-            }
             }
         }
         if (P.dbg && tid == 0)
@@ -695,11 +784,9 @@ __global__ void __launch_bounds__(kOxWalkThreads) ordered_walk_kernel(const OxPa
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) g_ord_stats[i] = st[i];
         g_ord_times[4] = gtimer();
-        *P.result = s;
+        *static_cast<A*>(P.result) = s;
     }
 }
-
-constexpr size_t kOxSmem = sizeof(OxWalkSmem);
 
 }  // namespace
 
@@ -717,46 +804,51 @@ int ordered_stats(unsigned long long* host) {
 
 int ordered_grid(uint64_t nb) { return int((nb + kOxPerCta - 1) / kOxPerCta); }
 
-size_t ordered_ws_bytes(uint64_t nb) {
+size_t ordered_ws_bytes(uint64_t nb, bool binary64) {
     const size_t grid = size_t(ordered_grid(nb));
-    return grid * kOxSegPerCta * (2 * sizeof(OrdRec) + sizeof(uint32_t)) + grid * (2 * sizeof(double) + sizeof(uint32_t)) +
-           256;
+    const size_t rec = binary64 ? sizeof(OxRec<double>) : sizeof(OxRec<float>);
+    return grid * kOxSegPerCta * (2 * rec + sizeof(uint32_t)) + grid * (2 * sizeof(double) + sizeof(uint32_t)) + 256;
 }
 
-cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, uint64_t nb, void* ws, uint32_t* ticket,
-                                    float* result, cudaStream_t s) {
-    (void)ticket;
-    const int dbg = knobs().debug_mode == 41;
+namespace {
+
+template <typename A>
+cudaError_t launch_chain(const float* blocks, const uint16_t* halves, const uint32_t* order, uint64_t nb, void* ws,
+                         A* result, cudaStream_t s) {
     const int grid = ordered_grid(nb);
+    constexpr size_t smem = sizeof(OxWalkSmem<A>);
     static PerDeviceOnce once;
     const cudaError_t ea = once([] {
-        return cudaFuncSetAttribute(ordered_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kOxSmem));
+        return cudaFuncSetAttribute(ordered_walk_kernel<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     });
     if (ea != cudaSuccess) return ea;
     OxParams P{};
     P.blocks = blocks;
+    P.halves = halves;
     P.order = order;
     P.nb = nb;
     P.grid = uint32_t(grid);
+    P.dbg = knobs().debug_mode == 41;
     char* w = static_cast<char*>(ws);
     const size_t ns = size_t(grid) * kOxSegPerCta;
-    // 8-byte members first
-    double* agg = reinterpret_cast<double*>(w);
+    // 16-byte aligned members first
+    OxRec<A>* segrec = reinterpret_cast<OxRec<A>*>(w);
+    OxRec<A>* runrec = segrec + ns;
+    double* agg = reinterpret_cast<double*>(runrec + ns);
     double* pre = agg + grid;
+    P.segrec = segrec;
+    P.runrec = runrec;
     P.pre = pre;
-    P.segrec = reinterpret_cast<OrdRec*>(pre + grid);
-    P.runrec = P.segrec + ns;
-    P.runinfo = reinterpret_cast<uint32_t*>(P.runrec + ns);
+    P.runinfo = reinterpret_cast<uint32_t*>(pre + grid);
     P.nrun = P.runinfo + ns;
     P.result = result;
-    P.dbg = dbg;
     // four stream-ordered launches with programmatic dependent launch: each grid is scheduled while
     // its predecessor runs and waits on it in-kernel (the launch latencies overlap)
-    auto pdl = [&](auto kernel, unsigned g, unsigned t, size_t smem, auto... args) {
+    auto pdl = [&](auto kernel, unsigned g, unsigned t, size_t dyn, auto... args) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(g);
         cfg.blockDim = dim3(t);
-        cfg.dynamicSmemBytes = smem;
+        cfg.dynamicSmemBytes = dyn;
         cfg.stream = s;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -767,9 +859,22 @@ cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, 
     };
     cudaError_t e = pdl(ordered_agg_kernel, unsigned(grid), unsigned(kOrdThreads), 0, P, agg);
     if (e == cudaSuccess) e = pdl(ordered_scan_kernel, 1u, 1024u, 0, static_cast<const double*>(agg), pre, uint32_t(grid));
-    if (e == cudaSuccess) e = pdl(ordered_records_kernel, unsigned(grid), unsigned(kOrdThreads), 0, P);
-    if (e == cudaSuccess) e = pdl(ordered_walk_kernel, 1u, unsigned(kOxWalkThreads), kOxSmem, P);
+    if (e == cudaSuccess) e = pdl(ordered_records_kernel<A>, unsigned(grid), unsigned(kOrdThreads), 0, P);
+    if (e == cudaSuccess) e = pdl(ordered_walk_kernel<A>, 1u, unsigned(OxWalk<A>::kThreads), smem, P);
     return e;
+}
+
+}  // namespace
+
+cudaError_t launch_ordered_parallel(const float* blocks, const uint32_t* order, uint64_t nb, void* ws, uint32_t* ticket,
+                                    float* result, cudaStream_t s) {
+    (void)ticket;
+    return launch_chain<float>(blocks, nullptr, order, nb, ws, result, s);
+}
+
+cudaError_t launch_serial_sum64(const void* x, bool f32, uint64_t n, void* ws, double* result, cudaStream_t s) {
+    return f32 ? launch_chain<double>(static_cast<const float*>(x), nullptr, nullptr, n, ws, result, s)
+               : launch_chain<double>(nullptr, static_cast<const uint16_t*>(x), nullptr, n, ws, result, s);
 }
 
 }  // namespace tcr

@@ -2,7 +2,6 @@
 //
 //   shuffle32  reduction.hpp:113-122  whole-array fp32 pairwise tree, v[i] += v[i + len/2]
 //   half_tree  reduction.hpp:126-151  same tree, every partial stored through binary16
-//   oracle64   reduction.hpp:106-110  binary64 sum
 //   (recurrence and split are composed on the host side of the C ABI from the single_pass
 //    kernels and these.)
 //
@@ -205,53 +204,6 @@ __global__ void __launch_bounds__(kRowThreads) tree_rows_kernel(const T* x, uint
     if (__any_sync(kFull, ovf) && lane_id() == 0) atomicOr(ovf_flag, 1u);
 }
 
-// binary64 sum (oracle64): fixed thread -> element assignment, fixed-order trees: deterministic.
-template <typename T>
-__global__ void __launch_bounds__(256) dsum_kernel(const T* x, uint64_t n, double* partials, uint32_t* ticket,
-                                                   double* out) {
-    double acc = 0.0;
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    constexpr int V = 16 / sizeof(T);                 // elements per 16-byte load
-    const uint64_t nv = n / V;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
-        const uint4 u = __ldcs(reinterpret_cast<const uint4*>(x) + i);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if constexpr (sizeof(T) == 2) {
-                acc += double(h_to_f32(uint16_t(w[j] & 0xFFFFu)));
-                acc += double(h_to_f32(uint16_t(w[j] >> 16)));
-            } else {
-                acc += double(__uint_as_float(w[j]));
-            }
-        }
-    }
-    for (uint64_t i = nv * V + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        if constexpr (sizeof(T) == 2) acc += double(h_to_f32(x[i]));
-        else acc += double(x[i]);
-    }
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(kFull, acc, off);
-    __shared__ double sw[8];
-    __shared__ int s_last;
-    if (lane_id() == 0) sw[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double b = 0.0;
-        for (int w = 0; w < 8; ++w) b += sw[w];
-        partials[blockIdx.x] = b;
-        __threadfence();
-        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        __threadfence();
-        double t = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(partials + b);
-        *out = t;
-        *ticket = 0u;
-    }
-}
-
 // fp32 level results -> binary16 next-level input with the overflow note (reduction.hpp:205-207)
 __global__ void round_level_kernel(const float* in, uint16_t* out, uint64_t count, uint32_t* ovf_flag) {
     bool ovf = false;
@@ -330,13 +282,6 @@ cudaError_t launch_pairwise_tree(const void* x, bool f32, uint64_t n, bool half,
                 : tree_impl<uint16_t, false>(static_cast<const uint16_t*>(x), n, cols, out, ovf, s);
 }
 
-cudaError_t launch_dsum(const void* x, bool f32, uint64_t n, double* partials, uint32_t* ticket, double* out,
-                        cudaStream_t s) {
-    const int grid = sm_count() * 4;
-    if (f32) dsum_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), n, partials, ticket, out);
-    else dsum_kernel<uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(x), n, partials, ticket, out);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_round_level(const float* in, uint16_t* out, uint64_t count, uint32_t* ovf, cudaStream_t s) {
     if (count == 0) return cudaSuccess;

@@ -546,13 +546,37 @@ def test_half_tree_overflows_like_reference(oracle):  # test_reduction.cpp:66-77
     assert T.reduce(np.array([1, 2, 3, 4], np.float32), T.ReductionConfig(variant=T.Variant.half_tree)).value == 10.0
 
 
+def _seq64(x):
+    """The reference's oracle64 (reduction.hpp:106-110): acc += double(v), left to right."""
+    return float(np.cumsum(np.asarray(x, np.float32).astype(np.float64))[-1])
+
+
 def test_oracle64_on_device(oracle):
-    for dist, seed, n in (("uniform", 3, 1000), ("normal", 1, (1 << 22) + 9), ("integers", 2, 1 << 20)):
-        x = oracle.generate(dist, seed, n)
+    """oracle64 is the serial binary64 loop bit for bit (tcr_ordered.cu, binary64 records), on the
+    reference's distributions and on sequences built to hit the hard cases of a binary64 chain:
+    huge / tiny magnitudes mixed (exact ties at the chain's ulp), sign changes, cancellation."""
+    rng = np.random.default_rng(5)
+    cases = [oracle.generate("uniform", 3, 1000), oracle.generate("normal", 1, (1 << 22) + 9),
+             oracle.generate("integers", 2, 1 << 20), oracle.generate("uniform", 0, (1 << 24) + 333),
+             np.ones(1000000, np.float32), np.array([1.5], np.float32), np.array([-0.0, 0.0], np.float32)]
+    big = rng.standard_normal(1 << 20).astype(np.float32) * np.float32(1e8)
+    big[::7] = np.float32(3e-8) * rng.standard_normal(big[::7].size).astype(np.float32)   # ulp-scale values
+    cases.append(big)
+    walk = rng.choice(np.array([-2 ** 30, -1.0, -2 ** -30, 2 ** -30, 1.0, 2 ** 30], np.float32), (1 << 18) + 5)
+    cases.append(walk)
+    ties = (2 * rng.integers(0, 1 << 20, 1 << 20) + 1).astype(np.float32) * np.float32(2 ** -21)
+    ties[0] = np.float32(2 ** 53)                  # the chain's ulp becomes 2: every odd half is a tie
+    cases.append(ties)
+    for x in cases:
         got = T.reduce(x, T.ReductionConfig(variant=T.Variant.oracle64)).value
-        ref = oracle.oracle64(x)
-        assert abs(got - ref) <= 1e-12 * max(abs(ref), 1.0)
-    assert T.reduce(np.ones(1000000, np.float32), T.ReductionConfig(variant=T.Variant.oracle64)).value == 1.0e6
+        assert got == _seq64(x), (x.size, got, _seq64(x))
+        if x.size <= (1 << 22):
+            assert got == oracle.oracle64(x)
+    # binary16 device input: the same chain over the widened values
+    h = oracle.generate_f16("normal", 4, (1 << 20) + 3)
+    xh = to_dev_f16(h)
+    got = T.reduce(xh, T.ReductionConfig(variant=T.Variant.oracle64)).value
+    assert got == _seq64(h.view(np.float16).astype(np.float32))
 
 
 @pytest.mark.parametrize("m,R,B", [(4, 1, 32), (4, 5, 32), (16, 1, 32), (16, 5, 32), (16, 3, 128), (8, 2, 64)])

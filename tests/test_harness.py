@@ -5,8 +5,9 @@ CPU: csv_row / the header against the reference's own csv_row (csv.hpp:19-48, co
 oracle/_ref) on records with identical fields -- every formatting branch (%.9g, nan error,
 true/false, inf / -inf / nan / -nan / -0 / subnormal / huge values, every variant).
 GPU: run_point / sweep_br / sweep_split / error_curve on the B200 against the reference's
-run_point on the CPU -- byte-identical rows where the value is exact (integer inputs), every
-non-float column identical and the value within the precision bars elsewhere."""
+run_point on the CPU -- byte-identical rows on exact inputs for every variant and on uniform
+inputs for single_pass (the ORDERED default combine and the bit-exact oracle64), every non-float
+column identical and the value within the precision bars elsewhere."""
 import io
 import math
 import random
@@ -155,3 +156,17 @@ def test_sweeps_match_reference_rows(oracle):
     lines = buf.getvalue().splitlines()
     assert len(lines) == 10 and lines[0].startswith(H.CSV_HEADER + ",ms,gelem_s")
     assert all(len(line.split(",")) == 16 for line in lines[1:])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a GPU")
+@pytest.mark.parametrize("m,R,B", [(16, 1, 1024), (4, 1, 128), (4, 4, 128), (16, 4, 128), (8, 2, 64)])
+def test_run_point_rows_byte_identical_uniform(oracle, m, R, B):
+    """Uniform inputs (the paper's figures): with the drop-in default ORDERED combine and the
+    bit-exact oracle64, the whole csv.hpp row -- value and error_pct included -- equals the
+    reference's wherever the device block results are the reference's (100 % on uniform data)."""
+    _ref_or_skip(oracle)
+    du = H.Distribution(T.DistKind.uniform, 0)
+    for n in (1 << 14, 100003, 1 << 18):
+        cfg = T.ReductionConfig(m=m, R=R, B=B)
+        assert H.csv_row(H.run_point(du, n, cfg)) == _ref_row(oracle, du, n, cfg)

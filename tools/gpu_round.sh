@@ -29,7 +29,7 @@ if [ "${NCU:-1}" = "1" ]; then
      -o $OUT/async python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-comparators > $OUT/ncu_async.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:sp_bulk -s 3 -c 1 \
      -o $OUT/tma python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-comparators --engine 1 > $OUT/ncu_tma.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gm_nat_fast -s 3 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gm_nat_fast -s 1 -c 1 \
      -o $OUT/genm_m4 python tools/ncu_one.py --m 4 --R 1 --B 128 --n 268435456 > $OUT/ncu_genm_m4.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:ordered_ -s 4 -c 4 \
      -o $OUT/ordered python tools/ordered_one.py 16:1:1024:30 > $OUT/ncu_ordered.log 2>&1
