@@ -708,11 +708,24 @@ __global__ void __launch_bounds__(OxWalk<A>::kThreads) ordered_walk_kernel(const
         // below it with an explicit stack
         if (warp == 0) {
             const uint32_t nit = W.nitems;
+            long long cy[6] = {0, 0, 0, 0, 0, 0};   // profiling (mode 41): cycles per step kind
+            int cn6[6] = {0, 0, 0, 0, 0, 0};
+            long long c_prev = clock64();
+            auto tick = [&](int k) {
+                if (P.dbg) {
+                    const long long c = clock64();
+                    cy[k] += c - c_prev;
+                    ++cn6[k];
+                    c_prev = c;
+                }
+            };
             for (uint32_t j = 0; j < nit; ++j) {
                 const uint32_t root = W.items[j];
+                tick(5);
                 if (W.pred[root] && rec_applies(W.node[root], s)) {
                     s = rec_apply(W.node[root], s);
                     ++st[0];
+                    tick(0);
                     continue;
                 }
                 uint32_t stk[24];
@@ -730,6 +743,7 @@ __global__ void __launch_bounds__(OxWalk<A>::kThreads) ordered_walk_kernel(const
                     if (i < L - 1) {                   // internal: right pushed first, left walked first
                         stk[top++] = 2 * i + 2;
                         stk[top++] = 2 * i + 1;
+                        tick(1);
                         continue;
                     }
                     // leaf: record CTA cb, its runs (staged or from global)
@@ -754,6 +768,7 @@ __global__ void __launch_bounds__(OxWalk<A>::kThreads) ordered_walk_kernel(const
                         if (rec_applies(rr, s)) {
                             s = rec_apply(rr, s);
                             ++st[1];
+                            tick(2);
                             continue;
                         }
                         const uint32_t sf = ri >> 8, sc = ri & 0xFFu;
@@ -764,16 +779,22 @@ __global__ void __launch_bounds__(OxWalk<A>::kThreads) ordered_walk_kernel(const
                                 if (rec_applies(sr, s)) {
                                     s = rec_apply(sr, s);
                                     ++st[2];
+                                    tick(3);
                                     continue;
                                 }
+                                tick(3);
                             }
                             if (sl != kOxNoPool) s = smem_chain32<A>(W.seg[sl], s);
                             else s = warp_chain32<A>(ox_load(P, gs * kOxSeg + lane), s);
                             ++st[3];
+                            tick(4);
                         }
                     }
                 }
             }
+            if (P.dbg && lane == 0)
+                printf("  walk cycles: roots %lld (%d), nodes %lld (%d), runs %lld (%d), segrec %lld (%d), serial %lld (%d), item starts %lld (%d)\n",
+                       cy[0], cn6[0], cy[1], cn6[1], cy[2], cn6[2], cy[3], cn6[3], cy[4], cn6[4], cy[5], cn6[5]);
         }
         if (P.dbg && tid == 0)
             printf("ordered walk chunk %llu: leaves %.2f us, runs staged %.2f us (%u), segments staged + tree %.2f us (%u), "
