@@ -164,6 +164,16 @@ __device__ __forceinline__ void group_epilogue(const SpParams& p, uint64_t gi, f
     __syncthreads();
 }
 
+// Group stage when the block trees already ran in registers (m = 4, W <= 8: the block results are
+// in s_block): publish them (ORDERED / ATOMIC finalisers), then the group tree.
+__device__ __forceinline__ void group_epilogue_blocks(const SpParams& p, uint64_t gi, float* s_block) {
+    __syncthreads();
+    if (p.block_partials || p.finalize == kFinAtomic)
+        for (uint32_t b = threadIdx.x; b < p.G; b += kGmThreads) publish_block(p, gi * p.G + b, s_block[b]);
+    group_tree_cta(p, gi, s_block);
+    __syncthreads();
+}
+
 // ===================================================================== natural layout, m in {2, 4}
 // A PERIOD is lcm(16, chunk) elements = PR 16-element rows holding CP whole chunks (m = 4: one
 // chunk of R rows; m = 2: CP = 4 / gcd(4, R) chunks, which may straddle rows).  A row i of an
@@ -354,7 +364,11 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_kernel(const SpParams p, co
 // them with cvt.rn.f16x2.f32 into its A registers -- a permutation of the MMA's k index
 // (k = 2c, 2c+1, 2c+8, 2c+9 <-> element 4c .. 4c+3) that the selector B follows, so D is
 // unchanged.  4 bytes per element from HBM, no conversion pass.
-template <int M, int RBC, int UPS, int ND, bool REPAIR, bool XG = true, bool F32 = false>
+// BT (m = 4, W = B/32 in {1, 2, 4, 8}; dispatched for W <= 2): the unit's 16 chunk results (lanes c = 0 hold chunks g and
+// g + 8 after the finishing MMA) go through the reference's block tree (reduction.hpp:90-101:
+// v[i] += v[i + len/2], len = W ... 2) in registers with shuffles; only block results reach shared
+// memory, and the chunk table disappears (a smaller footprint: one more CTA per SM).
+template <int M, int RBC, int UPS, int ND, bool REPAIR, bool XG = true, bool F32 = false, int BT = 0>
 __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams p, const NatShape S) {
     pdl_release();
     constexpr uint32_t ESZ = F32 ? 4u : 2u;                            // bytes per input element
@@ -371,7 +385,7 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
     const unsigned g = lane >> 2, c = lane & 3u;
     const uint32_t R = p.R;
     float* s_chunk = reinterpret_cast<float*>(dsm + kGmWarps * ND * STAGE_B);
-    float* s_block = s_chunk + p.G * p.W;
+    float* s_block = BT ? s_chunk : s_chunk + p.G * p.W;
     const uint32_t ring = smem_u32(dsm) + warp * ND * STAGE_B;
     const uint32_t ce = R * M * M;
     const uint32_t CP = S.CP, cpu = S.chunks_per_unit;
@@ -515,7 +529,21 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
                     nanacc = fmaf(d2[3], 0.0f, nanacc);
                 }
                 const uint32_t cu = cu0 + j * cpu;
-                if constexpr (M == 4) {
+                if constexpr (M == 4 && BT > 0) {
+                    // block trees of the unit's 16 / BT blocks: chunk k sits in lane 4 (k mod 8),
+                    // d2[0] for k < 8, d2[2] for k >= 8; level len pairs lanes 4 len / 2 apart
+                    float x0 = d2[0], x2 = d2[2];
+#pragma unroll
+                    for (int len = BT; len > 1; len >>= 1) {
+                        const float t0 = __shfl_down_sync(kFull, x0, 2 * len), t2 = __shfl_down_sync(kFull, x2, 2 * len);
+                        x0 = x0 + t0;   // v[i] += v[i + len/2] (only lanes with g mod len = 0 are used)
+                        x2 = x2 + t2;
+                    }
+                    const uint32_t bu = cu / BT, bj = g / BT;           // the unit's first block, this lane's
+                    const bool lead = c == 0 && (g % BT) == 0;
+                    sts_pred(smem_u32(s_block) + 4u * (bu + bj), x0, lead && (full || bu + bj < p.G));
+                    sts_pred(smem_u32(s_block) + 4u * (bu + 8u / BT + bj), x2, lead && (full || bu + 8u / BT + bj < p.G));
+                } else if constexpr (M == 4) {
                     // one chunk per period (CP = 1): lanes c = 0 own chunks g and g + 8 of the unit;
                     // predicated stores at compile-time offsets, no branches
                     const uint32_t ca = cu + g;
@@ -534,7 +562,8 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
             cu0 += kGmWarps * UPS * cpu;
         }
         ovf = nanacc != nanacc;
-        group_epilogue<REPAIR, F32>(p, gi, s_chunk, s_block, M, ovf);
+        if constexpr (BT > 0) group_epilogue_blocks(p, gi, s_block);
+        else group_epilogue<REPAIR, F32>(p, gi, s_chunk, s_block, M, ovf);
     }
     cp_wait<0>();
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
@@ -1262,8 +1291,19 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
         // PR <= 8 or 16: a unit of 16 periods is one contiguous stage of 512 PR bytes
         const bool fast = S.PR == S.RB && (S.PR <= 8 || S.PR == 16) && !knobs().gm_nat_generic;
+        if (fast && !REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
+            // m = 4, R = 1, B = 32 / 64: block trees in registers, no chunk table (tables: block
+            // results only).  Measured at 2^28: B = 32 4.07 -> 4.89 TB/s, B = 64 4.75 -> 4.79;
+            // B = 128 / 256 neutral / -4 % (the shuffle tree costs what the table saved), not used
+            void (*fb)(SpParams, NatShape) = nullptr;
+            switch (g.W) {
+            case 1: fb = gm_nat_fast_kernel<4, 1, 4, 3, false, true, false, 1>; break;
+            default: fb = gm_nat_fast_kernel<4, 1, 4, 3, false, true, false, 2>; break;
+            }
+            return launch_gm(fb, kGmWarps * 3u * (512u * 4u) + (g.G + 3u) / 4u * 16u, groups, p, S, s);
+        }
         if (fast) {
-            const int a = knobs().gm_nat_alt;                           // knob: ring shape A/B
+            const int a = knobs().gm_nat_alt;                           // knob: ring shape A/B (7: no register block trees)
             void (*ff)(SpParams, NatShape) = nullptr;
             uint32_t stage = 0, nd = 0;
             // (units per stage, stages): 2 KiB stages; one-row periods 3 stages -> 3 CTAs per SM
@@ -1364,6 +1404,15 @@ cudaError_t launch_genm_f32_t(const SpParams& p, const SpGeometry& g, cudaStream
     const uint32_t tables = (Cg + g.G + 3u) / 4u * 16u;
     NatShape S;
     if (!genm_f32_supported(g) || !nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
+    if (!REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
+        // fp32, m = 4, R = 1, B = 32 / 64: register block trees (as the binary16 path)
+        void (*fb)(SpParams, NatShape) = nullptr;
+        switch (g.W) {
+        case 1: fb = gm_nat_fast_kernel<4, 1, 2, 3, false, true, true, 1>; break;
+        default: fb = gm_nat_fast_kernel<4, 1, 2, 3, false, true, true, 2>; break;
+        }
+        return launch_gm(fb, kGmWarps * 3u * (1024u * 2u) + (g.G + 3u) / 4u * 16u, groups, p, S, s);
+    }
     void (*ff)(SpParams, NatShape) = nullptr;
     uint32_t stage = 0, nd = 0;
     // 2-4 KiB stages of fp32 (twice the bytes of the binary16 unit)
