@@ -32,7 +32,7 @@ def _case(rng):
     seed = int(rng.integers(0, 1000))
     fin = T.Finalize(int(rng.integers(0, 3)))
     engine = T.Engine(int(rng.choice([0, 0, 1, 2, 3, 4]))) if m == 16 else T.Engine.auto
-    variant = str(rng.choice(["single_pass"] * 6 + ["recurrence", "split", "shuffle32", "half_tree"]))
+    variant = str(rng.choice(["single_pass"] * 6 + ["recurrence", "split", "shuffle32", "half_tree", "oracle64"]))
     return m, R, B, n, dist, seed, fin, engine, variant
 
 
@@ -74,8 +74,8 @@ def test_random_config_matches_reference(oracle, k):
         gb = T.block_results(xd, T.ReductionConfig(m=m, R=R, B=B, engine=engine)).cpu().numpy()
         if np.array_equal(gb.view(np.uint32), ref_blocks.view(np.uint32)):
             assert got.value == ref.value, (tag, got.value, ref.value)
-    if variant in ("shuffle32", "half_tree"):
-        assert got.value == ref.value, tag                     # bit-exact strided trees
+    if variant in ("shuffle32", "half_tree", "oracle64"):
+        assert got.value == ref.value, tag                     # bit-exact strided trees / serial binary64
     elif dist == "integers" and 9 * R * m <= 2048 and absum < 2 ** 24:
         assert got.value == ref.value, tag                     # exact integer sums
     else:
