@@ -69,6 +69,9 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 // (the ORDERED finaliser chain) be scheduled now; it waits for this grid in-kernel
 // (griddepcontrol.wait).  A no-op for ordinary successors.
 __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// ... and, launched that way itself, wait for the predecessor grid's completion and memory flush
+// before the first global access (a no-op for an ordinary launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // SplitMix64 k-th draw, k >= 1 (rng.hpp:13-18 with the state jumped ahead by k*gamma).
 __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {

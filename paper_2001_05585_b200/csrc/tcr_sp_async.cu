@@ -291,6 +291,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 template <int RT, int D = AsDepth<RT>::value>
 __global__ void __launch_bounds__(kAsThreads) sp_async_kernel(const SpParams p) {
+    pdl_wait();      // launched early (programmatic serialization): the previous grid first
     pdl_release();
     extern __shared__ __align__(128) unsigned char s_ring[];
     __shared__ __align__(16) float s_chunk[kMaxChunksPerGroup];
@@ -543,8 +544,19 @@ int async_max_grid(uint32_t R, int mode) {
 cudaError_t launch_async(const SpParams& p, int grid, cudaStream_t s) {
     if (!as_attr_once()) return cudaErrorInvalidValue;
     const AsPick k = pick(p.R, p.debug_mode);
-    k.fn<<<grid, kAsThreads, as_launch(k, as_ctas_per_sm()).smem, s>>>(p);
-    return cudaGetLastError();
+    // programmatic dependent launch: back-to-back reductions on a stream overlap this grid's launch
+    // with the previous grid's tail (the kernel waits for it before its first global access)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kAsThreads);
+    cfg.dynamicSmemBytes = as_launch(k, as_ctas_per_sm()).smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k.fn, p);
 }
 
 }  // namespace tcr
