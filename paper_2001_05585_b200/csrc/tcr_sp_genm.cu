@@ -112,14 +112,8 @@ __device__ __forceinline__ void group_tree_cta(const SpParams& p, uint64_t gi, c
             acc = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         }
     } else if (lo < G) {
-        float stk[16];
-        int top = 0;
-        for (uint32_t i = 0; i < seg; ++i) {
-            float v = blocks[lo + i];
-            for (uint32_t b = i; b & 1; b >>= 1) v = stk[--top] + v;
-            stk[top++] = v;
-        }
-        acc = stk[0];
+        // longer segments (B = 32: G = 4096, 16 per thread): compile-time register trees
+        acc = lane_segment_tree([&](uint32_t i) { return blocks[i]; }, lo, seg);
     }
     acc = warp_tree_xor(acc);
     if (lane_id() == 0) s_w[threadIdx.x >> 5] = acc;
@@ -569,6 +563,154 @@ __global__ void __launch_bounds__(kGmThreads) gm_nat_fast_kernel(const SpParams 
     if (__any_sync(kFull, ovf) && lane == 0) atomicOr(p.overflow, 1u);
     __syncthreads();
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
+}
+
+// ============================================================ m = 4, R = 1: register-direct stream
+// The reference default shape (m = 4, R = 1, reduction.hpp:41) on binary16 data.  A TILE is 16
+// consecutive chunks of 16 elements = 512 bytes = one HMMA: row i of A is chunk i, and lane
+// (g, c) loads its A fragment straight from global memory -- 8 bytes of chunk g (elements 4c ..
+// 4c+3) and 8 bytes of chunk g + 8 (two LDG.64; the 32 lanes of one load cover 256 contiguous
+// bytes).  The k index is permuted exactly as in the fp32 path of gm_nat_fast_kernel (k = 2c,
+// 2c+1, 2c+8, 2c+9 <-> element 4c .. 4c+3), so the selector B[k][n] = [column of k == n] and
+// every MMA, binary16 rounding and finishing MMA is the same as there (bit-identical chunk
+// results).  No shared-memory ring, no cp.async / ldmatrix: the loads land in registers, NB
+// batches of U tiles per warp rotate through NB register buffers (NB - 1 batches = 6 KiB per
+// warp in flight), chunk results go to the group's chunk table and the block / group trees run in
+// the common epilogue.  Warp w of the CTA streams tiles [w T, (w+1) T) of each of its groups
+// (T = Cg / 128); the batch sequence runs across groups, so the next group's loads are in
+// flight during a group's epilogue.
+constexpr int kM4U = 4;    // tiles per batch
+constexpr int kM4NB = 4;   // register buffers (batches) per warp
+
+__device__ __forceinline__ uint2 ldg_stream_v2(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
+// 4 binary16 at element e, zero past n (the reference's zero padding, reduction.hpp:244-245)
+__device__ __forceinline__ uint2 ld4_tail(const uint16_t* x, uint64_t e, uint64_t n) {
+    if (e + 4 <= n) return ldg_stream_v2(x + e);
+    uint16_t h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = e + i < n ? x[e + i] : uint16_t(0);
+    return make_uint2(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16));
+}
+
+__global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p, const bool l2_prefetch) {
+    pdl_release();
+    extern __shared__ __align__(16) float s_tab[];
+    __shared__ float s_scratch[32];
+    __shared__ int s_last;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    const unsigned g = lane >> 2, c = lane & 3u;
+    const uint32_t Cg = p.G * p.W;
+    float* s_chunk = s_tab;
+    float* s_block = s_tab + Cg;
+    const uint32_t T = Cg / (16u * kGmWarps);       // tiles per warp per group
+    const uint32_t nb = T / kM4U;                   // batches per warp per group
+    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint64_t n = p.n;
+    // selector of the permuted k (see above): b0 rows k = 2c, 2c+1 -> columns 0, 1; b1 rows
+    // k = 2c+8, 2c+9 -> columns 2, 3
+    const uint32_t b0 = sel2(g == 0, g == 1), b1 = sel2(g == 2, g == 3);
+    const uint32_t bfin = sel2((2 * c) / 4 == g, (2 * c + 1) / 4 == g);
+    const uint64_t g0 = p.group_begin + blockIdx.x;
+    const uint64_t ngroups = p.group_end > g0 ? (p.group_end - g0 + gridDim.x - 1) / gridDim.x : 0;
+    // lane's element offset inside a tile: row g, elements 4c .. 4c+3 (row g + 8: +128)
+    const uint32_t lane_el = 16u * g + 4u * c;
+    // this warp's chunk-table slot of tile t of batch (j mod nb), lanes c = 0 store
+    const uint32_t s_lane = smem_u32(s_chunk) + 4u * (warp * T * 16u + g);
+
+    uint2 buf[kM4NB][2 * kM4U];
+    // issue cursor: the ik-th group of this CTA, batch ib of it, this lane's element ie (advanced
+    // by increments: no division on the issue path)
+    uint64_t ik = 0, ie = 0;
+    uint32_t ib = 0;
+    bool ifull = false;
+    auto iset = [&]() {
+        const uint64_t gi = g0 + ik * gridDim.x;
+        ie = gi * uint64_t(Cg) * 16u + uint64_t(warp * T) * 256u + lane_el;
+        ifull = (gi + 1) * uint64_t(Cg) * 16u <= n;
+    };
+    if (ngroups) iset();
+    auto issue = [&](uint2 (&b)[2 * kM4U]) {
+        if (ik >= ngroups) return;
+        const uint16_t* q = x + ie;
+        if (ifull) {
+#pragma unroll
+            for (int t = 0; t < kM4U; ++t) {
+                b[2 * t] = ldg_stream_v2(q + 256u * t);
+                b[2 * t + 1] = ldg_stream_v2(q + 256u * t + 128u);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < kM4U; ++t) {
+                b[2 * t] = ld4_tail(x, ie + 256u * t, n);
+                b[2 * t + 1] = ld4_tail(x, ie + 256u * t + 128u, n);
+            }
+        }
+        ie += 256u * kM4U;
+        if (++ib == nb) {
+            ib = 0;
+            if (++ik < ngroups) iset();
+        }
+    };
+    auto consume = [&](const uint2 (&b)[2 * kM4U], uint32_t jb) {
+        const uint32_t tb = jb * kM4U;   // first tile of the batch (jb-th of the group) in this warp's range
+        float d2[kM4U][4];
+#pragma unroll
+        for (int t = 0; t < kM4U; ++t) {
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            // C_1 = ones x M_1 (reduction.hpp:173-177) for 16 chunks: A rows = chunks
+            mma_16816(acc, b[2 * t].x, b[2 * t + 1].x, b[2 * t].y, b[2 * t + 1].y, b0, b1);
+            d2[t][0] = d2[t][1] = d2[t][2] = d2[t][3] = 0.f;
+            // C_R -> binary16 (:179-181), finishing MMA (:182): chunk g in d2[0], g + 8 in d2[2]
+            mma_16816(d2[t], pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), 0u, 0u, bfin, 0u);
+        }
+#pragma unroll
+        for (int t = 0; t < kM4U; ++t) {
+            const uint32_t a = s_lane + 64u * (tb + t);
+            sts_pred(a, d2[t][0], c == 0);
+            sts_pred(a + 32u, d2[t][2], c == 0);
+        }
+    };
+    // Profiling variant (knob): L2 prefetch one group ahead (cp.async.bulk.prefetch.L2, one
+    // instruction per warp range).  Measured slower (2^28: 93.7 vs 85.9 us, 2^30: 337 vs 314 us):
+    // the register pipeline alone keeps HBM busy, so it is off by default.
+    const uint32_t wbytes = T * 512u;                // this warp's contiguous range of a group
+    auto prefetch = [&](uint64_t gk) {
+        if (!l2_prefetch || gk >= ngroups || lane != 0) return;
+        const uint64_t gi = g0 + gk * gridDim.x;
+        const uint64_t e0 = gi * uint64_t(Cg) * 16u + uint64_t(warp) * T * 256u;
+        if (e0 + wbytes / 2u > n) return;            // a ragged group streams without it
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + e0), "r"(wbytes) : "memory");
+    };
+    prefetch(0);
+#pragma unroll
+    for (int s = 0; s < kM4NB - 1; ++s) issue(buf[s]);
+    // nb is a multiple of NB (gm4_reg_ok): buffer s always holds a batch j = s mod NB
+    for (uint64_t gk = 0; gk < ngroups; ++gk) {
+        prefetch(gk + 1);
+        for (uint32_t jj = 0; jj < nb; jj += kM4NB) {
+#pragma unroll
+            for (int s = 0; s < kM4NB; ++s) {
+                // refill the buffer consumed one step ago, then consume buffer s
+                issue(buf[(s + kM4NB - 1) % kM4NB]);
+                consume(buf[s], jj + s);
+            }
+        }
+        // the group's chunk table is complete: block trees (:90-101, :253), group tree
+        group_epilogue<false>(p, g0 + gk * gridDim.x, s_chunk, s_block, 4u, false);
+    }
+    __syncthreads();
+    finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
+}
+
+// m = 4, R = 1 register-direct engine eligibility: whole batches per warp per group
+// (W >= 2: for B = 32 the register block-tree ring kernel measured faster, 4.80 vs 4.59 TB/s at 2^28)
+__host__ __device__ inline bool gm4_reg_ok(uint32_t m, uint32_t R, uint32_t W, uint32_t Cg, bool gm4_all_w = false) {
+    return m == 4 && R == 1 && (W >= 2 || gm4_all_w) && Cg % (16u * kGmWarps * kM4U * kM4NB) == 0;
 }
 
 // ================================================================ transposed tiles, m = 8 or 16*S
@@ -1251,6 +1393,19 @@ cudaError_t launch_gm(K fn, uint32_t dyn, uint64_t groups, const SpParams& p, co
     return cudaGetLastError();
 }
 
+// Engines with a flag instead of a shape argument (gm4_reg_kernel)
+cudaError_t launch_gm(void (*fn)(SpParams, bool), uint32_t dyn, uint64_t groups, const SpParams& p, bool flag,
+                      cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kGmThreads, dyn);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = int(groups < uint64_t(per_sm) * sm_count() ? groups : uint64_t(per_sm) * sm_count());
+    fn<<<grid, kGmThreads, dyn, s>>>(p, flag);
+    return cudaGetLastError();
+}
+
 // Thread-block-cluster launch (CS CTAs per cluster, one group of chunks per cluster at a time).
 template <typename K>
 cudaError_t launch_cluster(K fn, uint32_t dyn, uint64_t groups, uint32_t CS, const SpParams& p, uint32_t m,
@@ -1291,6 +1446,11 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
         // PR <= 8 or 16: a unit of 16 periods is one contiguous stage of 512 PR bytes
         const bool fast = S.PR == S.RB && (S.PR <= 8 || S.PR == 16) && !knobs().gm_nat_generic;
+        if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
+            // m = 4, R = 1: register-direct stream (knob values: 8 the ring kernels, 9 with the
+            // L2 prefetch; A/B)
+            return launch_gm(gm4_reg_kernel, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
+        }
         if (fast && !REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
             // m = 4, R = 1, B = 32 / 64: block trees in registers, no chunk table (tables: block
             // results only).  Measured at 2^28: B = 32 4.07 -> 4.89 TB/s, B = 64 4.75 -> 4.79;

@@ -4,7 +4,7 @@
     python tools/ab.py [--n 1073741824] [--rounds 7] [--reps 10] SPEC [SPEC ...]
 
 SPEC = label:engine:R:B[:ENV=VAL,...]  e.g.  async:4:1:1024  tc05:2:1:1024:TCR_DEBUG_MODE=3
-(PROBE=1 in the ENV list times the streaming-read probe instead, e.g. tma:0:1:1:PROBE=1,TCR_PROBE=tma)
+(PROBE=1 / SHUFFLE=1 in the ENV list time the streaming-read probe / the warp-shuffle comparator instead, e.g. tma:0:1:1:PROBE=1,TCR_PROBE=tma)
 (LIB=path in the ENV list times another build of libtcreduce_b200.so, e.g. a previous commit's;
 M=m sets the fragment side, default 16)
 Rounds alternate between the specs so clock / thermal drift hits all of them alike; the
@@ -64,9 +64,11 @@ def main():
         lib_path = env.pop("LIB", None)
         m = int(env.pop("M", 16))
         probe = env.pop("PROBE", None) is not None   # time the streaming-read probe instead
+        if env.pop("SHUFFLE", None) is not None:     # time the warp-shuffle comparator instead
+            probe = "shuffle"
         cfg = T.ReductionConfig(m=m, R=int(parts[2]), B=int(parts[3]), engine=T.Engine(int(parts[1])),
                                 finalize=T.Finalize[env.pop("FIN", "tree")])
-        specs.append((parts[0], None if probe else cfg.to_c(), env,
+        specs.append((parts[0], probe if probe else cfg.to_c(), env,
                       _capi.load() if lib_path is None else _load_other(lib_path)))
     times = {s[0]: [] for s in specs}
     vals = {}
@@ -77,7 +79,9 @@ def main():
             lib.tcr_enable_profiling_knobs.restype = C.c_int
             lib.tcr_enable_profiling_knobs()   # knobs are read only on this explicit call
             def call():
-                if c is None:
+                if c == "shuffle":
+                    _capi.check(lib.tcr_shuffle_f16_async(xp, a.n, rp, sp))
+                elif c is True:
                     _capi.check(lib.tcr_read_probe_async(xp, 2 * a.n, sp))
                 else:
                     _capi.check(lib.tcr_single_pass_f16_async(xp, a.n, C.byref(c), rp, op, sp))

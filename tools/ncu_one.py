@@ -25,6 +25,7 @@ def main():
     import paper_2001_05585_b200 as T
     from paper_2001_05585_b200 import _capi
     lib = _capi.load()
+    lib.tcr_enable_profiling_knobs()   # TCR_* profiling knobs from the environment (A/B captures)
     x = T.generate("uniform", 0, a.n, dtype="float32" if a.f32 else "float16")
     res = torch.zeros(2, dtype=torch.float32, device="cuda")
     ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
