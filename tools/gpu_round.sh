@@ -25,14 +25,17 @@ timeout 300 python tools/ordered_one.py > $OUT/ordered_one.txt 2>&1
 if [ "${NCU:-1}" = "1" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
      python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_launch_bench.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sp_async -s 3 -c 1 \
-     -o $OUT/async python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-comparators > $OUT/ncu_async.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sp_bulk -s 3 -c 1 \
-     -o $OUT/tma python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-comparators --engine 1 > $OUT/ncu_tma.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gm_nat_fast -s 1 -c 1 \
-     -o $OUT/genm_m4 python tools/ncu_one.py --m 4 --R 1 --B 128 --n 268435456 > $OUT/ncu_genm_m4.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:ordered_ -s 4 -c 4 \
-     -o $OUT/ordered python tools/ordered_one.py 16:1:1024:30 > $OUT/ncu_ordered.log 2>&1
+  # reports stay on the box (/tmp): only their raw-page exports travel back (gpurun_out <= 64 MiB)
+  cap() {  # name kernel-regex skip count command...
+    name=$1; k=$2; sk=$3; cn=$4; shift 4
+    timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:$k -s $sk -c $cn -o /tmp/$name "$@" > $OUT/ncu_$name.log 2>&1
+    ncu -i /tmp/$name.ncu-rep --page raw --csv > $OUT/$name.raw.csv 2>> $OUT/ncu_$name.log
+    ncu -i /tmp/$name.ncu-rep --page source --csv --print-source sass 2>> $OUT/ncu_$name.log | gzip > $OUT/$name.source.csv.gz
+  }
+  cap async sp_async 3 1 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-comparators
+  cap tma sp_bulk 3 1 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-comparators --engine 1
+  cap genm_m4_reg gm4_reg 1 1 python tools/ncu_one.py --m 4 --R 1 --B 128 --n 268435456
+  cap ordered ordered_ 4 4 python tools/ordered_one.py 16:1:1024:30
 fi
 timeout 600 python tools/f32_probe.py > $OUT/f32_probe.txt 2>&1
 timeout 300 python tools/timeline.py > $OUT/timeline.txt 2>&1

@@ -35,12 +35,16 @@ CAPTURE_CONFIG = {
     "genm_m2": "single_pass_m2_R1_B128_n268435456",
     "genm_m4": "single_pass_m4_R1_B128_n268435456",
     "genm_m4_r2": "single_pass_m4_R1_B128_n268435456",
+    "genm_m4_reg": "single_pass_m4_R1_B128_n268435456",
     "ordered": "ordered_walk_m16_R1_B1024_n1073741824",
 }
 
 
 def ncu_raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".raw.csv"):   # exported on the GPU box (ncu -i X --page raw --csv)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return {}, {}
@@ -81,11 +85,11 @@ def main():
                 f.write(f"{v / 1e3:12.1f} us  {100 * v / s:5.1f} %  {k}\n")
     traffic_path = os.path.join(dst, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep")):
+    for rep in sorted(f for f in os.listdir(src) if f.endswith(".ncu-rep") or f.endswith(".raw.csv")):
         vals, units = ncu_raw(os.path.join(src, rep))
         if not vals:
             continue
-        name = rep[:-8]
+        name = rep[:-8] if rep.endswith(".ncu-rep") else rep[:-8]
         with open(os.path.join(dst, f"{rnd}_ncu_{name}.txt"), "w") as f:
             f.write(f"# ncu --set full --clock-control none capture {tag}/{rep}\n")
             f.write(f"# kernel: {vals.get('Kernel Name', '?')}\n")
