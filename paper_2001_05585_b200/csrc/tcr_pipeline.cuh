@@ -284,8 +284,9 @@ __device__ __forceinline__ void finalize_last_cta(const SpParams& p, float* s_sc
 // Block stage (reference pairwise tree over W chunk results, reduction.hpp:253, :90-101) for the
 // nblk logical blocks starting at global block block0, by `nwarps` warps (w = caller's index in
 // that set): chunk results chunks[b*W + j] -> blocks[b].
-//   W <= 8: one block per LANE (the tree in registers, v[i] += v[i + len/2] over pow2(W));
-//   W > 8:  one block per warp (shfl_down offsets pow2(W)/2 .. 1 pair the same operands).
+//   W <= 16: one block per LANE (the tree in registers, v[i] += v[i + len/2] over pow2(W));
+//   W > 16:  32 blocks per warp pass (transpose-reduce), or one block per warp (shfl_down offsets
+//            pow2(W)/2 .. 1 pair the same operands).
 __device__ __forceinline__ void publish_block(const SpParams& p, uint64_t gb, float x) {
     if (gb < p.n_blocks) {
         if (p.block_partials) p.block_partials[gb] = x;
@@ -293,11 +294,17 @@ __device__ __forceinline__ void publish_block(const SpParams& p, uint64_t gb, fl
     }
 }
 
-template <int PW>   // pow2(W) <= 8
+template <int PW>   // pow2(W) <= 16
 __device__ __forceinline__ float lane_block_tree(const float* chunks, uint32_t W, uint32_t b) {
     float v[PW];
     const float* src = chunks + b * W;
-    if (W == uint32_t(PW) && PW == 8) {
+    if (W == uint32_t(PW) && PW == 16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 a = reinterpret_cast<const float4*>(src)[q];
+            v[(4 * q) % PW] = a.x; v[(4 * q + 1) % PW] = a.y; v[(4 * q + 2) % PW] = a.z; v[(4 * q + 3) % PW] = a.w;
+        }
+    } else if (W == uint32_t(PW) && PW == 8) {
         const float4 a = reinterpret_cast<const float4*>(src)[0], c = reinterpret_cast<const float4*>(src)[1];
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
         v[4 % PW] = c.x; v[5 % PW] = c.y; v[6 % PW] = c.z; v[7 % PW] = c.w;
@@ -322,8 +329,9 @@ __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t b
                                                    const float* chunks, float* blocks, uint32_t w, uint32_t nwarps) {
     const uint32_t W = p.W;
     const unsigned lane = lane_id();
-    if (W <= 8) {
-        // the W dispatch hoisted out of the block loop (one loop per tree width)
+    if (W <= 16) {
+        // the W dispatch hoisted out of the block loop (one loop per tree width); W in 9..16
+        // (B = 512: one block per lane, 4 vector loads) measured faster than a warp per block
         auto run = [&](auto pw) {
             constexpr int PW = decltype(pw)::value;
             for (uint32_t b = w * 32u + lane; b < nblk; b += nwarps * 32u) {
@@ -335,7 +343,8 @@ __device__ __forceinline__ void range_trees_blocks(const SpParams& p, uint64_t b
         if (W == 1) run(std::integral_constant<int, 1>{});
         else if (W == 2) run(std::integral_constant<int, 2>{});
         else if (W <= 4) run(std::integral_constant<int, 4>{});
-        else run(std::integral_constant<int, 8>{});
+        else if (W <= 8) run(std::integral_constant<int, 8>{});
+        else run(std::integral_constant<int, 16>{});
         return;
     }
     uint32_t P = 1;
