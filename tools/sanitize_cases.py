@@ -27,7 +27,7 @@ def main():
     for eng in (T.Engine.mma_sync_async, T.Engine.mma_sync, T.Engine.mma_sync_regs, T.Engine.tcgen05):
         for R, B in ((1, 1024), (3, 96), (8, 32)):
             cases.append(("single_pass", dict(m=16, R=R, B=B, engine=eng)))
-    for m, R, B in ((2, 1, 128), (2, 3, 64), (4, 1, 128), (4, 5, 32), (8, 1, 128), (8, 3, 32), (32, 1, 128),
+    for m, R, B in ((2, 1, 128), (2, 3, 64), (4, 1, 128), (4, 1, 64), (4, 1, 1024), (4, 5, 32), (8, 1, 128), (8, 3, 32), (32, 1, 128),
                     (128, 1, 32), (256, 1, 32), (1024, 1, 32), (4096, 1, 32)):
         cases.append(("single_pass", dict(m=m, R=R, B=B)))
     for fin in (T.Finalize.ordered, T.Finalize.atomic):
