@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=7)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--dist", default="uniform", help="input distribution (generator seed 0 uniform, else seed 1)")
     ap.add_argument("specs", nargs="+")
     a = ap.parse_args()
     import torch
@@ -53,7 +54,7 @@ def main():
     dev = torch.device("cuda", 0)
     st = torch.cuda.current_stream(dev)
     sp = C.c_void_p(st.cuda_stream)
-    x = T.generate("uniform", 0, a.n, device=dev)
+    x = T.generate(a.dist, 0 if a.dist == "uniform" else 1, a.n, device=dev)
     res = torch.zeros(1, dtype=torch.float32, device=dev)
     ovf = torch.zeros(1, dtype=torch.int32, device=dev)
     xp, rp, op = C.c_void_p(x.data_ptr()), C.c_void_p(res.data_ptr()), C.c_void_p(ovf.data_ptr())
