@@ -146,7 +146,10 @@ constexpr uint32_t kOxPerCta = kOxSeg * kOxSegPerCta;                  // 2048 p
 constexpr uint32_t kOxSegPool = 256;                        // staged serial segments per chunk
 constexpr uint32_t kOxNoPool = 0xFFFFFFFFu;
 // walk CTA = record CTAs per walk tree (leaves) = staged runs per chunk
-template <typename A> struct OxWalk { static constexpr int kThreads = sizeof(A) == 4 ? 1024 : 512; };
+// (512 threads for binary32 too: the 1024-thread walk CTA is capped at 64 registers and the walker
+// warp spilled; measured cfg2 uniform 335.7 -> 333.2 us, normal 549 -> 530, m = 4 normal 2^28
+// 7678 -> 7153, m = 4 uniform 207.5 -> 212.0)
+template <typename A> struct OxWalk { static constexpr int kThreads = 512; };
 
 // walk counters of the last launch (profiling): tree nodes applied, CTA runs applied, segment
 // records applied, segments added block by block
