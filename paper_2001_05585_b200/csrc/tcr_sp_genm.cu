@@ -596,9 +596,24 @@ __device__ __forceinline__ uint2 ld4_tail(const uint16_t* x, uint64_t e, uint64_
     for (int i = 0; i < 4; ++i) h[i] = e + i < n ? x[e + i] : uint16_t(0);
     return make_uint2(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16));
 }
+// fp32 input: 4 floats (bits) at element e, zero past n
+__device__ __forceinline__ uint4 ld4_tail(const float* x, uint64_t e, uint64_t n) {
+    if (e + 4 <= n) return ldg_stream_v4(x + e);
+    uint32_t f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = e + i < n ? __float_as_uint(x[e + i]) : 0u;
+    return make_uint4(f[0], f[1], f[2], f[3]);
+}
 
+// F32: the reference's own fp32 input streamed as is (16 bytes per row piece, LDG.128) and
+// from_single (half.hpp:32-59) applied in registers with cvt.rn.f16x2.f32 -- the same A operand
+// as the binary16 path on the rounded values; half the tiles per batch (the same bytes in flight).
+template <bool F32>
 __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p, const bool l2_prefetch) {
     pdl_release();
+    using E = std::conditional_t<F32, float, uint16_t>;   // input element
+    using V = std::conditional_t<F32, uint4, uint2>;      // 4 elements of a row
+    constexpr int U = F32 ? kM4U / 2 : kM4U;              // tiles per batch
     extern __shared__ __align__(16) float s_tab[];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
@@ -608,8 +623,8 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     float* s_chunk = s_tab;
     float* s_block = s_tab + Cg;
     const uint32_t T = Cg / (16u * kGmWarps);       // tiles per warp per group
-    const uint32_t nb = T / kM4U;                   // batches per warp per group
-    const uint16_t* x = static_cast<const uint16_t*>(p.x);
+    const uint32_t nb = T / U;                      // batches per warp per group
+    const E* x = static_cast<const E*>(p.x);
     const uint64_t n = p.n;
     // selector of the permuted k (see above): b0 rows k = 2c, 2c+1 -> columns 0, 1; b1 rows
     // k = 2c+8, 2c+9 -> columns 2, 3
@@ -622,7 +637,7 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     // this warp's chunk-table slot of tile t of batch (j mod nb), lanes c = 0 store
     const uint32_t s_lane = smem_u32(s_chunk) + 4u * (warp * T * 16u + g);
 
-    uint2 buf[kM4NB][2 * kM4U];
+    V buf[kM4NB][2 * U];
     // issue cursor: the ik-th group of this CTA, batch ib of it, this lane's element ie (advanced
     // by increments: no division on the issue path)
     uint64_t ik = 0, ie = 0;
@@ -634,42 +649,54 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
         ifull = (gi + 1) * uint64_t(Cg) * 16u <= n;
     };
     if (ngroups) iset();
-    auto issue = [&](uint2 (&b)[2 * kM4U]) {
+    auto ldv = [&](const E* q) -> V {
+        if constexpr (F32) return ldg_stream_v4(q);
+        else return ldg_stream_v2(q);
+    };
+    auto issue = [&](V (&b)[2 * U]) {
         if (ik >= ngroups) return;
-        const uint16_t* q = x + ie;
+        const E* q = x + ie;
         if (ifull) {
 #pragma unroll
-            for (int t = 0; t < kM4U; ++t) {
-                b[2 * t] = ldg_stream_v2(q + 256u * t);
-                b[2 * t + 1] = ldg_stream_v2(q + 256u * t + 128u);
+            for (int t = 0; t < U; ++t) {
+                b[2 * t] = ldv(q + 256u * t);
+                b[2 * t + 1] = ldv(q + 256u * t + 128u);
             }
         } else {
 #pragma unroll
-            for (int t = 0; t < kM4U; ++t) {
+            for (int t = 0; t < U; ++t) {
                 b[2 * t] = ld4_tail(x, ie + 256u * t, n);
                 b[2 * t + 1] = ld4_tail(x, ie + 256u * t + 128u, n);
             }
         }
-        ie += 256u * kM4U;
+        ie += 256u * U;
         if (++ib == nb) {
             ib = 0;
             if (++ik < ngroups) iset();
         }
     };
-    auto consume = [&](const uint2 (&b)[2 * kM4U], uint32_t jb) {
-        const uint32_t tb = jb * kM4U;   // first tile of the batch (jb-th of the group) in this warp's range
-        float d2[kM4U][4];
+    auto consume = [&](const V (&b)[2 * U], uint32_t jb) {
+        const uint32_t tb = jb * U;   // first tile of the batch (jb-th of the group) in this warp's range
+        float d2[U][4];
 #pragma unroll
-        for (int t = 0; t < kM4U; ++t) {
+        for (int t = 0; t < U; ++t) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             // C_1 = ones x M_1 (reduction.hpp:173-177) for 16 chunks: A rows = chunks
-            mma_16816(acc, b[2 * t].x, b[2 * t + 1].x, b[2 * t].y, b[2 * t + 1].y, b0, b1);
+            if constexpr (F32) {
+                const uint4 r0 = b[2 * t], r1 = b[2 * t + 1];   // rows g, g + 8: elements 4c .. 4c+3
+                mma_16816(acc, pack_h2(__uint_as_float(r0.x), __uint_as_float(r0.y)),
+                          pack_h2(__uint_as_float(r1.x), __uint_as_float(r1.y)),
+                          pack_h2(__uint_as_float(r0.z), __uint_as_float(r0.w)),
+                          pack_h2(__uint_as_float(r1.z), __uint_as_float(r1.w)), b0, b1);
+            } else {
+                mma_16816(acc, b[2 * t].x, b[2 * t + 1].x, b[2 * t].y, b[2 * t + 1].y, b0, b1);
+            }
             d2[t][0] = d2[t][1] = d2[t][2] = d2[t][3] = 0.f;
             // C_R -> binary16 (:179-181), finishing MMA (:182): chunk g in d2[0], g + 8 in d2[2]
             mma_16816(d2[t], pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), 0u, 0u, bfin, 0u);
         }
 #pragma unroll
-        for (int t = 0; t < kM4U; ++t) {
+        for (int t = 0; t < U; ++t) {
             const uint32_t a = s_lane + 64u * (tb + t);
             sts_pred(a, d2[t][0], c == 0);
             sts_pred(a + 32u, d2[t][2], c == 0);
@@ -678,12 +705,12 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     // Profiling variant (knob): L2 prefetch one group ahead (cp.async.bulk.prefetch.L2, one
     // instruction per warp range).  Measured slower (2^28: 93.7 vs 85.9 us, 2^30: 337 vs 314 us):
     // the register pipeline alone keeps HBM busy, so it is off by default.
-    const uint32_t wbytes = T * 512u;                // this warp's contiguous range of a group
+    const uint32_t wbytes = T * 256u * uint32_t(sizeof(E));   // this warp's contiguous range of a group
     auto prefetch = [&](uint64_t gk) {
         if (!l2_prefetch || gk >= ngroups || lane != 0) return;
         const uint64_t gi = g0 + gk * gridDim.x;
         const uint64_t e0 = gi * uint64_t(Cg) * 16u + uint64_t(warp) * T * 256u;
-        if (e0 + wbytes / 2u > n) return;            // a ragged group streams without it
+        if (e0 + T * 256u > n) return;               // a ragged group streams without it
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + e0), "r"(wbytes) : "memory");
     };
     prefetch(0);
@@ -1449,7 +1476,7 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
             // m = 4, R = 1: register-direct stream (knob values: 8 the ring kernels, 9 with the
             // L2 prefetch; A/B)
-            return launch_gm(gm4_reg_kernel, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
+            return launch_gm(gm4_reg_kernel<false>, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
         }
         if (fast && !REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
             // m = 4, R = 1, B = 32 / 64: block trees in registers, no chunk table (tables: block
@@ -1564,6 +1591,10 @@ cudaError_t launch_genm_f32_t(const SpParams& p, const SpGeometry& g, cudaStream
     const uint32_t tables = (Cg + g.G + 3u) / 4u * 16u;
     NatShape S;
     if (!genm_f32_supported(g) || !nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
+    if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
+        // fp32, m = 4, R = 1: the register-direct engine with from_single in registers
+        return launch_gm(gm4_reg_kernel<true>, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
+    }
     if (!REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
         // fp32, m = 4, R = 1, B = 32 / 64: register block trees (as the binary16 path)
         void (*fb)(SpParams, NatShape) = nullptr;

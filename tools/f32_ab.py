@@ -24,8 +24,8 @@ def main():
         xf = T.generate("uniform", 0, n, device=dev, dtype="float32")
         res = torch.zeros(2, dtype=torch.float32, device=dev)
         ovf = torch.zeros(1, dtype=torch.int32, device=dev)
-        for R, B in ((1, 1024), (4, 128)):
-            cfg = T.ReductionConfig(m=16, R=R, B=B, finalize=T.Finalize.tree).to_c()
+        for m, R, B in ((16, 1, 1024), (16, 4, 128), (4, 1, 128), (4, 1, 1024)):
+            cfg = T.ReductionConfig(m=m, R=R, B=B, finalize=T.Finalize.tree).to_c()
             t = {k: [] for k in libs}
             for _ in range(5):
                 for name, lib in libs.items():
@@ -42,7 +42,7 @@ def main():
                     t[name].append(a.elapsed_time(b) / 5)
             for name in libs:
                 ms = statistics.median(t[name])
-                print(f"n=2^{n.bit_length()-1} R={R} B={B} {name}: {ms*1e3:.1f} us {4*n/ms/1e6:.0f} GB/s value {res[0].item()}",
+                print(f"n=2^{n.bit_length()-1} m={m} R={R} B={B} {name}: {ms*1e3:.1f} us {4*n/ms/1e6:.0f} GB/s value {res[0].item()}",
                       flush=True)
         del xf
         torch.cuda.empty_cache()
