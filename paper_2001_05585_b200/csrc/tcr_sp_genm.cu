@@ -608,8 +608,15 @@ __device__ __forceinline__ uint4 ld4_tail(const float* x, uint64_t e, uint64_t n
 // F32: the reference's own fp32 input streamed as is (16 bytes per row piece, LDG.128) and
 // from_single (half.hpp:32-59) applied in registers with cvt.rn.f16x2.f32 -- the same A operand
 // as the binary16 path on the rounded values; half the tiles per batch (the same bytes in flight).
-template <bool F32>
+// RTREE: the block and group trees in registers instead of through the chunk table (for small
+// blocks, whose shared-memory epilogue dominates): after the finishing MMA, chunk k of a tile sits
+// in lane 4 (k mod 8) (k < 8: d2[0], else d2[2]); the reference's block tree (v[i] += v[i + len/2],
+// reduction.hpp:90-101) pairs lanes 2 len apart, the blocks' adjacent group tree continues across
+// the tile, the batch, and the warp's contiguous range of tiles; one barrier per group combines
+// the 8 warps.  The same operand pairs as the shared-memory path: bit-identical partials.
+template <bool F32, int WT = 0>   // WT > 0: RTREE with compile-time W = WT
 __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p, const bool l2_prefetch) {
+    constexpr bool RTREE = WT > 0;
     pdl_release();
     using E = std::conditional_t<F32, float, uint16_t>;   // input element
     using V = std::conditional_t<F32, uint4, uint2>;      // 4 elements of a row
@@ -675,7 +682,9 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
             if (++ik < ngroups) iset();
         }
     };
-    auto consume = [&](const V (&b)[2 * U], uint32_t jb) {
+    const uint32_t W = RTREE ? uint32_t(WT) : p.W;
+    uint64_t gblk0 = 0;   // RTREE: global block index of this warp's first block in the current group
+    auto consume = [&](const V (&b)[2 * U], uint32_t jb) -> float {
         const uint32_t tb = jb * U;   // first tile of the batch (jb-th of the group) in this warp's range
         float d2[U][4];
 #pragma unroll
@@ -695,11 +704,55 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
             // C_R -> binary16 (:179-181), finishing MMA (:182): chunk g in d2[0], g + 8 in d2[2]
             mma_16816(d2[t], pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), 0u, 0u, bfin, 0u);
         }
+        if constexpr (RTREE) {
+            float tv[U];
 #pragma unroll
-        for (int t = 0; t < U; ++t) {
-            const uint32_t a = s_lane + 64u * (tb + t);
-            sts_pred(a, d2[t][0], c == 0);
-            sts_pred(a + 32u, d2[t][2], c == 0);
+            for (int t = 0; t < U; ++t) {
+                float x0 = d2[t][0], x2 = d2[t][2];
+                // block trees (W = 1, 2, 4, 8, 16 chunks)
+                if constexpr (WT == 16) {
+                    x0 = x0 + x2;
+#pragma unroll
+                    for (uint32_t len = 8; len > 1; len >>= 1) x0 += __shfl_down_sync(kFull, x0, 2 * len);
+                } else {
+#pragma unroll
+                    for (uint32_t len = WT; len > 1; len >>= 1) {
+                        const float t0 = __shfl_down_sync(kFull, x0, 2 * len), t2 = __shfl_down_sync(kFull, x2, 2 * len);
+                        x0 += t0;
+                        x2 += t2;
+                    }
+                }
+                if (p.block_partials || p.finalize == kFinAtomic) {
+                    // block i of the tile: x0 of lane 4 W i (i < 8 / W), x2 of lane 4 W (i - 8 / W)
+                    const uint64_t bt = gblk0 + uint64_t(tb + t) * (16u / W);
+                    if (c == 0 && g % W == 0) {
+                        publish_block(p, bt + g / W, x0);
+                        if constexpr (WT < 16) publish_block(p, bt + 8u / W + g / W, x2);
+                    }
+                }
+                // the tile's blocks, adjacent tree (lane 0)
+                if constexpr (WT < 16) {
+#pragma unroll
+                    for (uint32_t off = 4 * WT; off < 32; off <<= 1) {
+                        const float t0 = __shfl_down_sync(kFull, x0, off), t2 = __shfl_down_sync(kFull, x2, off);
+                        x0 += t0;
+                        x2 += t2;
+                    }
+                    x0 = x0 + x2;
+                }
+                tv[t] = x0;
+            }
+            // the batch's tiles, adjacent (U = 2 or 4)
+            if constexpr (U == 4) return (tv[0] + tv[1]) + (tv[2 % U] + tv[3 % U]);
+            else return tv[0] + tv[1 % U];
+        } else {
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                const uint32_t a = s_lane + 64u * (tb + t);
+                sts_pred(a, d2[t][0], c == 0);
+                sts_pred(a + 32u, d2[t][2], c == 0);
+            }
+            return 0.f;
         }
     };
     // Profiling variant (knob): L2 prefetch one group ahead (cp.async.bulk.prefetch.L2, one
@@ -717,27 +770,50 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
 #pragma unroll
     for (int s = 0; s < kM4NB - 1; ++s) issue(buf[s]);
     // nb is a multiple of NB (gm4_reg_ok): buffer s always holds a batch j = s mod NB
+    __shared__ float s_wv[2][kGmWarps];   // RTREE: warp subtrees, double-buffered by group parity
     for (uint64_t gk = 0; gk < ngroups; ++gk) {
         prefetch(gk + 1);
+        const uint64_t gi = g0 + gk * gridDim.x;
+        gblk0 = gi * p.G + uint64_t(warp) * (T * 16u / W);
+        float wacc = 0.f;
         for (uint32_t jj = 0; jj < nb; jj += kM4NB) {
+            float bv[kM4NB];
 #pragma unroll
             for (int s = 0; s < kM4NB; ++s) {
                 // refill the buffer consumed one step ago, then consume buffer s
                 issue(buf[(s + kM4NB - 1) % kM4NB]);
-                consume(buf[s], jj + s);
+                bv[s] = consume(buf[s], jj + s);
+            }
+            if constexpr (RTREE) {
+                static_assert(kM4NB == 4, "adjacent tree over 4 batches");
+                const float v = (bv[0] + bv[1]) + (bv[2] + bv[3]);
+                wacc = jj == 0 ? v : wacc + v;   // nb / NB is 1 or 2 (Cg = 2048 or 4096)
             }
         }
-        // the group's chunk table is complete: block trees (:90-101, :253), group tree
-        group_epilogue<false>(p, g0 + gk * gridDim.x, s_chunk, s_block, 4u, false);
+        if constexpr (RTREE) {
+            // the group tree: the 8 warps' adjacent subtrees
+            if (lane == 0) s_wv[gk & 1][warp] = wacc;
+            __syncthreads();
+            if (threadIdx.x == 0 && p.group_partials) {
+                const float* w = s_wv[gk & 1];
+                const float v = ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+                p.group_partials[gi] = v;
+                if (!isfinite(v)) atomicOr(p.overflow, 1u);   // the overflow note, as group_tree_cta
+            }
+        } else {
+            // the group's chunk table is complete: block trees (:90-101, :253), group tree
+            group_epilogue<false>(p, gi, s_chunk, s_block, 4u, false);
+        }
     }
     __syncthreads();
     finalize_last_cta(p, s_scratch, &s_last, kGmThreads);
 }
 
 // m = 4, R = 1 register-direct engine eligibility: whole batches per warp per group
-// (W >= 2: for B = 32 the register block-tree ring kernel measured faster, 4.80 vs 4.59 TB/s at 2^28)
+// (B = 32, W = 1: the RTREE instantiation -- trees in registers; the chunk-table epilogue of its
+// 4096-block groups made the shared-memory form slower than the ring kernel, 4.59 vs 4.80 TB/s)
 __host__ __device__ inline bool gm4_reg_ok(uint32_t m, uint32_t R, uint32_t W, uint32_t Cg, bool gm4_all_w = false) {
-    return m == 4 && R == 1 && (W >= 2 || gm4_all_w) && Cg % (16u * kGmWarps * kM4U * kM4NB) == 0;
+    return m == 4 && R == 1 && Cg % (16u * kGmWarps * kM4U * kM4NB) == 0 && (W >= 1 || gm4_all_w);
 }
 
 // ================================================================ transposed tiles, m = 8 or 16*S
@@ -1476,6 +1552,9 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
             // m = 4, R = 1: register-direct stream (knob values: 8 the ring kernels, 9 with the
             // L2 prefetch; A/B)
+            if (g.W == 1) return launch_gm(gm4_reg_kernel<false, 1>, 16u, groups, p, knobs().gm_nat_alt == 9, s);
+            if (g.W == 4 && knobs().gm_nat_alt == 11)   // profiling A/B
+                return launch_gm(gm4_reg_kernel<false, 4>, 16u, groups, p, false, s);
             return launch_gm(gm4_reg_kernel<false>, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
         }
         if (fast && !REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
@@ -1593,6 +1672,7 @@ cudaError_t launch_genm_f32_t(const SpParams& p, const SpGeometry& g, cudaStream
     if (!genm_f32_supported(g) || !nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
     if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
         // fp32, m = 4, R = 1: the register-direct engine with from_single in registers
+        if (g.W == 1) return launch_gm(gm4_reg_kernel<true, 1>, 16u, groups, p, knobs().gm_nat_alt == 9, s);
         return launch_gm(gm4_reg_kernel<true>, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
     }
     if (!REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {

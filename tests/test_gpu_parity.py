@@ -1061,12 +1061,12 @@ def test_ordered_parallel_real_inputs(oracle, dist, seed, lgn, m, R, B):
 
 # ------------------------------------------------- m = 4, R = 1 register-direct engine (gm4_reg_kernel)
 
-@pytest.mark.parametrize("B", [64, 128, 256, 1024])
+@pytest.mark.parametrize("B", [32, 64, 128, 256, 1024])
 @pytest.mark.parametrize("n", [(1 << 22) + 4093, (1 << 24), 65536 * 3 + 6, 4097])
 @pytest.mark.parametrize("dist", ["uniform", "normal"])
 def test_m4_register_engine_equals_ring_kernel(oracle, B, n, dist):
-    """The register-direct m = 4 R = 1 engine (LDG.64 straight into the A fragments, permuted k)
-    against the cp.async ring kernel it replaced (profiling knob TCR_GM_NAT_ALT=8): block results
+    """The register-direct m = 4 R = 1 engine (LDG.64 straight into the A fragments, permuted k;
+    B = 32: block and group trees in registers) against the cp.async ring kernel it replaced (profiling knob TCR_GM_NAT_ALT=8): block results
     bit for bit -- ragged tails included (the last group is partial, n mod 4 != 0) -- and both
     finalize orders; against the reference restatement within the bars of this file."""
     from paper_2001_05585_b200 import _capi
