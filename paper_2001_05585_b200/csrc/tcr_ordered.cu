@@ -459,7 +459,15 @@ __global__ void __launch_bounds__(kOrdThreads, 4) ordered_records_kernel(const O
     if (tid == 0) atomicMin(&g_ord_times[0], gtimer());
     float v[kOxSegPerWarp];
 #pragma unroll
-    for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = ox_load(P, base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
+    for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = 0.0f;
+    if (!P.order && !P.halves && base + kOxPerCta <= P.nb) {
+        // ascending block results, a whole window: plain coalesced L2 loads, all in flight
+#pragma unroll
+        for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = __ldcg(P.blocks + base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
+    } else {
+#pragma unroll
+        for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = ox_load(P, base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
+    }
 #pragma unroll
     for (uint32_t i = 0; i < kOxSegPerWarp; ++i) {
         double d = double(v[i]);
