@@ -402,6 +402,17 @@ __global__ void __launch_bounds__(kOrdThreads) ordered_agg_kernel(const OxParams
         for (uint32_t i = 0; i < NV; ++i) q[i] = __ldcg(v + i * kOrdThreads);
 #pragma unroll
         for (uint32_t i = 0; i < NV; ++i) d += (double(q[i].x) + double(q[i].y)) + (double(q[i].z) + double(q[i].w));
+    } else if (P.order && !P.halves && base + kOxPerCta <= P.nb) {
+        // seeded permutation, a whole window: the order indices, then the gathers, all in flight
+        constexpr uint32_t NP = kOxPerCta / kOrdThreads;
+        uint32_t ix[NP];
+#pragma unroll
+        for (uint32_t i = 0; i < NP; ++i) ix[i] = __ldg(P.order + base + i * kOrdThreads + threadIdx.x);
+        float q[NP];
+#pragma unroll
+        for (uint32_t i = 0; i < NP; ++i) q[i] = __ldcg(P.blocks + ix[i]);
+#pragma unroll
+        for (uint32_t i = 0; i < NP; ++i) d += double(q[i]);
     } else {
 #pragma unroll
         for (uint32_t i = 0; i < kOxPerCta / kOrdThreads; ++i) d += double(ox_load(P, base + i * kOrdThreads + threadIdx.x));
@@ -464,6 +475,13 @@ __global__ void __launch_bounds__(kOrdThreads, 4) ordered_records_kernel(const O
         // ascending block results, a whole window: plain coalesced L2 loads, all in flight
 #pragma unroll
         for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = __ldcg(P.blocks + base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
+    } else if (P.order && !P.halves && base + kOxPerCta <= P.nb) {
+        // seeded permutation, a whole window: all 8 order indices, then all 8 gathers in flight
+        uint32_t ix[kOxSegPerWarp];
+#pragma unroll
+        for (uint32_t i = 0; i < kOxSegPerWarp; ++i) ix[i] = __ldg(P.order + base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
+#pragma unroll
+        for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = __ldcg(P.blocks + ix[i]);
     } else {
 #pragma unroll
         for (uint32_t i = 0; i < kOxSegPerWarp; ++i) v[i] = ox_load(P, base + (warp * kOxSegPerWarp + i) * kOxSeg + lane);
