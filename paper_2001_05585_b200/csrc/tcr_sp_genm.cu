@@ -614,13 +614,16 @@ __device__ __forceinline__ uint4 ld4_tail(const float* x, uint64_t e, uint64_t n
 // reduction.hpp:90-101) pairs lanes 2 len apart, the blocks' adjacent group tree continues across
 // the tile, the batch, and the warp's contiguous range of tiles; one barrier per group combines
 // the 8 warps.  The same operand pairs as the shared-memory path: bit-identical partials.
-template <bool F32, int WT = 0>   // WT > 0: RTREE with compile-time W = WT
+template <bool F32, int WT = 0, int RC = 1>   // WT > 0: RTREE with compile-time W = WT; RC = R
 __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p, const bool l2_prefetch) {
     constexpr bool RTREE = WT > 0;
+    // R = RC rows of 16 elements per chunk: a tile is 16 chunks = RC HMMAs chained through the
+    // accumulator (C_r = ones x M_r + C_{r-1}, reduction.hpp:173-177), row r of every chunk per MMA
     pdl_release();
     using E = std::conditional_t<F32, float, uint16_t>;   // input element
     using V = std::conditional_t<F32, uint4, uint2>;      // 4 elements of a row
-    constexpr int U = F32 ? kM4U / 2 : kM4U;              // tiles per batch
+    constexpr int U = (F32 ? kM4U / 2 : kM4U) / RC;       // tiles per batch (the same bytes for every R)
+    static_assert(U >= 1, "R too large for the register batches");
     extern __shared__ __align__(16) float s_tab[];
     __shared__ float s_scratch[32];
     __shared__ int s_last;
@@ -639,12 +642,13 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     const uint32_t bfin = sel2((2 * c) / 4 == g, (2 * c + 1) / 4 == g);
     const uint64_t g0 = p.group_begin + blockIdx.x;
     const uint64_t ngroups = p.group_end > g0 ? (p.group_end - g0 + gridDim.x - 1) / gridDim.x : 0;
-    // lane's element offset inside a tile: row g, elements 4c .. 4c+3 (row g + 8: +128)
-    const uint32_t lane_el = 16u * g + 4u * c;
+    // lane's element offset inside a tile: chunk g row 0, elements 4c .. 4c+3 (chunk g + 8:
+    // +128 RC; row r: +16 r)
+    const uint32_t lane_el = 16u * RC * g + 4u * c;
     // this warp's chunk-table slot of tile t of batch (j mod nb), lanes c = 0 store
     const uint32_t s_lane = smem_u32(s_chunk) + 4u * (warp * T * 16u + g);
 
-    V buf[kM4NB][2 * U];
+    V buf[kM4NB][2 * U * RC];
     // issue cursor: the ik-th group of this CTA, batch ib of it, this lane's element ie (advanced
     // by increments: no division on the issue path)
     uint64_t ik = 0, ie = 0;
@@ -652,31 +656,35 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     bool ifull = false;
     auto iset = [&]() {
         const uint64_t gi = g0 + ik * gridDim.x;
-        ie = gi * uint64_t(Cg) * 16u + uint64_t(warp * T) * 256u + lane_el;
-        ifull = (gi + 1) * uint64_t(Cg) * 16u <= n;
+        ie = gi * uint64_t(Cg) * 16u * RC + uint64_t(warp * T) * 256u * RC + lane_el;
+        ifull = (gi + 1) * uint64_t(Cg) * 16u * RC <= n;
     };
     if (ngroups) iset();
     auto ldv = [&](const E* q) -> V {
         if constexpr (F32) return ldg_stream_v4(q);
         else return ldg_stream_v2(q);
     };
-    auto issue = [&](V (&b)[2 * U]) {
+    auto issue = [&](V (&b)[2 * U * RC]) {
         if (ik >= ngroups) return;
         const E* q = x + ie;
         if (ifull) {
 #pragma unroll
-            for (int t = 0; t < U; ++t) {
-                b[2 * t] = ldv(q + 256u * t);
-                b[2 * t + 1] = ldv(q + 256u * t + 128u);
-            }
+            for (int t = 0; t < U; ++t)
+#pragma unroll
+                for (int r = 0; r < RC; ++r) {
+                    b[2 * (t * RC + r)] = ldv(q + 256u * RC * t + 16u * r);
+                    b[2 * (t * RC + r) + 1] = ldv(q + 256u * RC * t + 16u * r + 128u * RC);
+                }
         } else {
 #pragma unroll
-            for (int t = 0; t < U; ++t) {
-                b[2 * t] = ld4_tail(x, ie + 256u * t, n);
-                b[2 * t + 1] = ld4_tail(x, ie + 256u * t + 128u, n);
-            }
+            for (int t = 0; t < U; ++t)
+#pragma unroll
+                for (int r = 0; r < RC; ++r) {
+                    b[2 * (t * RC + r)] = ld4_tail(x, ie + 256u * RC * t + 16u * r, n);
+                    b[2 * (t * RC + r) + 1] = ld4_tail(x, ie + 256u * RC * t + 16u * r + 128u * RC, n);
+                }
         }
-        ie += 256u * U;
+        ie += 256u * RC * U;
         if (++ib == nb) {
             ib = 0;
             if (++ik < ngroups) iset();
@@ -684,21 +692,25 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     };
     const uint32_t W = RTREE ? uint32_t(WT) : p.W;
     uint64_t gblk0 = 0;   // RTREE: global block index of this warp's first block in the current group
-    auto consume = [&](const V (&b)[2 * U], uint32_t jb) -> float {
+    auto consume = [&](const V (&b)[2 * U * RC], uint32_t jb) -> float {
         const uint32_t tb = jb * U;   // first tile of the batch (jb-th of the group) in this warp's range
         float d2[U][4];
 #pragma unroll
         for (int t = 0; t < U; ++t) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            // C_1 = ones x M_1 (reduction.hpp:173-177) for 16 chunks: A rows = chunks
-            if constexpr (F32) {
-                const uint4 r0 = b[2 * t], r1 = b[2 * t + 1];   // rows g, g + 8: elements 4c .. 4c+3
-                mma_16816(acc, pack_h2(__uint_as_float(r0.x), __uint_as_float(r0.y)),
-                          pack_h2(__uint_as_float(r1.x), __uint_as_float(r1.y)),
-                          pack_h2(__uint_as_float(r0.z), __uint_as_float(r0.w)),
-                          pack_h2(__uint_as_float(r1.z), __uint_as_float(r1.w)), b0, b1);
-            } else {
-                mma_16816(acc, b[2 * t].x, b[2 * t + 1].x, b[2 * t].y, b[2 * t + 1].y, b0, b1);
+            // C_r = ones x M_r + C_{r-1} (reduction.hpp:173-177) for 16 chunks: A rows = chunks
+#pragma unroll
+            for (int r = 0; r < RC; ++r) {
+                const int k = 2 * (t * RC + r);
+                if constexpr (F32) {
+                    const uint4 r0 = b[k], r1 = b[k + 1];   // chunks g, g + 8: elements 4c .. 4c+3 of row r
+                    mma_16816(acc, pack_h2(__uint_as_float(r0.x), __uint_as_float(r0.y)),
+                              pack_h2(__uint_as_float(r1.x), __uint_as_float(r1.y)),
+                              pack_h2(__uint_as_float(r0.z), __uint_as_float(r0.w)),
+                              pack_h2(__uint_as_float(r1.z), __uint_as_float(r1.w)), b0, b1);
+                } else {
+                    mma_16816(acc, b[k].x, b[k + 1].x, b[k].y, b[k + 1].y, b0, b1);
+                }
             }
             d2[t][0] = d2[t][1] = d2[t][2] = d2[t][3] = 0.f;
             // C_R -> binary16 (:179-181), finishing MMA (:182): chunk g in d2[0], g + 8 in d2[2]
@@ -742,9 +754,11 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
                 }
                 tv[t] = x0;
             }
-            // the batch's tiles, adjacent (U = 2 or 4)
-            if constexpr (U == 4) return (tv[0] + tv[1]) + (tv[2 % U] + tv[3 % U]);
-            else return tv[0] + tv[1 % U];
+            // the batch's tiles, adjacent (U = 1, 2 or 4)
+            static_assert(U == 1 || U == 2 || U == 4, "batch tree");
+            if constexpr (U == 4) return (tv[0] + tv[1 % U]) + (tv[2 % U] + tv[3 % U]);
+            else if constexpr (U == 2) return tv[0] + tv[1 % U];
+            else return tv[0];
         } else {
 #pragma unroll
             for (int t = 0; t < U; ++t) {
@@ -758,12 +772,12 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
     // Profiling variant (knob): L2 prefetch one group ahead (cp.async.bulk.prefetch.L2, one
     // instruction per warp range).  Measured slower (2^28: 93.7 vs 85.9 us, 2^30: 337 vs 314 us):
     // the register pipeline alone keeps HBM busy, so it is off by default.
-    const uint32_t wbytes = T * 256u * uint32_t(sizeof(E));   // this warp's contiguous range of a group
+    const uint32_t wbytes = T * 256u * RC * uint32_t(sizeof(E));   // this warp's contiguous range of a group
     auto prefetch = [&](uint64_t gk) {
         if (!l2_prefetch || gk >= ngroups || lane != 0) return;
         const uint64_t gi = g0 + gk * gridDim.x;
-        const uint64_t e0 = gi * uint64_t(Cg) * 16u + uint64_t(warp) * T * 256u;
-        if (e0 + T * 256u > n) return;               // a ragged group streams without it
+        const uint64_t e0 = gi * uint64_t(Cg) * 16u * RC + uint64_t(warp) * T * 256u * RC;
+        if (e0 + T * 256u * RC > n) return;          // a ragged group streams without it
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + e0), "r"(wbytes) : "memory");
     };
     prefetch(0);
@@ -775,7 +789,10 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
         prefetch(gk + 1);
         const uint64_t gi = g0 + gk * gridDim.x;
         gblk0 = gi * p.G + uint64_t(warp) * (T * 16u / W);
-        float wacc = 0.f;
+        // RTREE: adjacent tree over the nb / NB (a power of two) iteration values of the group:
+        // a binary counter of partial subtrees (at most 6 levels: nb <= 256)
+        float stk[8];
+        int top = 0;
         for (uint32_t jj = 0; jj < nb; jj += kM4NB) {
             float bv[kM4NB];
 #pragma unroll
@@ -786,13 +803,14 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
             }
             if constexpr (RTREE) {
                 static_assert(kM4NB == 4, "adjacent tree over 4 batches");
-                const float v = (bv[0] + bv[1]) + (bv[2] + bv[3]);
-                wacc = jj == 0 ? v : wacc + v;   // nb / NB is 1 or 2 (Cg = 2048 or 4096)
+                float v = (bv[0] + bv[1]) + (bv[2] + bv[3]);
+                for (uint32_t k = jj / kM4NB; k & 1u; k >>= 1) v = stk[--top] + v;
+                stk[top++] = v;
             }
         }
         if constexpr (RTREE) {
             // the group tree: the 8 warps' adjacent subtrees
-            if (lane == 0) s_wv[gk & 1][warp] = wacc;
+            if (lane == 0) s_wv[gk & 1][warp] = stk[0];
             __syncthreads();
             if (threadIdx.x == 0 && p.group_partials) {
                 const float* w = s_wv[gk & 1];
@@ -813,7 +831,8 @@ __global__ void __launch_bounds__(kGmThreads, 2) gm4_reg_kernel(const SpParams p
 // (B = 32, W = 1: the RTREE instantiation -- trees in registers; the chunk-table epilogue of its
 // 4096-block groups made the shared-memory form slower than the ring kernel, 4.59 vs 4.80 TB/s)
 __host__ __device__ inline bool gm4_reg_ok(uint32_t m, uint32_t R, uint32_t W, uint32_t Cg, bool gm4_all_w = false) {
-    return m == 4 && R == 1 && Cg % (16u * kGmWarps * kM4U * kM4NB) == 0 && (W >= 1 || gm4_all_w);
+    return m == 4 && (R == 1 || R == 2 || R == 4) && Cg % (16u * kGmWarps * kM4U * kM4NB) == 0 &&
+           (W >= 1 || gm4_all_w);
 }
 
 // ================================================================ transposed tiles, m = 8 or 16*S
@@ -1549,13 +1568,22 @@ cudaError_t launch_genm_t(const SpParams& p, const SpGeometry& g, cudaStream_t s
         if (!nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
         // PR <= 8 or 16: a unit of 16 periods is one contiguous stage of 512 PR bytes
         const bool fast = S.PR == S.RB && (S.PR <= 8 || S.PR == 16) && !knobs().gm_nat_generic;
-        if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
+        if (!REPAIR && g.R <= 2 && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
             // m = 4, R = 1: register-direct stream (knob values: 8 the ring kernels, 9 with the
             // L2 prefetch; A/B)
-            if (g.W == 1) return launch_gm(gm4_reg_kernel<false, 1>, 16u, groups, p, knobs().gm_nat_alt == 9, s);
+            const bool pf = knobs().gm_nat_alt == 9;
+            if (g.R == 2) {
+                if (g.W == 1) return launch_gm(gm4_reg_kernel<false, 1, 2>, 16u, groups, p, pf, s);
+                return launch_gm(gm4_reg_kernel<false, 0, 2>, tables * 1u, groups, p, pf, s);
+            }
+            if (g.R == 4) {
+                if (g.W == 1) return launch_gm(gm4_reg_kernel<false, 1, 4>, 16u, groups, p, pf, s);
+                return launch_gm(gm4_reg_kernel<false, 0, 4>, tables * 1u, groups, p, pf, s);
+            }
+            if (g.W == 1) return launch_gm(gm4_reg_kernel<false, 1>, 16u, groups, p, pf, s);
             if (g.W == 4 && knobs().gm_nat_alt == 11)   // profiling A/B
                 return launch_gm(gm4_reg_kernel<false, 4>, 16u, groups, p, false, s);
-            return launch_gm(gm4_reg_kernel<false>, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
+            return launch_gm(gm4_reg_kernel<false>, tables * 1u, groups, p, pf, s);
         }
         if (fast && !REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
             // m = 4, R = 1, B = 32 / 64: block trees in registers, no chunk table (tables: block
@@ -1670,10 +1698,15 @@ cudaError_t launch_genm_f32_t(const SpParams& p, const SpGeometry& g, cudaStream
     const uint32_t tables = (Cg + g.G + 3u) / 4u * 16u;
     NatShape S;
     if (!genm_f32_supported(g) || !nat_shape(g.m, g.R, Cg, &S)) return cudaErrorInvalidValue;
-    if (!REPAIR && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
+    if (!REPAIR && g.R <= 2 && gm4_reg_ok(g.m, g.R, g.W, Cg, knobs().gm_nat_alt == 10) && knobs().gm_nat_alt != 8) {
         // fp32, m = 4, R = 1: the register-direct engine with from_single in registers
-        if (g.W == 1) return launch_gm(gm4_reg_kernel<true, 1>, 16u, groups, p, knobs().gm_nat_alt == 9, s);
-        return launch_gm(gm4_reg_kernel<true>, tables * 1u, groups, p, knobs().gm_nat_alt == 9, s);
+        const bool pf = knobs().gm_nat_alt == 9;
+        if (g.R == 2) {
+            if (g.W == 1) return launch_gm(gm4_reg_kernel<true, 1, 2>, 16u, groups, p, pf, s);
+            return launch_gm(gm4_reg_kernel<true, 0, 2>, tables * 1u, groups, p, pf, s);
+        }
+        if (g.W == 1) return launch_gm(gm4_reg_kernel<true, 1>, 16u, groups, p, pf, s);
+        return launch_gm(gm4_reg_kernel<true>, tables * 1u, groups, p, pf, s);
     }
     if (!REPAIR && g.m == 4 && S.RB == 1 && g.W <= 2 && knobs().gm_nat_alt == 0) {
         // fp32, m = 4, R = 1, B = 32 / 64: register block trees (as the binary16 path)

@@ -1061,27 +1061,28 @@ def test_ordered_parallel_real_inputs(oracle, dist, seed, lgn, m, R, B):
 
 # ------------------------------------------------- m = 4, R = 1 register-direct engine (gm4_reg_kernel)
 
+@pytest.mark.parametrize("R", [1, 2, 4])
 @pytest.mark.parametrize("B", [32, 64, 128, 256, 1024])
 @pytest.mark.parametrize("n", [(1 << 22) + 4093, (1 << 24), 65536 * 3 + 6, 4097])
 @pytest.mark.parametrize("dist", ["uniform", "normal"])
-def test_m4_register_engine_equals_ring_kernel(oracle, B, n, dist):
-    """The register-direct m = 4 R = 1 engine (LDG.64 straight into the A fragments, permuted k;
+def test_m4_register_engine_equals_ring_kernel(oracle, R, B, n, dist):
+    """The register-direct m = 4 engine, R = 1 / 2 / 4 (LDG.64 straight into the A fragments, permuted k;
     B = 32: block and group trees in registers) against the cp.async ring kernel it replaced (profiling knob TCR_GM_NAT_ALT=8): block results
     bit for bit -- ragged tails included (the last group is partial, n mod 4 != 0) -- and both
     finalize orders; against the reference restatement within the bars of this file."""
     from paper_2001_05585_b200 import _capi
     h = oracle.generate_f16(dist, 11, n)
     xd = to_dev_f16(h)
-    cfg = T.ReductionConfig(m=4, R=1, B=B)
+    cfg = T.ReductionConfig(m=4, R=R, B=B)
     new = T.block_results(xd, cfg).cpu().numpy()
     with _capi.profiling_knobs({"TCR_GM_NAT_ALT": "8"}):
         old = T.block_results(xd, cfg).cpu().numpy()
-        olds = [T.reduce(xd, T.ReductionConfig(m=4, R=1, B=B, finalize=f)) for f in (T.Finalize.tree, T.Finalize.ordered)]
+        olds = [T.reduce(xd, T.ReductionConfig(m=4, R=R, B=B, finalize=f)) for f in (T.Finalize.tree, T.Finalize.ordered)]
     assert np.array_equal(new.view(np.uint32), old.view(np.uint32))
-    news = [T.reduce(xd, T.ReductionConfig(m=4, R=1, B=B, finalize=f)) for f in (T.Finalize.tree, T.Finalize.ordered)]
+    news = [T.reduce(xd, T.ReductionConfig(m=4, R=R, B=B, finalize=f)) for f in (T.Finalize.tree, T.Finalize.ordered)]
     for a, b in zip(news, olds):
         assert a.value == b.value and a.overflow == b.overflow
-    ref = oracle.single_pass(h, threads=8, m=4, R=1, B=B)
+    ref = oracle.single_pass(h, threads=8, m=4, R=R, B=B)
     exact, absum = oracle.exact_sum_f16(h)
     assert abs(news[1].value - ref.value) <= max(2e-5 * abs(exact), 1e-6 * absum)
     assert news[1].atomic_count == ref.atomic_count and news[1].mma_count == ref.mma_count
